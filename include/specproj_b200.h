@@ -1,0 +1,123 @@
+/*
+ * specproj_b200 — C-ABI of the B200 (sm_100a, FP64) hQDWH spectral-projector path.
+ *
+ * Drop-in boundary for the reference's hot path.  The
+ * reference has no FFI of its own: its "API" is the header-only C++ surface
+ *   ProjectorResult specproj::hqdwh(const BandedSymmetric& A, int n_min,
+ *                                   double eps, double delta)   (qdwh.hpp:196)
+ * plus HodlrMatrix (hodlr.hpp:20-48), make_tree (tree.hpp:58-60),
+ * to_dense / hodlr_trace / diagnostics (hodlr.hpp:253, 658, 679).
+ * These entry points carry exactly that information through plain pointers;
+ * the C++ shim include/specproj_b200/specproj.hpp rebuilds the reference-shaped
+ * types on top of them, and INTEGRATION.md shows the ctypes binding.
+ *
+ * Band layout (banded.hpp:19-23): bands packed diagonal-major,
+ *   bands[d*n - d*(d-1)/2 + i] = A(i+d, i),  d = 0..b,  i = 0..n-d-1.
+ * Flat HODLR layout (preorder nodes, tree.hpp:44-56):
+ *   ranks[2*nnodes] = (rank upper, rank lower), 0 for leaves;
+ *   data: per node, leaf -> size*size row-major; internal -> U_up (s1 x ku),
+ *         V_up (s2 x ku), U_lo (s2 x kl), V_lo (s1 x kl), all row-major
+ *         (the storage order of the reference's Matrix, dense.hpp:16-59).
+ */
+#ifndef SPECPROJ_B200_H
+#define SPECPROJ_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the C++ shim rethrows the reference's exception types */
+enum spg_status {
+    SPG_OK = 0,
+    SPG_NOT_POSITIVE_DEFINITE = 1, /* NotPositiveDefiniteError (dense_factor.hpp:19-21)  */
+    SPG_SINGULAR = 2,              /* SingularMatrixError      (dense_factor.hpp:23-25)  */
+    SPG_INVALID_ARGUMENT = 3,      /* std::invalid_argument (qdwh.hpp:198, tree.hpp:29-30) */
+    SPG_DOMAIN = 4,                /* std::domain_error (qdwh.hpp:28)                    */
+    SPG_RANK_CAPACITY = 5,         /* a block needed more than the compiled rank capacity */
+    SPG_CUDA_ERROR = 6,
+    SPG_NO_DEVICE = 7
+};
+
+typedef struct spg_result spg_result; /* opaque: device-resident P and U */
+
+/* per-iteration diagnostics (IterationDiag, qdwh.hpp:176-183) */
+typedef struct spg_iter_diag {
+    int k;
+    double l, c;
+    int max_rank;
+    long long memory_bytes;
+    double wall_ms;
+} spg_iter_diag;
+
+typedef struct spg_info {
+    int n, b, n_min;
+    double eps, delta;
+    int iterations;        /* ProjectorResult::iterations */
+    double alpha, l0;      /* ProjectorResult::alpha / l0 */
+    double ms_total;       /* device time of the whole projector (CUDA events) */
+    double ms_setup;       /* H2D of the bands + alpha/l0 estimates + schedule */
+    double ms_first;       /* first (QR-based) iterate */
+    double ms_multiply, ms_cholesky, ms_solve, ms_solveT, ms_axpby_sym; /* summed over iterations */
+    long long launches;    /* kernel launches issued for the projector */
+    int max_rank;          /* diagnostics(P).max_offdiag_rank */
+    long long memory_bytes;/* diagnostics(P).memory_bytes */
+    double trace;          /* hodlr_trace(P) */
+    int kcap;              /* compiled rank capacity */
+} spg_info;
+
+/* Runs the hQDWH projector on device 0 (current device).  `bands` is host
+ * memory (copied to the device inside the call).  On success *out owns the
+ * device-resident P and U.  Mirrors specproj::hqdwh (qdwh.hpp:196-241). */
+int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double delta, spg_result** out);
+
+int spg_result_info(const spg_result* r, spg_info* info);
+/* per-iteration diagnostics, `out` has room for info.iterations entries */
+int spg_result_diag(const spg_result* r, spg_iter_diag* out);
+/* which = 0: P (projector), 1: U (sign approximant).  Flat size in doubles. */
+int spg_result_flat_size(const spg_result* r, int which, long long* ndoubles);
+/* downloads into caller-owned host buffers (ranks: 2*nnodes ints) */
+int spg_result_export(const spg_result* r, int which, int* ranks, double* data);
+/* Y = H X on device for a host block X (n x m, row-major) — verification (h_apply, hodlr.hpp:277) */
+int spg_result_apply(const spg_result* r, int which, int m, const double* X, double* Y);
+void spg_result_free(spg_result* r);
+
+/* thread-local message of the last failing call */
+const char* spg_last_error(void);
+
+/* ---- host helpers (no GPU needed) ------------------------------------------ */
+/* make_tree (tree.hpp:58-60): returns nnodes; arrays may be NULL to query */
+int spg_tree(int n, int n_min, int* begin, int* size, int* left, int* right, int* depth);
+/* qdwh_params (qdwh.hpp:27-35) + l_update (38-40) */
+int spg_qdwh_params(double l, double* abc);
+double spg_l_update(double l, double a, double b, double c);
+/* Dimer-chain test input: bond i = t1 (i even) / t2 (i odd),
+ * diag = eps_dis * U(-1,1), then band perturbation s * U(-1,1) for d = 0..b,
+ * std::mt19937_64(seed) + uniform_real_distribution<double>(-1,1). */
+int spg_make_dimer_chain(int n, int b, double t1, double t2, double eps_dis, double s, unsigned long long seed,
+                         double* bands);
+/* generic random banded input (test_hodlr.cpp:19-26 convention) */
+int spg_make_random_banded(int n, int b, unsigned long long seed, double* bands);
+/* compiled capacities */
+int spg_kcap(void);
+
+/* ---- component-level entry points (parity tests of each HODLR operation) --- */
+typedef struct spg_ctx spg_ctx;
+spg_ctx* spg_ctx_create(int n, int n_min, double eps, int nslots);
+void spg_ctx_free(spg_ctx* c);
+int spg_ctx_upload(spg_ctx* c, int slot, const int* ranks, const double* data);
+int spg_ctx_flat_size(spg_ctx* c, int slot, long long* ndoubles);
+int spg_ctx_download(spg_ctx* c, int slot, int* ranks, double* data);
+/* op codes: 1 multiply(dst = a*b), 2 axpby(dst = alpha a + beta b), 3 symmetrize(dst in place),
+ *           4 cholesky(dst = chol(a)), 5 solve_upper_right(dst W = a, W = b),
+ *           6 solve_upperT_right(dst W^T = a), 7 scale_shift(dst = alpha dst + beta I),
+ *           8 from_banded(dst, bands in `bands`, b = band) */
+int spg_ctx_op(spg_ctx* c, int op, int dst, int a, int b, double alpha, double beta);
+int spg_ctx_from_banded(spg_ctx* c, int dst, int b, const double* bands);
+/* single truncate (lowrank.hpp:67-86) on device: U p x k, V s x k row-major in,
+ * outputs row-major with leading dimension k; returns kept rank via *r */
+int spg_truncate(int p, int s, int k, const double* U, const double* V, double eps, double* Uo, double* Vo, int* r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECPROJ_B200_H */

@@ -1,0 +1,107 @@
+// Shared definitions for the B200 hQDWH engine (sm_100a, FP64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace spg {
+
+// Capacities.  A stored off-diagonal factor holds at most KCAP columns; a
+// truncation input (concatenation of <= 2 groups) at most KIN_MAX = 2*KCAP.
+// KIN_MAX bounds the shared-memory footprint of the recompression kernels:
+// R (k x k) + one 128-row sub-block (128 x k) + Jacobi (2 k^2) all fit in 227 KB.
+constexpr int KCAP = 56;
+constexpr int KIN_MAX = 2 * KCAP;   // 112
+constexpr int SB = 128;             // TSQR sub-block rows
+constexpr int TS_THREADS = 512;     // threads of the TSQR / apply kernels
+
+// Device status word bits (checked once per projector).
+enum StatusBits : unsigned {
+    ST_NPD = 1u << 0,        // leaf Cholesky hit a non-positive pivot
+    ST_SINGULAR = 1u << 1,   // zero diagonal in a triangular solve / banded LU
+    ST_RANK_CAP = 1u << 2,   // truncation kept more than KCAP columns
+    ST_NONFINITE = 1u << 3,  // NaN/Inf produced
+    ST_KIN_CAP = 1u << 4,    // concatenated rank exceeded KIN_MAX
+};
+
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& s) : std::runtime_error(s) {}
+};
+
+#define SPG_CUDA(x)                                                                      \
+    do {                                                                                 \
+        cudaError_t e_ = (x);                                                            \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::spg::CudaError(std::string("CUDA error ") + cudaGetErrorString(e_) + \
+                                   " at " + __FILE__ + ":" + std::to_string(__LINE__));   \
+    } while (0)
+
+extern std::atomic<long long> g_launches;   // kernel launches issued (host-side count)
+#define SPG_LAUNCH_CHECK()            \
+    do {                              \
+        SPG_CUDA(cudaGetLastError()); \
+        ++::spg::g_launches;          \
+    } while (0)
+
+// ---------------------------------------------------------------- truncation
+// One column group of a concatenated factor pair: value contribution
+// su * U_g * V_g^T.  Factors are column-major (ld = rows stride).  The rank is
+// either read from device memory (kp != nullptr) or constant.
+struct TGroup {
+    const double* u;
+    const double* v;
+    int ldu, ldv;
+    const int* kp;
+    int kc;
+    double su;
+    const double* sup;   // optional device scalar multiplied into su
+};
+
+struct TTask {
+    int p, s;          // rows of the U side / V side
+    int ng;            // number of groups (<= 2)
+    TGroup g[2];
+    double* ou;        // output U (p x r), ld ldou
+    double* ov;        // output V (s x r), ld ldov
+    int ldou, ldov;
+    int* orank;        // output rank (may alias a group's kp)
+    int skipg;         // >= 0: if group skipg has rank 0 the task is a no-op (output untouched)
+    int seg[2];        // segment length per side (rows)
+    int nseg[2];       // segments per side
+    long long ws;      // workspace base (doubles)
+    long long wsz[2];  // workspace offsets of side 0/1 areas (relative to ws)
+};
+
+// Workspace layout of one task, per side (offsets in doubles, relative to the side base):
+//   per segment s: refl[s]  : nsub*SB*KIN_MAX  reflector tails, column-major (SB rows)
+//                  tau[s]   : nsub*KIN_MAX
+//                  R[s]     : KIN_MAX*KIN_MAX  (column-major, ld KIN_MAX)
+//   merge (nseg > 1): refl   : nsubm*SB*KIN_MAX over the stacked R rows (nseg*k rows)
+//                     tau    : nsubm*KIN_MAX
+//                     R      : KIN_MAX*KIN_MAX
+//                     Zst    : nseg*KIN_MAX*KCAP stacked coefficient blocks
+//   Z (core output, KIN_MAX x KCAP)
+// plus a task header of 8 ints at ws (k_in, r, flags) stored as doubles.
+__host__ __device__ inline long long ts_nsub(int rows) { return (rows + SB - 1) / SB; }
+__host__ __device__ inline long long ts_seg_doubles(int seglen) {
+    const long long ns = ts_nsub(seglen);
+    return ns * SB * KIN_MAX + ns * KIN_MAX + (long long)KIN_MAX * KIN_MAX;
+}
+__host__ __device__ inline long long ts_side_doubles(int rows, int seglen, int nseg) {
+    long long tot = (long long)nseg * ts_seg_doubles(seglen);
+    if (nseg > 1) {
+        const int mrows = nseg * KIN_MAX;
+        const long long ns = ts_nsub(mrows);
+        tot += ns * SB * KIN_MAX + ns * KIN_MAX + (long long)KIN_MAX * KIN_MAX + (long long)nseg * KIN_MAX * KCAP;
+    }
+    tot += (long long)KIN_MAX * KCAP;  // Z
+    (void)rows;
+    return tot;
+}
+constexpr long long TS_HEADER = 8;
+
+}  // namespace spg

@@ -1,0 +1,186 @@
+// Host-side engine of the B200 hQDWH path: tree, device HODLR storage,
+// descriptor arena, workspace and the plan builders for every HODLR operation.
+#pragma once
+
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace spg {
+
+// ---------------------------------------------------------------- tree
+// PartitionTree (tree.hpp:12-56): preorder nodes, split at ceil(size/2) while size > n_min.
+struct HTree {
+    int n = 0, nmin = 0, depth = 0;
+    std::vector<int> begin, size, left, right, level, parent, leaf_ord;
+    std::vector<int> leaves;                      // preorder ids of leaves, ascending begin
+    std::vector<std::vector<int>> internal_at;    // internal nodes per tree depth
+    HTree(int n, int nmin);
+    int nnodes() const { return (int)begin.size(); }
+    bool leaf(int i) const { return left[i] < 0; }
+    // all internal nodes / leaves of the subtree rooted at r (preorder)
+    void subtree(int r, std::vector<int>& internal, std::vector<int>& lvs) const;
+private:
+    int build(int b, int s, int lev, int par);
+};
+
+// ---------------------------------------------------------------- device arena
+// Descriptor arrays are staged on the host and uploaded once; device addresses
+// are fixed at plan time so a plan can be replayed (or graph-captured).
+class Arena {
+public:
+    explicit Arena(size_t bytes);
+    ~Arena();
+    template <class T>
+    T* push(const std::vector<T>& v) {
+        if (v.empty()) return nullptr;
+        return static_cast<T*>(push_raw(v.data(), sizeof(T) * v.size()));
+    }
+    void* push_raw(const void* src, size_t bytes);
+    void commit(cudaStream_t st);   // upload everything staged since the last commit
+    size_t used() const { return off_; }
+    void reset() { off_ = 0; committed_ = 0; }
+private:
+    char* dev_ = nullptr;
+    size_t cap_ = 0, off_ = 0, committed_ = 0;
+    std::vector<char> host_;
+};
+
+// stack allocator over one big device buffer (doubles); stream order makes reuse safe
+class Workspace {
+public:
+    explicit Workspace(size_t ndoubles);
+    ~Workspace();
+    double* base() const { return base_; }
+    long long alloc(long long n);   // returns offset (doubles)
+    double* ptr(long long off) const { return base_ + off; }
+    long long mark() const { return top_; }
+    void release(long long m) { top_ = m; }
+    long long peak() const { return peak_; }
+    size_t capacity() const { return cap_; }
+private:
+    double* base_ = nullptr;
+    size_t cap_ = 0;
+    long long top_ = 0, peak_ = 0;
+};
+
+// ---------------------------------------------------------------- device HODLR
+// Level-ordered packed storage: leaves packed column-major;
+// per tree depth t one U slab and one V slab of n x KCAP (column-major, ld n).
+// Node x at depth t: upper.U = U_t[rows of left(x)], upper.V = V_t[rows of right(x)],
+//                    lower.U = U_t[rows of right(x)], lower.V = V_t[rows of left(x)].
+struct DHodlr {
+    DHodlr() = default;
+    DHodlr(const DHodlr&) = delete;
+    DHodlr& operator=(const DHodlr&) = delete;
+    ~DHodlr() { release(); }
+    const HTree* t = nullptr;
+    double* leaves = nullptr;
+    long long* d_leaf_off = nullptr;
+    std::vector<long long> leaf_off;
+    double* U = nullptr;
+    double* V = nullptr;
+    int* rank = nullptr;
+    size_t leaf_doubles = 0, slab_doubles = 0;
+    void alloc(const HTree& tree, Arena& arena);
+    void release();
+    double* leaf(int id) const { return leaves + leaf_off[t->leaf_ord[id]]; }
+    double* slabU(int lev) const { return U + (size_t)lev * KCAP * t->n; }
+    double* slabV(int lev) const { return V + (size_t)lev * KCAP * t->n; }
+    double* upU(int id) const { return slabU(t->level[id]) + t->begin[t->left[id]]; }
+    double* upV(int id) const { return slabV(t->level[id]) + t->begin[t->right[id]]; }
+    double* loU(int id) const { return slabU(t->level[id]) + t->begin[t->right[id]]; }
+    double* loV(int id) const { return slabV(t->level[id]) + t->begin[t->left[id]]; }
+    int* rup(int id) const { return rank + 2 * id; }
+    int* rlo(int id) const { return rank + 2 * id + 1; }
+    DevHodlrView view() const { return {leaves, d_leaf_off, U, V, rank, t->n}; }
+    void zero(cudaStream_t st) const;
+};
+
+// a global-row-indexed panel: rows [0, n), KCAP columns, ld n
+struct Panel {
+    double* p = nullptr;
+    int ld = 0;
+    double* at(int row) const { return p + row; }
+};
+
+using Launch = std::function<void(cudaStream_t)>;
+
+struct Plan {
+    std::vector<Launch> launches;
+    void run(cudaStream_t st) const { for (auto& l : launches) l(st); }
+    size_t size() const { return launches.size(); }
+};
+
+// ---------------------------------------------------------------- the engine
+struct Scalars {          // device scalar block
+    double* scal;         // [0] alpha [1] l0 [2] 1/alpha
+    double* slots;        // per-iteration coefficients (see launch_iter_params)
+    double* sched;        // 4 * 64
+    int* count;
+    int* counter;
+    unsigned* status;
+};
+
+class Engine {
+public:
+    Engine(int n, int nmin, double eps, size_t ws_doubles = 0);
+    ~Engine();
+    const HTree& tree() const { return tree_; }
+    Arena& arena() { return *arena_; }
+    Workspace& ws() { return *ws_; }
+    cudaStream_t stream() const { return st_; }
+    Scalars& sc() { return sc_; }
+    double eps() const { return eps_; }
+    DevTree dtree() const { return dtree_; }
+
+    // ---- plan builders (append launches to `p`) ------------------------------
+    // truncation batch (lowrank.hpp:67-86); tasks' workspace is assigned here
+    void trunc(Plan& p, std::vector<TTask> tasks);
+    void gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>& caps);
+    // Y = H|_sub X (trans: H|_sub^T X) for each request (apply_rec/applyT_rec, hodlr.hpp:202-249)
+    struct ApplyReq { const DHodlr* H; int root; int trans; const double* X; const int* ncp; double* Y; };
+    void apply(Plan& p, const std::vector<ApplyReq>& reqs);
+    // add_lowrank_into (hodlr.hpp:400-405) of s * QU QV^T into the subtrees (batched, disjoint)
+    struct Cascade { int root; const double* QU; const double* QV; const int* qrank; double s; };
+    void cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs);
+    void hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items);
+    void copy(Plan& p, std::vector<CopyItem> items, int maxm, int maxk);
+
+    // ---- HODLR operations (hodlr.hpp) ------------------------------------------
+    void op_axpby(Plan& p, double a, const double* ap, const DHodlr& A, double b, const double* bp, const DHodlr& B,
+                  DHodlr& C);
+    void op_symmetrize(Plan& p, DHodlr& H);
+    void op_scale_shift(Plan& p, DHodlr& H, double s, const double* sp, double mu);
+    void op_copy(Plan& p, const DHodlr& src, DHodlr& dst);
+    void op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C);
+    void op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work);
+    void op_solve_upper_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work);
+    void op_solve_upperT_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work);
+
+    std::unique_ptr<DHodlr> new_hodlr();
+
+private:
+    void chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W);
+    void sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y);
+    void surt_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y);
+    double* panel(int which);   // persistent global-row panels (n x KCAP)
+
+    HTree tree_;
+    double eps_;
+    cudaStream_t st_ = nullptr;
+    std::unique_ptr<Arena> arena_;
+    std::unique_ptr<Workspace> ws_;
+    DevTree dtree_{};
+    Scalars sc_{};
+    double* scalar_mem_ = nullptr;
+    std::vector<double*> panels_;
+    double* coef_ = nullptr;    // per-node coefficient blocks (KCAP x KCAP)
+    int* iranks_ = nullptr;     // scratch ranks (4 * nnodes)
+    std::vector<std::unique_ptr<DHodlr>> owned_;
+};
+
+}  // namespace spg

@@ -1,0 +1,766 @@
+// hQDWH driver (qdwh.hpp:196-241) on sm_100a and the extern "C" boundary
+// declared in include/specproj_b200.h.
+//
+//   setup     : H2D bands, alpha = estimate_2norm, l0 = estimate_l0, the whole
+//               (a_k, b_k, c_k) schedule from l0 (one 4-byte D2H: the count)
+//   k = 0     : R of the stacked QR [sqrt(c0) A/alpha; I] (Givens, fast_qr.hpp:83-232);
+//               Q1 = (sqrt(c0) X0) R^{-1}, M = Q1 R^{-T} = Q1 Q2^T by HODLR
+//               triangular solves (replaces assemble_q + q1q2t, fast_qr.hpp:275-514)
+//   k >= 1    : Z = X X, Z = cZ + I, W = chol(Z), Y = X W^{-1}, V = Y W^{-T}
+//   every k   : X = (b/c) X + (a - b/c) V  (or M-scaled), symmetrize
+//   final     : P = (I - X) / 2
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/specproj_b200.h"
+#include "engine.cuh"
+
+namespace spg {
+std::atomic<long long> g_launches{0};
+}
+
+using namespace spg;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct StatusError : std::runtime_error {
+    int code;
+    StatusError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+long long band_len(int n, int b) { return (long long)(b + 1) * n - (long long)b * (b + 1) / 2; }
+
+// per-iteration diagnostics: max rank and memory of X (diagnostics, hodlr.hpp:679-695)
+__global__ void k_diag(const int* rank, int nnodes, const int* left, const int* right, const int* size,
+                       const int* counter, double* out, long long leaf_entries) {
+    __shared__ int smax;
+    __shared__ unsigned long long sent;
+    if (threadIdx.x == 0) { smax = 0; sent = 0; }
+    __syncthreads();
+    for (int id = threadIdx.x; id < nnodes; id += blockDim.x) {
+        if (left[id] < 0) continue;
+        const int ku = rank[2 * id], kl = rank[2 * id + 1];
+        atomicMax(&smax, max(ku, kl));
+        const unsigned long long e = (unsigned long long)(ku + kl) * (size[left[id]] + size[right[id]]);
+        atomicAdd(&sent, e);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int k = *counter - 1;
+        out[2 * k] = smax;
+        out[2 * k + 1] = 8.0 * (double)(sent + (unsigned long long)leaf_entries);
+    }
+}
+
+// flat preorder export (see include/specproj_b200.h): sizes -> offsets -> data
+__global__ void k_flat_offsets(DevTree t, const int* rank, long long* off) {
+    if (threadIdx.x != 0) return;
+    long long o = 0;
+    for (int id = 0; id < t.nnodes; ++id) {
+        off[id] = o;
+        if (t.left[id] < 0) o += (long long)t.size[id] * t.size[id];
+        else o += (long long)(rank[2 * id] + rank[2 * id + 1]) * (t.size[t.left[id]] + t.size[t.right[id]]);
+    }
+    off[t.nnodes] = o;
+}
+
+__global__ void k_flat_pack(DevTree t, DevHodlrView H, const long long* off, double* out) {
+    const int id = blockIdx.x;
+    double* o = out + off[id];
+    const int n = H.n;
+    if (t.left[id] < 0) {
+        const int s = t.size[id];
+        const double* L = H.leaves + H.leaf_off[t.leaf_ord[id]];
+        for (long long idx = threadIdx.x; idx < (long long)s * s; idx += blockDim.x) {
+            const int i = idx / s, j = idx % s;   // row-major out
+            o[idx] = L[i + (long long)j * s];
+        }
+        return;
+    }
+    const int l = t.left[id], r = t.right[id];
+    const int s1 = t.size[l], s2 = t.size[r], lev = t.level[id];
+    const int ku = H.rank[2 * id], kl = H.rank[2 * id + 1];
+    const double* Us = H.U + (long long)lev * KCAP * n;
+    const double* Vs = H.V + (long long)lev * KCAP * n;
+    struct F { const double* src; int rows, k; };
+    const F f[4] = {{Us + t.begin[l], s1, ku}, {Vs + t.begin[r], s2, ku}, {Us + t.begin[r], s2, kl}, {Vs + t.begin[l], s1, kl}};
+    long long base = 0;
+    for (int q = 0; q < 4; ++q) {
+        const long long tot = (long long)f[q].rows * f[q].k;
+        for (long long idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const int i = idx / f[q].k, c = idx % f[q].k;
+            o[base + idx] = f[q].src[i + (long long)c * n];
+        }
+        base += tot;
+    }
+}
+
+__global__ void k_flat_unpack(DevTree t, DevHodlrView H, const long long* off, const double* in) {
+    const int id = blockIdx.x;
+    const double* o = in + off[id];
+    const int n = H.n;
+    if (t.left[id] < 0) {
+        const int s = t.size[id];
+        double* L = H.leaves + H.leaf_off[t.leaf_ord[id]];
+        for (long long idx = threadIdx.x; idx < (long long)s * s; idx += blockDim.x) {
+            const int i = idx / s, j = idx % s;
+            L[i + (long long)j * s] = o[idx];
+        }
+        return;
+    }
+    const int l = t.left[id], r = t.right[id];
+    const int s1 = t.size[l], s2 = t.size[r], lev = t.level[id];
+    const int ku = H.rank[2 * id], kl = H.rank[2 * id + 1];
+    double* Us = H.U + (long long)lev * KCAP * n;
+    double* Vs = H.V + (long long)lev * KCAP * n;
+    struct F { double* dst; int rows, k; };
+    const F f[4] = {{Us + t.begin[l], s1, ku}, {Vs + t.begin[r], s2, ku}, {Us + t.begin[r], s2, kl}, {Vs + t.begin[l], s1, kl}};
+    long long base = 0;
+    for (int q = 0; q < 4; ++q) {
+        const long long tot = (long long)f[q].rows * f[q].k;
+        for (long long idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+            const int i = idx / f[q].k, c = idx % f[q].k;
+            f[q].dst[i + (long long)c * n] = o[base + idx];
+        }
+        base += tot;
+    }
+}
+
+__global__ void k_trace(DevTree t, DevHodlrView H, double* out) {
+    // hodlr_trace (hodlr.hpp:658-663), fixed order: leaves in preorder, one thread
+    if (threadIdx.x != 0) return;
+    double tr = 0.0;
+    for (int id = 0; id < t.nnodes; ++id) {
+        if (t.left[id] >= 0) continue;
+        const int s = t.size[id];
+        const double* L = H.leaves + H.leaf_off[t.leaf_ord[id]];
+        double ts = 0.0;
+        for (int i = 0; i < s; ++i) ts += L[i + (long long)i * s];
+        tr += ts;
+    }
+    *out = tr;
+}
+
+int check_status(unsigned st) {
+    if (st & ST_NPD) throw StatusError(SPG_NOT_POSITIVE_DEFINITE, "hodlr_cholesky: leaf factorization failed");
+    if (st & ST_SINGULAR) throw StatusError(SPG_SINGULAR, "triangular solve / banded LU: zero pivot");
+    if (st & (ST_RANK_CAP | ST_KIN_CAP))
+        throw StatusError(SPG_RANK_CAPACITY, "off-diagonal rank exceeded the compiled capacity KCAP=" + std::to_string(KCAP));
+    return 0;
+}
+
+enum Phase { PH_SETUP, PH_FIRST, PH_MUL, PH_CHOL, PH_SOLVE, PH_SOLVET, PH_AXPBY, PH_NPH };
+
+}  // namespace
+
+struct spg_result {
+    std::unique_ptr<Engine> eng;
+    std::unique_ptr<DHodlr> X, P;
+    spg_info info{};
+    std::vector<spg_iter_diag> diag;
+};
+
+struct spg_ctx {
+    std::unique_ptr<Engine> eng;
+    std::vector<std::unique_ptr<DHodlr>> slots;
+    std::unique_ptr<DHodlr> work, work2;
+};
+
+namespace {
+
+void export_flat(Engine& E, const DHodlr& H, int* ranks, double* data, long long* nd) {
+    const HTree& t = E.tree();
+    const int nn = t.nnodes();
+    long long* doff;
+    SPG_CUDA(cudaMalloc(&doff, sizeof(long long) * (nn + 1)));
+    cudaStream_t st = E.stream();
+    k_flat_offsets<<<1, 32, 0, st>>>(E.dtree(), H.rank, doff);
+    long long total = 0;
+    SPG_CUDA(cudaMemcpyAsync(&total, doff + nn, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    SPG_CUDA(cudaStreamSynchronize(st));
+    if (nd) *nd = total;
+    if (data) {
+        double* buf;
+        SPG_CUDA(cudaMalloc(&buf, sizeof(double) * std::max<long long>(total, 1)));
+        k_flat_pack<<<nn, 256, 0, st>>>(E.dtree(), H.view(), doff, buf);
+        SPG_CUDA(cudaMemcpyAsync(data, buf, sizeof(double) * total, cudaMemcpyDeviceToHost, st));
+        SPG_CUDA(cudaStreamSynchronize(st));
+        cudaFree(buf);
+    }
+    if (ranks) {
+        SPG_CUDA(cudaMemcpyAsync(ranks, H.rank, sizeof(int) * 2 * nn, cudaMemcpyDeviceToHost, st));
+        SPG_CUDA(cudaStreamSynchronize(st));
+        for (int id = 0; id < nn; ++id)
+            if (t.leaf(id)) ranks[2 * id] = ranks[2 * id + 1] = 0;
+    }
+    cudaFree(doff);
+}
+
+void import_flat(Engine& E, DHodlr& H, const int* ranks, const double* data) {
+    const HTree& t = E.tree();
+    const int nn = t.nnodes();
+    cudaStream_t st = E.stream();
+    H.zero(st);
+    std::vector<int> rk(ranks, ranks + 2 * nn);
+    long long total = 0;
+    for (int id = 0; id < nn; ++id) {
+        if (t.leaf(id)) { rk[2 * id] = rk[2 * id + 1] = 0; total += (long long)t.size[id] * t.size[id]; }
+        else {
+            if (rk[2 * id] > KCAP || rk[2 * id + 1] > KCAP) throw StatusError(SPG_RANK_CAPACITY, "upload rank > KCAP");
+            total += (long long)(rk[2 * id] + rk[2 * id + 1]) * (t.size[t.left[id]] + t.size[t.right[id]]);
+        }
+    }
+    SPG_CUDA(cudaMemcpyAsync(H.rank, rk.data(), sizeof(int) * 2 * nn, cudaMemcpyHostToDevice, st));
+    long long* doff;
+    double* buf;
+    SPG_CUDA(cudaMalloc(&doff, sizeof(long long) * (nn + 1)));
+    SPG_CUDA(cudaMalloc(&buf, sizeof(double) * std::max<long long>(total, 1)));
+    SPG_CUDA(cudaMemcpyAsync(buf, data, sizeof(double) * total, cudaMemcpyHostToDevice, st));
+    k_flat_offsets<<<1, 32, 0, st>>>(E.dtree(), H.rank, doff);
+    k_flat_unpack<<<nn, 256, 0, st>>>(E.dtree(), H.view(), doff, buf);
+    SPG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(buf);
+    cudaFree(doff);
+}
+
+void check_tree(const HTree& t) {
+    for (int f : t.leaves)
+        if (t.size[f] > 1024) throw StatusError(SPG_INVALID_ARGUMENT, "leaf size > 1024 unsupported (choose n_min <= 1024)");
+}
+
+// ------------------------------------------------------------------ the driver
+spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double eps, double delta) {
+    if (n < 2 || b < 1 || b >= n) throw StatusError(SPG_INVALID_ARGUMENT, "BandedSymmetric: n >= 2, 1 <= b < n required");
+    const long long blen = band_len(n, b);
+    for (long long i = 0; i < blen; ++i)
+        if (!std::isfinite(bands_host[i])) throw StatusError(SPG_INVALID_ARGUMENT, "hqdwh: nonfinite input");
+    auto R = std::make_unique<spg_result>();
+    R->eng = std::make_unique<Engine>(n, n_min, eps);
+    Engine& E = *R->eng;
+    check_tree(E.tree());
+    cudaStream_t st = E.stream();
+    const long long launches0 = g_launches.load();
+    Scalars& S = E.sc();
+
+    auto X = E.new_hodlr();
+    auto Z = E.new_hodlr();
+    auto W = E.new_hodlr();
+    auto Y = E.new_hodlr();
+    auto V = E.new_hodlr();
+    auto WK = E.new_hodlr();
+    auto P = E.new_hodlr();
+
+    // device scratch for the setup kernels
+    const int wbl = 3 * b + 1;
+    double *d_bands, *d_tmp, *d_rdiag, *d_diag;
+    int* d_piv;
+    const size_t tmp_doubles = (size_t)n * std::max(wbl, 4 * b + 4) + 8 * (size_t)n + 128;
+    SPG_CUDA(cudaMalloc(&d_bands, sizeof(double) * blen));
+    SPG_CUDA(cudaMalloc(&d_tmp, sizeof(double) * tmp_doubles));
+    SPG_CUDA(cudaMalloc(&d_rdiag, sizeof(double) * (size_t)(2 * b + 1) * n));
+    SPG_CUDA(cudaMalloc(&d_diag, sizeof(double) * 2 * 64));
+    SPG_CUDA(cudaMalloc(&d_piv, sizeof(int) * n));
+
+    // ---- timing instrumentation: per-run event tables, no host sync inside the loop
+    std::vector<cudaEvent_t> evs;
+    auto mkev = [&]() { cudaEvent_t e; SPG_CUDA(cudaEventCreate(&e)); evs.push_back(e); return e; };
+    const int nruns = 64;                     // one row per projector phase-run (k <= 60)
+    const int nmarks = PH_NPH;
+    std::vector<cudaEvent_t> evtab((size_t)nruns * nmarks * 2);
+    for (auto& e : evtab) e = mkev();
+    std::vector<int> used((size_t)nruns * nmarks, 0);
+    int cur_run = 0;
+    int* cur_run_p = &cur_run;
+    auto timed = [&](Plan& p, int phase, const std::function<void()>& body) {
+        cudaEvent_t* tab = evtab.data();
+        int* up = used.data();
+        p.launches.push_back([=](cudaStream_t s) {
+            const int r = *cur_run_p;
+            up[r * nmarks + phase] = 1;
+            SPG_CUDA(cudaEventRecord(tab[(r * nmarks + phase) * 2], s));
+        });
+        body();
+        p.launches.push_back([=](cudaStream_t s) {
+            const int r = *cur_run_p;
+            SPG_CUDA(cudaEventRecord(tab[(r * nmarks + phase) * 2 + 1], s));
+        });
+    };
+    auto commit_run = [&](Plan& p) {
+        E.arena().commit(st);
+        p.run(st);
+    };
+    cudaEvent_t t_start = mkev(), t_end = mkev();
+
+    // ---------------- setup: H2D, estimates, schedule
+    int count = 0;
+    double alpha = 0.0, l0 = 0.0;
+    unsigned status = 0;
+    {
+        Plan p;
+        p.launches.push_back([t_start](cudaStream_t s) { SPG_CUDA(cudaEventRecord(t_start, s)); });
+        timed(p, PH_SETUP, [&]() {
+            p.launches.push_back([=](cudaStream_t s) {
+                SPG_CUDA(cudaMemsetAsync(S.status, 0, sizeof(unsigned), s));
+                SPG_CUDA(cudaMemsetAsync(S.counter, 0, sizeof(int), s));
+                SPG_CUDA(cudaMemcpyAsync(d_bands, bands_host, sizeof(double) * blen, cudaMemcpyHostToDevice, s));
+                launch_estimate_2norm(n, b, d_bands, d_tmp, s);            // d_tmp[0] = alpha
+                SPG_CUDA(cudaMemcpyAsync(S.scal, d_tmp, sizeof(double), cudaMemcpyDeviceToDevice, s));
+                launch_estimate_l0(n, b, d_bands, S.scal, d_tmp + 128, d_piv, d_tmp + 128 + (size_t)n * wbl,
+                                   S.scal + 1, S.status, s);
+                launch_schedule(S.scal, delta, S.sched, S.count, s);
+            });
+        });
+        commit_run(p);
+        double sc[2];
+        SPG_CUDA(cudaMemcpyAsync(&count, S.count, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SPG_CUDA(cudaMemcpyAsync(&status, S.status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        SPG_CUDA(cudaMemcpyAsync(sc, S.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+        SPG_CUDA(cudaStreamSynchronize(st));
+        alpha = sc[0];
+        l0 = sc[1];
+        if (alpha == 0.0) throw StatusError(SPG_SINGULAR, "hqdwh: zero matrix");
+        if (status & ST_SINGULAR) throw StatusError(SPG_SINGULAR, "BandedLu: zero pivot");
+        if (count == -1) throw StatusError(SPG_INVALID_ARGUMENT, "qdwh: nonpositive lower bound l0");
+        if (count < 0) throw StatusError(SPG_DOMAIN, "qdwh_params: l must lie in (0, 1]");
+    }
+
+    // ---------------- X0 = from_banded(A / alpha)
+    {
+        Plan p;
+        const DevTree dt = E.dtree();
+        const DHodlr* Xp = X.get();
+        p.launches.push_back([=](cudaStream_t s) {
+            Xp->zero(s);
+            launch_from_band(dt, Xp->view(), 0, b, d_bands, S.scal + 2, 1.0, s);
+        });
+        commit_run(p);
+    }
+
+    // per-iteration diagnostics kernel
+    const long long leaf_entries = [&]() { long long e = 0; for (int f : E.tree().leaves) e += (long long)E.tree().size[f] * E.tree().size[f]; return e; }();
+    auto push_diag = [&](Plan& p) {
+        const DevTree dt = E.dtree();
+        const int* rk = X->rank;
+        p.launches.push_back([=](cudaStream_t s) {
+            k_diag<<<1, 256, 0, s>>>(rk, dt.nnodes, dt.left, dt.right, dt.size, S.counter, d_diag, leaf_entries);
+            SPG_LAUNCH_CHECK();
+        });
+    };
+    std::vector<cudaEvent_t> it_ev;
+
+    // ---------------- k = 0: QR-based first iterate
+    if (count >= 1) {
+        Plan p;
+        cudaEvent_t e0 = mkev();
+        it_ev.push_back(e0);
+        p.launches.push_back([e0](cudaStream_t s) { SPG_CUDA(cudaEventRecord(e0, s)); });
+        timed(p, PH_FIRST, [&]() {
+            const DevTree dt = E.dtree();
+            const DHodlr* Wp = W.get();
+            const DHodlr* Zp = Z.get();
+            p.launches.push_back([=](cudaStream_t s) {
+                launch_iter_params(S.sched, S.counter, S.slots, S.scal, s);
+                launch_givens_reduce(n, b, d_bands, S.slots, d_tmp, d_rdiag, s);
+                Wp->zero(s);
+                launch_from_band(dt, Wp->view(), 1, 2 * b, d_rdiag, nullptr, 1.0, s);
+                Zp->zero(s);
+                launch_from_band(dt, Zp->view(), 0, b, d_bands, S.slots + 5, 1.0, s);   // sqrt(c0) A / alpha
+            });
+            E.op_solve_upper_right(p, *Z, *W, *Y, *WK);    // Q1 = B R^{-1}
+            E.op_solve_upperT_right(p, *Y, *W, *V, *WK);   // M  = Q1 R^{-T} = Q1 Q2^T
+            E.op_symmetrize(p, *V);                        // q1q2t symmetrizes M (fast_qr.hpp:513)
+            E.op_axpby(p, 1.0, S.slots + 1, *X, 1.0, S.slots + 4, *V, *X);
+            E.op_symmetrize(p, *X);
+        });
+        push_diag(p);
+        commit_run(p);
+    }
+
+    // ---------------- k >= 1: Cholesky-based iterates (one plan, replayed)
+    if (count >= 2) {
+        Plan p;
+        timed(p, PH_MUL, [&]() {
+            p.launches.push_back([=](cudaStream_t s) { launch_iter_params(S.sched, S.counter, S.slots, S.scal, s); });
+            E.op_multiply(p, *X, *X, *Z);
+            E.op_scale_shift(p, *Z, 1.0, S.slots + 0, 1.0);
+        });
+        timed(p, PH_CHOL, [&]() { E.op_cholesky(p, *Z, *W, *WK); });
+        timed(p, PH_SOLVE, [&]() { E.op_solve_upper_right(p, *X, *W, *Y, *WK); });
+        timed(p, PH_SOLVET, [&]() { E.op_solve_upperT_right(p, *Y, *W, *V, *WK); });
+        timed(p, PH_AXPBY, [&]() {
+            E.op_axpby(p, 1.0, S.slots + 1, *X, 1.0, S.slots + 2, *V, *X);
+            E.op_symmetrize(p, *X);
+        });
+        push_diag(p);
+        E.arena().commit(st);
+        for (int k = 1; k < count; ++k) {
+            cur_run = k;
+            cudaEvent_t e0 = mkev();
+            it_ev.push_back(e0);
+            SPG_CUDA(cudaEventRecord(e0, st));
+            p.run(st);
+        }
+    }
+    {
+        cudaEvent_t e0 = mkev();
+        it_ev.push_back(e0);
+        SPG_CUDA(cudaEventRecord(e0, st));
+    }
+    // ---------------- P = (I - X) / 2  (qdwh.hpp:235-239)
+    {
+        Plan p;
+        E.op_copy(p, *X, *P);
+        E.op_scale_shift(p, *P, -0.5, nullptr, 0.5);
+        p.launches.push_back([t_end](cudaStream_t s) { SPG_CUDA(cudaEventRecord(t_end, s)); });
+        commit_run(p);
+    }
+    SPG_CUDA(cudaStreamSynchronize(st));
+    SPG_CUDA(cudaGetLastError());
+    SPG_CUDA(cudaMemcpy(&status, S.status, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    check_status(status);
+
+    // ---------------- report
+    spg_info& I = R->info;
+    I.n = n; I.b = b; I.n_min = n_min; I.eps = eps; I.delta = delta;
+    I.iterations = count;
+    I.alpha = alpha; I.l0 = l0;
+    I.kcap = KCAP;
+    float ms = 0.f;
+    SPG_CUDA(cudaEventElapsedTime(&ms, t_start, t_end));
+    I.ms_total = ms;
+    for (int r = 0; r < nruns; ++r)
+        for (int ph = 0; ph < nmarks; ++ph) {
+            if (!used[r * nmarks + ph]) continue;
+            SPG_CUDA(cudaEventElapsedTime(&ms, evtab[(r * nmarks + ph) * 2], evtab[(r * nmarks + ph) * 2 + 1]));
+            switch (ph) {
+                case PH_SETUP: I.ms_setup += ms; break;
+                case PH_FIRST: I.ms_first += ms; break;
+                case PH_MUL: I.ms_multiply += ms; break;
+                case PH_CHOL: I.ms_cholesky += ms; break;
+                case PH_SOLVE: I.ms_solve += ms; break;
+                case PH_SOLVET: I.ms_solveT += ms; break;
+                default: I.ms_axpby_sym += ms; break;
+            }
+        }
+    std::vector<double> sched(4 * 64), dg(2 * 64);
+    SPG_CUDA(cudaMemcpy(sched.data(), S.sched, sizeof(double) * 4 * 64, cudaMemcpyDeviceToHost));
+    SPG_CUDA(cudaMemcpy(dg.data(), d_diag, sizeof(double) * 2 * 64, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < count; ++k) {
+        spg_iter_diag d{};
+        d.k = k + 1;
+        d.l = sched[4 * k + 3];
+        d.c = sched[4 * k + 2];
+        d.max_rank = (int)dg[2 * k];
+        d.memory_bytes = (long long)dg[2 * k + 1];
+        float w = 0.f;
+        if (k + 1 < (int)it_ev.size()) SPG_CUDA(cudaEventElapsedTime(&w, it_ev[k], it_ev[k + 1]));
+        d.wall_ms = w;
+        R->diag.push_back(d);
+    }
+    I.launches = g_launches.load() - launches0;
+    // diagnostics of P
+    {
+        std::vector<int> rk(2 * E.tree().nnodes());
+        SPG_CUDA(cudaMemcpy(rk.data(), P->rank, sizeof(int) * rk.size(), cudaMemcpyDeviceToHost));
+        long long ent = leaf_entries;
+        int mx = 0;
+        for (int id = 0; id < E.tree().nnodes(); ++id) {
+            if (E.tree().leaf(id)) continue;
+            mx = std::max(mx, std::max(rk[2 * id], rk[2 * id + 1]));
+            ent += (long long)(rk[2 * id] + rk[2 * id + 1]) *
+                   (E.tree().size[E.tree().left[id]] + E.tree().size[E.tree().right[id]]);
+        }
+        I.max_rank = mx;
+        I.memory_bytes = 8 * ent;
+        double* dtr;
+        SPG_CUDA(cudaMalloc(&dtr, sizeof(double)));
+        k_trace<<<1, 32, 0, st>>>(E.dtree(), P->view(), dtr);
+        SPG_CUDA(cudaMemcpyAsync(&I.trace, dtr, sizeof(double), cudaMemcpyDeviceToHost, st));
+        SPG_CUDA(cudaStreamSynchronize(st));
+        cudaFree(dtr);
+    }
+    for (auto e : evs) cudaEventDestroy(e);
+    cudaFree(d_bands); cudaFree(d_tmp); cudaFree(d_rdiag); cudaFree(d_diag); cudaFree(d_piv);
+    R->X = std::move(X);
+    R->P = std::move(P);
+    return R.release();
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SPG_OK;
+    } catch (const StatusError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return SPG_CUDA_ERROR;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SPG_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SPG_CUDA_ERROR;
+    }
+}
+
+int ensure_device() {
+    int nd = 0;
+    if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) {
+        cudaGetLastError();
+        throw StatusError(SPG_NO_DEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+    }
+    return 0;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* spg_last_error(void) { return g_err.c_str(); }
+int spg_kcap(void) { return KCAP; }
+
+int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double delta, spg_result** out) {
+    *out = nullptr;
+    return guarded([&]() {
+        ensure_device();
+        *out = run_hqdwh(n, b, bands, n_min, eps, delta);
+    });
+}
+
+int spg_result_info(const spg_result* r, spg_info* info) {
+    if (!r) return SPG_INVALID_ARGUMENT;
+    *info = r->info;
+    return SPG_OK;
+}
+
+int spg_result_diag(const spg_result* r, spg_iter_diag* out) {
+    if (!r) return SPG_INVALID_ARGUMENT;
+    for (size_t i = 0; i < r->diag.size(); ++i) out[i] = r->diag[i];
+    return SPG_OK;
+}
+
+int spg_result_flat_size(const spg_result* r, int which, long long* nd) {
+    return guarded([&]() { export_flat(*r->eng, which == 0 ? *r->P : *r->X, nullptr, nullptr, nd); });
+}
+
+int spg_result_export(const spg_result* r, int which, int* ranks, double* data) {
+    return guarded([&]() { export_flat(*r->eng, which == 0 ? *r->P : *r->X, ranks, data, nullptr); });
+}
+
+int spg_result_apply(const spg_result* r, int which, int m, const double* X, double* Y) {
+    return guarded([&]() {
+        Engine& E = *r->eng;
+        const int n = E.tree().n;
+        if (m < 1 || m > KCAP) throw StatusError(SPG_INVALID_ARGUMENT, "spg_result_apply: 1 <= m <= KCAP");
+        const DHodlr& H = which == 0 ? *r->P : *r->X;
+        cudaStream_t st = E.stream();
+        std::vector<double> cm((size_t)n * m);
+        for (int i = 0; i < n; ++i)
+            for (int c = 0; c < m; ++c) cm[i + (size_t)c * n] = X[(size_t)i * m + c];
+        double *dx, *dy;
+        int* dm;
+        SPG_CUDA(cudaMalloc(&dx, sizeof(double) * (size_t)n * m));
+        SPG_CUDA(cudaMalloc(&dy, sizeof(double) * (size_t)n * m));
+        SPG_CUDA(cudaMalloc(&dm, sizeof(int)));
+        SPG_CUDA(cudaMemcpyAsync(dx, cm.data(), sizeof(double) * cm.size(), cudaMemcpyHostToDevice, st));
+        SPG_CUDA(cudaMemcpyAsync(dm, &m, sizeof(int), cudaMemcpyHostToDevice, st));
+        SPG_CUDA(cudaMemsetAsync(dy, 0, sizeof(double) * (size_t)n * m, st));
+        Plan p;
+        E.apply(p, {Engine::ApplyReq{&H, 0, 0, dx, dm, dy}});
+        E.arena().commit(st);
+        p.run(st);
+        SPG_CUDA(cudaMemcpyAsync(cm.data(), dy, sizeof(double) * cm.size(), cudaMemcpyDeviceToHost, st));
+        SPG_CUDA(cudaStreamSynchronize(st));
+        for (int i = 0; i < n; ++i)
+            for (int c = 0; c < m; ++c) Y[(size_t)i * m + c] = cm[i + (size_t)c * n];
+        cudaFree(dx); cudaFree(dy); cudaFree(dm);
+    });
+}
+
+void spg_result_free(spg_result* r) { delete r; }
+
+int spg_tree(int n, int n_min, int* begin, int* size, int* left, int* right, int* depth) {
+    int nn = -1;
+    const int st = guarded([&]() {
+        HTree t(n, n_min);
+        nn = t.nnodes();
+        if (begin)
+            for (int i = 0; i < nn; ++i) { begin[i] = t.begin[i]; size[i] = t.size[i]; left[i] = t.left[i]; right[i] = t.right[i]; }
+        if (depth) *depth = t.depth;
+    });
+    return st == SPG_OK ? nn : -st;
+}
+
+int spg_qdwh_params(double l, double* abc) {
+    if (!(l > 0.0) || l > 1.0) { g_err = "qdwh_params: l must lie in (0, 1]"; return SPG_DOMAIN; }
+    const double l2 = l * l;
+    const double gamma = std::cbrt(4.0 * (1.0 - l2) / (l2 * l2));
+    const double sq = std::sqrt(1.0 + gamma);
+    const double a = sq + 0.5 * std::sqrt(8.0 - 4.0 * gamma + 8.0 * (2.0 - l2) / (l2 * sq));
+    const double bb = 0.25 * (a - 1.0) * (a - 1.0);
+    abc[0] = a; abc[1] = bb; abc[2] = a + bb - 1.0;
+    return SPG_OK;
+}
+
+double spg_l_update(double l, double a, double b, double c) { return l * (a + b * l * l) / (1.0 + c * l * l); }
+
+int spg_make_dimer_chain(int n, int b, double t1, double t2, double eps_dis, double s, unsigned long long seed,
+                         double* bands) {
+    if (n < 2 || b < 1 || b >= n) return SPG_INVALID_ARGUMENT;
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    const long long len = band_len(n, b);
+    std::fill(bands, bands + len, 0.0);
+    for (int i = 0; i < n; ++i) bands[i] = eps_dis * dist(rng);
+    for (int i = 0; i + 1 < n; ++i) bands[n + i] = (i % 2 == 0) ? t1 : t2;
+    if (s != 0.0) {
+        long long off = 0;
+        for (int d = 0; d <= b; ++d) {
+            for (int i = 0; i + d < n; ++i) bands[off + i] += s * dist(rng);
+            off += n - d;
+        }
+    }
+    return SPG_OK;
+}
+
+int spg_make_random_banded(int n, int b, unsigned long long seed, double* bands) {
+    if (n < 2 || b < 1 || b >= n) return SPG_INVALID_ARGUMENT;
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    const long long len = band_len(n, b);
+    for (long long i = 0; i < len; ++i) bands[i] = dist(rng);
+    return SPG_OK;
+}
+
+// ---------------------------------------------------------------- component API
+spg_ctx* spg_ctx_create(int n, int n_min, double eps, int nslots) {
+    spg_ctx* c = nullptr;
+    guarded([&]() {
+        ensure_device();
+        auto C = std::make_unique<spg_ctx>();
+        C->eng = std::make_unique<Engine>(n, n_min, eps);
+        check_tree(C->eng->tree());
+        for (int i = 0; i < nslots; ++i) {
+            C->slots.push_back(C->eng->new_hodlr());
+            C->slots.back()->zero(C->eng->stream());
+        }
+        C->work = C->eng->new_hodlr();
+        C->work2 = C->eng->new_hodlr();
+        C->eng->arena().commit(C->eng->stream());
+        c = C.release();
+    });
+    return c;
+}
+
+void spg_ctx_free(spg_ctx* c) { delete c; }
+
+int spg_ctx_upload(spg_ctx* c, int slot, const int* ranks, const double* data) {
+    return guarded([&]() { import_flat(*c->eng, *c->slots.at(slot), ranks, data); });
+}
+
+int spg_ctx_flat_size(spg_ctx* c, int slot, long long* nd) {
+    return guarded([&]() { export_flat(*c->eng, *c->slots.at(slot), nullptr, nullptr, nd); });
+}
+
+int spg_ctx_download(spg_ctx* c, int slot, int* ranks, double* data) {
+    return guarded([&]() { export_flat(*c->eng, *c->slots.at(slot), ranks, data, nullptr); });
+}
+
+int spg_ctx_from_banded(spg_ctx* c, int dst, int b, const double* bands) {
+    return guarded([&]() {
+        Engine& E = *c->eng;
+        const int n = E.tree().n;
+        const long long len = band_len(n, b);
+        double* d;
+        SPG_CUDA(cudaMalloc(&d, sizeof(double) * len));
+        SPG_CUDA(cudaMemcpy(d, bands, sizeof(double) * len, cudaMemcpyHostToDevice));
+        DHodlr& H = *c->slots.at(dst);
+        H.zero(E.stream());
+        launch_from_band(E.dtree(), H.view(), 0, b, d, nullptr, 1.0, E.stream());
+        SPG_CUDA(cudaStreamSynchronize(E.stream()));
+        cudaFree(d);
+    });
+}
+
+int spg_ctx_op(spg_ctx* c, int op, int dst, int a, int b, double alpha, double beta) {
+    return guarded([&]() {
+        Engine& E = *c->eng;
+        cudaStream_t st = E.stream();
+        SPG_CUDA(cudaMemsetAsync(E.sc().status, 0, sizeof(unsigned), st));
+        Plan p;
+        DHodlr& D = *c->slots.at(dst);
+        switch (op) {
+            case 1: E.op_multiply(p, *c->slots.at(a), *c->slots.at(b), D); break;
+            case 2: E.op_axpby(p, alpha, nullptr, *c->slots.at(a), beta, nullptr, *c->slots.at(b), D); break;
+            case 3: E.op_symmetrize(p, D); break;
+            case 4: E.op_cholesky(p, *c->slots.at(a), D, *c->work); break;
+            case 5: E.op_solve_upper_right(p, *c->slots.at(a), *c->slots.at(b), D, *c->work); break;
+            case 6: E.op_solve_upperT_right(p, *c->slots.at(a), *c->slots.at(b), D, *c->work); break;
+            case 7: E.op_scale_shift(p, D, alpha, nullptr, beta); break;
+            default: throw StatusError(SPG_INVALID_ARGUMENT, "spg_ctx_op: unknown op");
+        }
+        E.arena().commit(st);
+        p.run(st);
+        SPG_CUDA(cudaStreamSynchronize(st));
+        unsigned s = 0;
+        SPG_CUDA(cudaMemcpy(&s, E.sc().status, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        check_status(s);
+    });
+}
+
+int spg_truncate(int p, int s, int k, const double* U, const double* V, double eps, double* Uo, double* Vo, int* r) {
+    return guarded([&]() {
+        ensure_device();
+        if (k > KIN_MAX) throw StatusError(SPG_RANK_CAPACITY, "spg_truncate: k > KIN_MAX");
+        Engine E(std::max(p, s), 2, eps, (size_t)8 << 20);
+        cudaStream_t st = E.stream();
+        std::vector<double> cu((size_t)p * k), cv((size_t)s * k);
+        for (int i = 0; i < p; ++i) for (int j = 0; j < k; ++j) cu[i + (size_t)j * p] = U[(size_t)i * k + j];
+        for (int i = 0; i < s; ++i) for (int j = 0; j < k; ++j) cv[i + (size_t)j * s] = V[(size_t)i * k + j];
+        double *du, *dv, *ou, *ov;
+        int* dr;
+        SPG_CUDA(cudaMalloc(&du, sizeof(double) * std::max<size_t>(cu.size(), 1)));
+        SPG_CUDA(cudaMalloc(&dv, sizeof(double) * std::max<size_t>(cv.size(), 1)));
+        SPG_CUDA(cudaMalloc(&ou, sizeof(double) * (size_t)p * KCAP));
+        SPG_CUDA(cudaMalloc(&ov, sizeof(double) * (size_t)s * KCAP));
+        SPG_CUDA(cudaMalloc(&dr, sizeof(int)));
+        SPG_CUDA(cudaMemcpy(du, cu.data(), sizeof(double) * cu.size(), cudaMemcpyHostToDevice));
+        SPG_CUDA(cudaMemcpy(dv, cv.data(), sizeof(double) * cv.size(), cudaMemcpyHostToDevice));
+        SPG_CUDA(cudaMemset(E.sc().status, 0, sizeof(unsigned)));
+        TTask t{};
+        t.p = p; t.s = s; t.ng = 1; t.skipg = -1;
+        t.g[0] = TGroup{du, dv, p, s, nullptr, k, 1.0, nullptr};
+        t.ou = ou; t.ov = ov; t.ldou = p; t.ldov = s; t.orank = dr;
+        Plan pl;
+        E.trunc(pl, {t});
+        E.arena().commit(st);
+        pl.run(st);
+        SPG_CUDA(cudaStreamSynchronize(st));
+        int rr = 0;
+        SPG_CUDA(cudaMemcpy(&rr, dr, sizeof(int), cudaMemcpyDeviceToHost));
+        unsigned stt = 0;
+        SPG_CUDA(cudaMemcpy(&stt, E.sc().status, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        std::vector<double> hu((size_t)p * KCAP), hv((size_t)s * KCAP);
+        SPG_CUDA(cudaMemcpy(hu.data(), ou, sizeof(double) * hu.size(), cudaMemcpyDeviceToHost));
+        SPG_CUDA(cudaMemcpy(hv.data(), ov, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < p; ++i) for (int j = 0; j < rr; ++j) Uo[(size_t)i * k + j] = hu[i + (size_t)j * p];
+        for (int i = 0; i < s; ++i) for (int j = 0; j < rr; ++j) Vo[(size_t)i * k + j] = hv[i + (size_t)j * s];
+        *r = rr;
+        cudaFree(du); cudaFree(dv); cudaFree(ou); cudaFree(ov); cudaFree(dr);
+        check_status(stt);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,128 @@
+// Batched FP64 GEMM on the sm_100a FP64 tensor path (mma.sync m8n8k4 -> SASS DMMA.8x8x4).
+//
+// Used for every dense contraction of the HODLR arithmetic: leaf x leaf
+// (matmul, dense.hpp:69-83), leaf x panel and factor x coefficient products
+// (gemm_acc_rows / gemm_tn_rows, hodlr.hpp:169-198), the k x k cores of
+// lr_multiply (lowrank.hpp:89-93) and the Schur factors (hodlr.hpp:557-558).
+// Dimensions may be ranks living in device memory; CTAs beyond the runtime
+// extent exit.  Split-K partials are reduced in a fixed order (deterministic).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spg {
+
+constexpr int GBM = 64, GBN = 64, GBK = 16, GPAD = 8;
+constexpr int G_THREADS = 256;
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ int dimv(int c, const int* p) { return p ? *p : c; }
+
+__global__ void __launch_bounds__(G_THREADS) k_gemm(const GemmItem* __restrict__ items, const int4* __restrict__ ctas) {
+    __shared__ double As[GBK][GBM + GPAD];
+    __shared__ double Bs[GBK][GBN + GPAD];
+    const int4 cm = ctas[blockIdx.x];
+    const GemmItem& g = items[cm.x];
+    const int M = dimv(g.M, g.Mp), N = dimv(g.N, g.Np), K = dimv(g.K, g.Kp);
+    const int m0 = cm.y * GBM, n0 = cm.z * GBN;
+    if (m0 >= M || n0 >= N) return;
+    const bool split = g.nsplit > 1;
+    int kbeg = 0, kend = K;
+    if (split) {
+        const int chunk = ((K + g.nsplit - 1) / g.nsplit + GBK - 1) / GBK * GBK;
+        kbeg = cm.w * chunk;
+        kend = min(K, kbeg + chunk);
+    }
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;   // warp tile 32 x 16
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int k0 = kbeg; k0 < kend; k0 += GBK) {
+        // A tile: As[kk][mm] = A(m0+mm, k0+kk)
+        for (int idx = tid; idx < GBK * GBM; idx += G_THREADS) {
+            int mm, kk;
+            if (!g.ta) { mm = idx % GBM; kk = idx / GBM; } else { kk = idx % GBK; mm = idx / GBK; }
+            const int m = m0 + mm, k = k0 + kk;
+            double v = 0.0;
+            if (m < M && k < kend) v = g.ta ? g.A[k + (long long)m * g.lda] : g.A[m + (long long)k * g.lda];
+            As[kk][mm] = v;
+        }
+        // B tile: Bs[kk][nn] = B(k0+kk, n0+nn)
+        for (int idx = tid; idx < GBK * GBN; idx += G_THREADS) {
+            int nn, kk;
+            if (!g.tb) { kk = idx % GBK; nn = idx / GBK; } else { nn = idx % GBN; kk = idx / GBN; }
+            const int n = n0 + nn, k = k0 + kk;
+            double v = 0.0;
+            if (n < N && k < kend) v = g.tb ? g.B[n + (long long)k * g.ldb] : g.B[k + (long long)n * g.ldb];
+            Bs[kk][nn] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < GBK; ks += 4) {
+            double af[4], bf[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = As[ks + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) bf[j] = Bs[ks + (lane & 3)][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();
+    }
+    const double alpha = g.alphap ? g.alpha * *g.alphap : g.alpha;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int m = m0 + wm + i * 8 + (lane >> 2);
+                const int n = n0 + wn + j * 8 + 2 * (lane & 3) + v;
+                if (m < M && n < N) {
+                    if (split) {
+                        g.partial[(long long)cm.w * g.Mcap * g.Ncap + m + (long long)n * g.Mcap] = acc[i][j][v];
+                    } else {
+                        double* c = g.C + m + (long long)n * g.ldc;
+                        *c = g.beta == 0.0 ? alpha * acc[i][j][v] : alpha * acc[i][j][v] + g.beta * *c;
+                    }
+                }
+            }
+}
+
+// fixed-order split-K reduction: one CTA per item
+__global__ void k_gemm_reduce(const GemmItem* __restrict__ items, const int* __restrict__ red) {
+    const GemmItem& g = items[red[blockIdx.x]];
+    const int M = dimv(g.M, g.Mp), N = dimv(g.N, g.Np), K = dimv(g.K, g.Kp);
+    const double alpha = g.alphap ? g.alpha * *g.alphap : g.alpha;
+    const int chunk = ((K + g.nsplit - 1) / g.nsplit + GBK - 1) / GBK * GBK;
+    const int nused = chunk > 0 ? min(g.nsplit, (K + chunk - 1) / chunk) : 0;
+    for (int idx = threadIdx.x; idx < M * N; idx += blockDim.x) {
+        const int m = idx % M, n = idx / M;
+        double s = 0.0;
+        for (int p = 0; p < nused; ++p) s += g.partial[(long long)p * g.Mcap * g.Ncap + m + (long long)n * g.Mcap];
+        double* c = g.C + m + (long long)n * g.ldc;
+        *c = g.beta == 0.0 ? alpha * s : alpha * s + g.beta * *c;
+    }
+}
+
+void launch_gemm(const GemmBatch& b, cudaStream_t st) {
+    if (b.nctas == 0) return;
+    k_gemm<<<b.nctas, G_THREADS, 0, st>>>(b.d_items, b.d_ctas);
+    SPG_LAUNCH_CHECK();
+    if (b.nred) {
+        k_gemm_reduce<<<b.nred, 256, 0, st>>>(b.d_items, b.d_red_items);
+        SPG_LAUNCH_CHECK();
+    }
+}
+
+}  // namespace spg

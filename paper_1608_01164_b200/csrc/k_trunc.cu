@@ -1,0 +1,463 @@
+// Batched low-rank recompression ("truncate", lowrank.hpp:67-86) for sm_100a.
+//
+//   B = sum_g su_g U_g V_g^T      (concatenation lr_concat, lowrank.hpp:43-63)
+//   QR(U) = Q_u R_u, QR(V) = Q_v R_v   -- streaming Householder TSQR, 2 levels
+//   C = R_u R_v^T, one-sided Jacobi SVD C V_rot = W   (dense_factor.hpp:112-193)
+//   keep sigma_j = ||W_j|| > eps  (absolute, lowrank.hpp:74)
+//   U' = Q_u W_r,  V' = Q_v V_rot_r                    (lowrank.hpp:82-83)
+//
+// Five launches per batch: tsqr(level 0) -> tsqr(merge) -> core -> apply(merge) -> apply(level 0).
+// Ranks are read from / written to device memory, so a batch never syncs the host.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spg {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ bool task_skip(const TTask& t) {
+    if (t.skipg < 0) return false;
+    const TGroup& g = t.g[t.skipg];
+    return (g.kp ? *g.kp : g.kc) == 0;
+}
+
+__device__ __forceinline__ int task_kin(const TTask& t) {
+    int k = 0;
+    for (int g = 0; g < t.ng; ++g) k += t.g[g].kp ? *t.g[g].kp : t.g[g].kc;
+    return k;
+}
+
+// group lookup for concatenated column c (side 0 = U, 1 = V); returns pointer to column start
+__device__ __forceinline__ const double* col_ptr(const TTask& t, int side, int c, double& scale, int& ld) {
+    int off = 0;
+    for (int g = 0; g < t.ng; ++g) {
+        const int kg = t.g[g].kp ? *t.g[g].kp : t.g[g].kc;
+        if (c < off + kg) {
+            const int cc = c - off;
+            if (side == 0) { scale = t.g[g].sup ? t.g[g].su * *t.g[g].sup : t.g[g].su; ld = t.g[g].ldu; return t.g[g].u + (long long)cc * t.g[g].ldu; }
+            scale = 1.0; ld = t.g[g].ldv; return t.g[g].v + (long long)cc * t.g[g].ldv;
+        }
+        off += kg;
+    }
+    scale = 0.0; ld = 0;
+    return nullptr;
+}
+
+__device__ __forceinline__ double* seg_area(const TTask& t, double* ws, int side, int s) {
+    return ws + t.ws + TS_HEADER + t.wsz[side] + (long long)s * ts_seg_doubles(t.seg[side]);
+}
+__device__ __forceinline__ double* merge_area(const TTask& t, double* ws, int side) {
+    return ws + t.ws + TS_HEADER + t.wsz[side] + (long long)t.nseg[side] * ts_seg_doubles(t.seg[side]);
+}
+__device__ __forceinline__ double* z_area(const TTask& t, double* ws, int side) {
+    const int rows = side == 0 ? t.p : t.s;
+    return ws + t.ws + TS_HEADER + t.wsz[side] + ts_side_doubles(rows, t.seg[side], t.nseg[side]) -
+           (long long)KIN_MAX * KCAP;
+}
+
+// ------------------------------------------------------------------ TSQR
+// Streaming Householder QR of the rows [r0, r0+nrows) of an implicit matrix with
+// k columns, starting from R = 0:  [0_k; A] = Q [R; 0].  Each 128-row sub-block
+// is folded into R by k reflectors acting on (R row j, block rows); reflector
+// tails and taus are stored for the later Q application.
+//
+// Loader: fills Bk (SB x k, col-major ld SB) with rows [row0, row0+SB) (zero padded).
+template <class Loader>
+__device__ void stream_qr(int k, int nrows, double* refl, double* tau_out, double* Rout,
+                          double* sR, double* sB, double* sTau, const Loader& load) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = blockDim.x >> 5;
+    for (int i = tid; i < KIN_MAX * KIN_MAX; i += blockDim.x) sR[i] = 0.0;
+    const int nsub = (nrows + SB - 1) / SB;
+    for (int b = 0; b < nsub; ++b) {
+        __syncthreads();
+        load(b * SB, sB);
+        __syncthreads();
+        for (int j = 0; j < k; ++j) {
+            if (warp == 0) {
+                double* x = sB + (long long)j * SB;
+                double s2 = 0.0;
+#pragma unroll
+                for (int t = 0; t < SB / 32; ++t) { const double v = x[lane + 32 * t]; s2 += v * v; }
+                s2 = warp_sum(s2);
+                const double alpha = sR[j + j * KIN_MAX];
+                double tau = 0.0, scal = 0.0;
+                if (s2 > 0.0) {
+                    const double nrm = sqrt(alpha * alpha + s2);
+                    const double beta = alpha > 0.0 ? -nrm : nrm;
+                    tau = (beta - alpha) / beta;
+                    scal = 1.0 / (alpha - beta);
+                    if (lane == 0) sR[j + j * KIN_MAX] = beta;
+                }
+#pragma unroll
+                for (int t = 0; t < SB / 32; ++t) x[lane + 32 * t] *= scal;   // scal = 0 -> v = 0
+                if (lane == 0) sTau[j] = tau;
+            }
+            __syncthreads();
+            const double tau = sTau[j];
+            if (tau != 0.0) {
+                const double* v = sB + (long long)j * SB;
+                double vr[SB / 32];
+#pragma unroll
+                for (int t = 0; t < SB / 32; ++t) vr[t] = v[lane + 32 * t];
+                for (int c = j + 1 + warp; c < k; c += nwarps) {
+                    double* a = sB + (long long)c * SB;
+                    double d = 0.0;
+#pragma unroll
+                    for (int t = 0; t < SB / 32; ++t) d += vr[t] * a[lane + 32 * t];
+                    d = warp_sum(d) + sR[j + c * KIN_MAX];
+                    const double w = tau * d;
+#pragma unroll
+                    for (int t = 0; t < SB / 32; ++t) a[lane + 32 * t] -= w * vr[t];
+                    if (lane == 0) sR[j + c * KIN_MAX] -= w;
+                }
+            }
+            __syncthreads();
+        }
+        // store reflector tails (SB x k) and taus for this sub-block
+        double* dst = refl + (long long)b * SB * KIN_MAX;
+        for (int i = tid; i < SB * k; i += blockDim.x) dst[i] = sB[i];
+        for (int i = tid; i < k; i += blockDim.x) tau_out[(long long)b * KIN_MAX + i] = sTau[i];
+    }
+    __syncthreads();
+    for (int i = tid; i < KIN_MAX * KIN_MAX; i += blockDim.x) {
+        const int r = i % KIN_MAX, c = i / KIN_MAX;
+        Rout[i] = (r <= c && r < k && c < k) ? sR[i] : 0.0;
+    }
+}
+
+// items: (task, side, seg) for level 0; (task, side, -1) for the merge level
+__global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ tasks, const int3* __restrict__ items,
+                                                    double* __restrict__ ws, unsigned* status, int merge) {
+    extern __shared__ double smem[];
+    double* sR = smem;                        // KIN_MAX^2
+    double* sB = sR + KIN_MAX * KIN_MAX;      // SB * KIN_MAX
+    double* sTau = sB + SB * KIN_MAX;         // KIN_MAX
+    const int3 it = items[blockIdx.x];
+    const TTask& t = tasks[it.x];
+    const int side = it.y;
+    if (task_skip(t)) return;
+    int k = task_kin(t);
+    if (k > KIN_MAX) { if (threadIdx.x == 0) atomicOr(status, ST_KIN_CAP); k = KIN_MAX; }
+    if (k == 0) return;
+    const int rows = side == 0 ? t.p : t.s;
+    if (!merge) {
+        const int s = it.z;
+        const int r0 = s * t.seg[side];
+        const int nr = min(t.seg[side], rows - r0);
+        if (nr <= 0) return;
+        double* base = seg_area(t, ws, side, s);
+        const long long nsub = ts_nsub(t.seg[side]);
+        auto load = [&](int sub0, double* B) {
+            for (int c = threadIdx.x >> 7; c < k; c += blockDim.x >> 7) {
+                double sc; int ld;
+                const double* cp = col_ptr(t, side, c, sc, ld);
+                const int i = threadIdx.x & 127;
+                const int gi = sub0 + i;
+                B[(long long)c * SB + i] = (gi < nr) ? sc * cp[r0 + gi] : 0.0;
+            }
+        };
+        stream_qr(k, nr, base, base + nsub * SB * KIN_MAX, base + nsub * SB * KIN_MAX + nsub * KIN_MAX, sR, sB,
+                  sTau, load);
+    } else {
+        const int ns = t.nseg[side];
+        if (ns <= 1) return;
+        // stacked R_s (k x k each): row i -> segment i / k, local i % k
+        const int mrows = ns * k;
+        double* mb = merge_area(t, ws, side);
+        const long long nsubm = ts_nsub(ns * KIN_MAX);
+        auto load = [&](int sub0, double* B) {
+            for (int idx = threadIdx.x; idx < SB * k; idx += blockDim.x) {
+                const int i = idx % SB, c = idx / SB;
+                const int gi = sub0 + i;
+                double v = 0.0;
+                if (gi < mrows) {
+                    const int s = gi / k, lr = gi % k;
+                    const double* Rs = seg_area(t, ws, side, s) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + KIN_MAX);
+                    v = Rs[lr + (long long)c * KIN_MAX];
+                }
+                B[(long long)c * SB + i] = v;
+            }
+        };
+        stream_qr(k, mrows, mb, mb + nsubm * SB * KIN_MAX, mb + nsubm * SB * KIN_MAX + nsubm * KIN_MAX, sR, sB,
+                  sTau, load);
+    }
+}
+
+// ------------------------------------------------------------------ core SVD
+__device__ __forceinline__ const double* final_R(const TTask& t, double* ws, int side) {
+    if (t.nseg[side] > 1) {
+        const long long nsubm = ts_nsub(t.nseg[side] * KIN_MAX);
+        return merge_area(t, ws, side) + nsubm * (SB * KIN_MAX + KIN_MAX);
+    }
+    return seg_area(t, ws, side, 0) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + KIN_MAX);
+}
+
+// one CTA per task: C = R_u R_v^T, parallel one-sided Jacobi, sort, threshold
+__global__ void __launch_bounds__(TS_THREADS) k_core(const TTask* __restrict__ tasks, double* __restrict__ ws,
+                                                    double eps, unsigned* status) {
+    extern __shared__ double smem[];
+    double* sW = smem;                       // k x k (ld KIN_MAX)
+    double* sV = sW + KIN_MAX * KIN_MAX;     // k x k
+    __shared__ double sSig[KIN_MAX];
+    __shared__ int sPerm[KIN_MAX];
+    __shared__ int sTop[KIN_MAX / 2 + 1], sBot[KIN_MAX / 2 + 1];
+    __shared__ int sRot;
+    const TTask& t = tasks[blockIdx.x];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    double* hdr = ws + t.ws;
+    if (task_skip(t)) {
+        if (tid == 0) { hdr[0] = 0; hdr[1] = 0; }
+        return;
+    }
+    int k = task_kin(t);
+    if (k > KIN_MAX) k = KIN_MAX;
+    if (k == 0) {
+        if (tid == 0) { hdr[0] = 0; hdr[1] = 0; *t.orank = 0; }
+        return;
+    }
+    const double* Ru = final_R(t, ws, 0);
+    const double* Rv = final_R(t, ws, 1);
+    // C[i][j] = sum_l Ru[i][l] Rv[j][l], l >= max(i, j)
+    for (int idx = tid; idx < k * k; idx += blockDim.x) {
+        const int i = idx % k, j = idx / k;
+        double s = 0.0;
+        for (int l = max(i, j); l < k; ++l) s += Ru[i + (long long)l * KIN_MAX] * Rv[j + (long long)l * KIN_MAX];
+        sW[i + j * KIN_MAX] = s;
+        sV[i + j * KIN_MAX] = (i == j) ? 1.0 : 0.0;
+    }
+    const int kk = k + (k & 1);   // even number of slots; slot k (if odd) is a dummy
+    const int npairs = kk / 2;
+    if (tid < npairs) { sTop[tid] = 2 * tid; sBot[tid] = 2 * tid + 1; }
+    __syncthreads();
+    const double tol = 1e-15;
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        if (tid == 0) sRot = 0;
+        __syncthreads();
+        int rotated = 0;
+        for (int round = 0; round < kk - 1; ++round) {
+            for (int pi = warp; pi < npairs; pi += nwarps) {
+                int p = sTop[pi], q = sBot[pi];
+                if (p > q) { const int tmp = p; p = q; q = tmp; }
+                if (q >= k) continue;
+                double* wp = sW + p * KIN_MAX;
+                double* wq = sW + q * KIN_MAX;
+                double app = 0.0, aqq = 0.0, apq = 0.0;
+                for (int i = lane; i < k; i += 32) {
+                    const double a = wp[i], b = wq[i];
+                    app += a * a; aqq += b * b; apq += a * b;
+                }
+                app = warp_sum(app); aqq = warp_sum(aqq); apq = warp_sum(apq);
+                if (app == 0.0 || aqq == 0.0) continue;
+                if (fabs(apq) <= tol * sqrt(app * aqq)) continue;
+                rotated = 1;
+                const double zeta = (aqq - app) / (2.0 * apq);
+                const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / sqrt(1.0 + tt * tt);
+                const double s = c * tt;
+                for (int i = lane; i < k; i += 32) {
+                    const double x = wp[i], y = wq[i];
+                    wp[i] = c * x - s * y; wq[i] = s * x + c * y;
+                }
+                double* vp = sV + p * KIN_MAX;
+                double* vq = sV + q * KIN_MAX;
+                for (int i = lane; i < k; i += 32) {
+                    const double x = vp[i], y = vq[i];
+                    vp[i] = c * x - s * y; vq[i] = s * x + c * y;
+                }
+            }
+            __syncthreads();
+            // round-robin tournament rotation (slot top[0] fixed)
+            if (tid == 0) {
+                const int lastTop = sTop[npairs - 1];
+                const int firstBot = sBot[0];
+                for (int i = npairs - 1; i >= 2; --i) sTop[i] = sTop[i - 1];
+                if (npairs > 1) sTop[1] = firstBot;
+                for (int i = 0; i < npairs - 1; ++i) sBot[i] = sBot[i + 1];
+                sBot[npairs - 1] = lastTop;
+                if (npairs == 1) { sBot[0] = firstBot; }
+            }
+            __syncthreads();
+        }
+        if (rotated) sRot = 1;   // benign race: any writer sets 1
+        __syncthreads();
+        if (!sRot) break;
+        __syncthreads();
+    }
+    // singular values = column norms of W, descending order (stable by index)
+    for (int j = warp; j < k; j += nwarps) {
+        double s = 0.0;
+        for (int i = lane; i < k; i += 32) { const double a = sW[i + j * KIN_MAX]; s += a * a; }
+        s = warp_sum(s);
+        if (lane == 0) sSig[j] = sqrt(s);
+    }
+    __syncthreads();
+    if (tid < k) {
+        const double sj = sSig[tid];
+        int pos = 0;
+        for (int i = 0; i < k; ++i) {
+            const double si = sSig[i];
+            pos += (si > sj) || (si == sj && i < tid);
+        }
+        sPerm[pos] = tid;
+    }
+    __syncthreads();
+    __shared__ int sR_;
+    if (tid == 0) {
+        int r = 0;
+        while (r < k && sSig[sPerm[r]] > eps) ++r;
+        if (r > KCAP) { atomicOr(status, ST_RANK_CAP); r = KCAP; }
+        sR_ = r;
+        hdr[0] = k; hdr[1] = r;
+        if (!(sSig[sPerm[0]] == sSig[sPerm[0]])) atomicOr(status, ST_NONFINITE);
+    }
+    __syncthreads();
+    const int r = sR_;
+    double* Zu = z_area(t, ws, 0);
+    double* Zv = z_area(t, ws, 1);
+    for (int idx = tid; idx < k * r; idx += blockDim.x) {
+        const int i = idx % k, c = idx / k;
+        const int src = sPerm[c];
+        Zu[i + (long long)c * KIN_MAX] = sW[i + src * KIN_MAX];
+        Zv[i + (long long)c * KIN_MAX] = sV[i + src * KIN_MAX];
+    }
+    __syncthreads();
+    if (tid == 0) *t.orank = r;
+}
+
+// ------------------------------------------------------------------ Q application
+// Applies Q (stored as per-sub-block reflectors, see stream_qr) to [Z; 0]:
+// the R-part starts as Z (k x r), every sub-block's output rows start at 0;
+// sub-blocks are visited in reverse, reflectors within a block in reverse.
+template <class Writer>
+__device__ void stream_apply(int k, int r, int nrows, const double* refl, const double* taus, const double* Z0,
+                             int ldz, double* sZ, double* sO, double* sV, const Writer& write) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (int idx = tid; idx < k * r; idx += blockDim.x) {
+        const int i = idx % k, c = idx / k;
+        sZ[i + c * KIN_MAX] = Z0[i + (long long)c * ldz];
+    }
+    const int nsub = (nrows + SB - 1) / SB;
+    for (int b = nsub - 1; b >= 0; --b) {
+        __syncthreads();
+        const double* vb = refl + (long long)b * SB * KIN_MAX;
+        for (int i = tid; i < SB * k; i += blockDim.x) sV[i] = vb[i];
+        for (int i = tid; i < SB * r; i += blockDim.x) sO[i] = 0.0;
+        __syncthreads();
+        for (int j = k - 1; j >= 0; --j) {
+            const double tau = taus[(long long)b * KIN_MAX + j];
+            if (tau != 0.0) {
+                const double* v = sV + (long long)j * SB;
+                double vr[SB / 32];
+#pragma unroll
+                for (int t = 0; t < SB / 32; ++t) vr[t] = v[lane + 32 * t];
+                for (int c = warp; c < r; c += nwarps) {
+                    double* o = sO + (long long)c * SB;
+                    double d = 0.0;
+#pragma unroll
+                    for (int t = 0; t < SB / 32; ++t) d += vr[t] * o[lane + 32 * t];
+                    d = warp_sum(d) + sZ[j + c * KIN_MAX];
+                    const double w = tau * d;
+#pragma unroll
+                    for (int t = 0; t < SB / 32; ++t) o[lane + 32 * t] -= w * vr[t];
+                    if (lane == 0) sZ[j + c * KIN_MAX] -= w;
+                }
+            }
+            __syncthreads();
+        }
+        write(b * SB, sO);
+    }
+}
+
+__global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ tasks, const int3* __restrict__ items,
+                                                     double* __restrict__ ws, int merge) {
+    extern __shared__ double smem[];
+    double* sZ = smem;                         // KIN_MAX x KCAP
+    double* sO = sZ + KIN_MAX * KCAP;          // SB x KCAP
+    double* sV = sO + SB * KCAP;               // SB x KIN_MAX
+    const int3 it = items[blockIdx.x];
+    const TTask& t = tasks[it.x];
+    const int side = it.y;
+    const double* hdr = ws + t.ws;
+    const int k = (int)hdr[0], r = (int)hdr[1];
+    if (k == 0 || r == 0) return;
+    const int rows = side == 0 ? t.p : t.s;
+    if (merge) {
+        const int ns = t.nseg[side];
+        if (ns <= 1) return;
+        double* mb = merge_area(t, ws, side);
+        const long long nsubm = ts_nsub(ns * KIN_MAX);
+        double* Zst = mb + nsubm * (SB * KIN_MAX + KIN_MAX) + (long long)KIN_MAX * KIN_MAX;
+        const int mrows = ns * k;
+        const int ldst = ns * KIN_MAX;
+        auto write = [&](int r0, const double* O) {
+            for (int idx = threadIdx.x; idx < SB * r; idx += blockDim.x) {
+                const int i = idx % SB, c = idx / SB;
+                if (r0 + i < mrows) Zst[r0 + i + (long long)c * ldst] = O[i + (long long)c * SB];
+            }
+        };
+        stream_apply(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, sZ, sO, sV, write);
+    } else {
+        const int s = it.z;
+        const int r0 = s * t.seg[side];
+        const int nr = min(t.seg[side], rows - r0);
+        if (nr <= 0) return;
+        const double* base = seg_area(t, ws, side, s);
+        const long long nsub = ts_nsub(t.seg[side]);
+        const double* Z0;
+        int ldz;
+        if (t.nseg[side] > 1) {
+            const long long nsubm = ts_nsub(t.nseg[side] * KIN_MAX);
+            const double* Zst = merge_area(t, ws, side) + nsubm * (SB * KIN_MAX + KIN_MAX) + (long long)KIN_MAX * KIN_MAX;
+            Z0 = Zst + (long long)s * k;
+            ldz = t.nseg[side] * KIN_MAX;
+        } else {
+            Z0 = z_area(t, ws, side);
+            ldz = KIN_MAX;
+        }
+        double* out = side == 0 ? t.ou : t.ov;
+        const int ldo = side == 0 ? t.ldou : t.ldov;
+        auto write = [&](int sub0, const double* O) {
+            for (int idx = threadIdx.x; idx < SB * r; idx += blockDim.x) {
+                const int i = idx % SB, c = idx / SB;
+                if (sub0 + i < nr) out[r0 + sub0 + i + (long long)c * ldo] = O[i + (long long)c * SB];
+            }
+        };
+        stream_apply(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, sZ, sO, sV, write);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + SB * KIN_MAX + KIN_MAX); }
+size_t trunc_smem_core() { return sizeof(double) * (2 * KIN_MAX * KIN_MAX); }
+size_t trunc_smem_apply() { return sizeof(double) * (KIN_MAX * KCAP + SB * KCAP + SB * KIN_MAX); }
+
+void trunc_init_attributes() {
+    SPG_CUDA(cudaFuncSetAttribute(k_tsqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_tsqr()));
+    SPG_CUDA(cudaFuncSetAttribute(k_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_core()));
+    SPG_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_apply()));
+}
+
+void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* status, cudaStream_t st) {
+    if (b.ntasks == 0) return;
+    k_tsqr<<<b.n_items0, TS_THREADS, trunc_smem_tsqr(), st>>>(b.d_tasks, b.d_items0, ws, status, 0);
+    SPG_LAUNCH_CHECK();
+    if (b.n_itemsm) {
+        k_tsqr<<<b.n_itemsm, TS_THREADS, trunc_smem_tsqr(), st>>>(b.d_tasks, b.d_itemsm, ws, status, 1);
+        SPG_LAUNCH_CHECK();
+    }
+    k_core<<<b.ntasks, TS_THREADS, trunc_smem_core(), st>>>(b.d_tasks, ws, eps, status);
+    SPG_LAUNCH_CHECK();
+    if (b.n_itemsm) {
+        k_apply<<<b.n_itemsm, TS_THREADS, trunc_smem_apply(), st>>>(b.d_tasks, b.d_itemsm, ws, 1);
+        SPG_LAUNCH_CHECK();
+    }
+    k_apply<<<b.n_items0, TS_THREADS, trunc_smem_apply(), st>>>(b.d_tasks, b.d_items0, ws, 0);
+    SPG_LAUNCH_CHECK();
+}
+
+}  // namespace spg
