@@ -70,6 +70,7 @@ struct TTask {
     int ldou, ldov;
     int* orank;        // output rank (may alias a group's kp)
     int skipg;         // >= 0: if group skipg has rank 0 the task is a no-op (output untouched)
+    int tag;           // op * 100000 + node (diagnostics of capacity overflows)
     int seg[2];        // segment length per side (rows)
     int nseg[2];       // segments per side
     long long ws;      // workspace base (doubles)

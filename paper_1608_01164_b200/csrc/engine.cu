@@ -131,7 +131,7 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     dtree_.begin = arena_->push(tb); dtree_.size = arena_->push(ts); dtree_.left = arena_->push(tl);
     dtree_.right = arena_->push(tr); dtree_.level = arena_->push(tv); dtree_.leaf_ord = arena_->push(to);
     // scalars
-    const size_t nsc = 32 + 32 + 256 + 8;
+    const size_t nsc = 32 + 32 + 256 + 32;
     SPG_CUDA(cudaMalloc(&scalar_mem_, nsc * sizeof(double)));
     SPG_CUDA(cudaMemset(scalar_mem_, 0, nsc * sizeof(double)));
     sc_.scal = scalar_mem_;
@@ -333,13 +333,13 @@ void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs) {
             up.p = tree_.size[l]; up.s = tree_.size[r]; up.ng = 2;
             up.g[0] = TGroup{H.upU(y), H.upV(y), tree_.n, tree_.n, H.rup(y), 0, 1.0, nullptr};
             up.g[1] = TGroup{c.QU + bl, c.QV + br, tree_.n, tree_.n, c.qrank, 0, c.s, nullptr};
-            up.ou = H.upU(y); up.ov = H.upV(y); up.ldou = up.ldov = tree_.n; up.orank = H.rup(y); up.skipg = 1;
+            up.ou = H.upU(y); up.ov = H.upV(y); up.ldou = up.ldov = tree_.n; up.orank = H.rup(y); up.skipg = 1; up.tag = cur_op_ * 100000 + 50000 + y;
             tasks.push_back(up);
             TTask lo{};
             lo.p = tree_.size[r]; lo.s = tree_.size[l]; lo.ng = 2;
             lo.g[0] = TGroup{H.loU(y), H.loV(y), tree_.n, tree_.n, H.rlo(y), 0, 1.0, nullptr};
             lo.g[1] = TGroup{c.QU + br, c.QV + bl, tree_.n, tree_.n, c.qrank, 0, c.s, nullptr};
-            lo.ou = H.loU(y); lo.ov = H.loV(y); lo.ldou = lo.ldov = tree_.n; lo.orank = H.rlo(y); lo.skipg = 1;
+            lo.ou = H.loU(y); lo.ov = H.loV(y); lo.ldou = lo.ldov = tree_.n; lo.orank = H.rlo(y); lo.skipg = 1; lo.tag = cur_op_ * 100000 + 60000 + y;
             tasks.push_back(lo);
         }
         for (int f : lv) {
@@ -410,10 +410,10 @@ void Engine::op_axpby(Plan& p, double a, const double* ap, const DHodlr& A, doub
         up.p = s1; up.s = s2; up.ng = 2; up.skipg = -1;
         up.g[0] = TGroup{A.upU(x), A.upV(x), n, n, A.rup(x), 0, a, ap};
         up.g[1] = TGroup{B.upU(x), B.upV(x), n, n, B.rup(x), 0, b, bp};
-        up.ou = C.upU(x); up.ov = C.upV(x); up.ldou = up.ldov = n; up.orank = C.rup(x);
+        up.ou = C.upU(x); up.ov = C.upV(x); up.ldou = up.ldov = n; up.orank = C.rup(x); up.tag = 100000 + x;
         tasks.push_back(up);
         TTask lo{};
-        lo.p = s2; lo.s = s1; lo.ng = 2; lo.skipg = -1;
+        lo.p = s2; lo.s = s1; lo.ng = 2; lo.skipg = -1; lo.tag = 100000 + 50000 + x;
         lo.g[0] = TGroup{A.loU(x), A.loV(x), n, n, A.rlo(x), 0, a, ap};
         lo.g[1] = TGroup{B.loU(x), B.loV(x), n, n, B.rlo(x), 0, b, bp};
         lo.ou = C.loU(x); lo.ov = C.loV(x); lo.ldou = lo.ldov = n; lo.orank = C.rlo(x);
@@ -445,7 +445,7 @@ void Engine::op_symmetrize(Plan& p, DHodlr& H) {
         up.p = s1; up.s = s2; up.ng = 2; up.skipg = -1;
         up.g[0] = TGroup{H.upU(x), H.upV(x), n, n, H.rup(x), 0, 0.5, nullptr};
         up.g[1] = TGroup{H.loV(x), H.loU(x), n, n, H.rlo(x), 0, 0.5, nullptr};   // lr_transpose(lower)
-        up.ou = H.upU(x); up.ov = H.upV(x); up.ldou = up.ldov = n; up.orank = H.rup(x);
+        up.ou = H.upU(x); up.ov = H.upV(x); up.ldou = up.ldov = n; up.orank = H.rup(x); up.tag = 200000 + x;
         tasks.push_back(up);
         // mirror: lo.U = up.V (rows r), lo.V = up.U (rows l)
         cp.push_back(CopyItem{H.upV(x), H.loU(x), s2, n, n, H.rup(x), 0, 1.0, H.rlo(x)});
@@ -504,6 +504,7 @@ void Engine::op_copy(Plan& p, const DHodlr& src, DHodlr& dst) {
 // (1) leaf products, (2) all own-term panels, (3) own-term truncations,
 // (4) ancestor products trunc(lr_multiply), (5) cascades nearest ancestor first.
 void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
+    cur_op_ = 3;
     const int n = tree_.n, D = std::max(tree_.depth, 1);
     // (1) leaves
     {
@@ -554,13 +555,13 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
             up.p = s1; up.s = s2; up.ng = 2; up.skipg = -1;
             up.g[0] = TGroup{T1 + t * slab + bl, B.upV(x), n, n, B.rup(x), 0, 1.0, nullptr};
             up.g[1] = TGroup{A.upU(x), T2 + t * slab + br, n, n, A.rup(x), 0, 1.0, nullptr};
-            up.ou = C.upU(x); up.ov = C.upV(x); up.ldou = up.ldov = n; up.orank = C.rup(x);
+            up.ou = C.upU(x); up.ov = C.upV(x); up.ldou = up.ldov = n; up.orank = C.rup(x); up.tag = 300000 + x;
             tasks.push_back(up);
             TTask lo{};
             lo.p = s2; lo.s = s1; lo.ng = 2; lo.skipg = -1;
             lo.g[0] = TGroup{A.loU(x), U1 + t * slab + bl, n, n, A.rlo(x), 0, 1.0, nullptr};
             lo.g[1] = TGroup{U2 + t * slab + br, B.loV(x), n, n, B.rlo(x), 0, 1.0, nullptr};
-            lo.ou = C.loU(x); lo.ov = C.loV(x); lo.ldou = lo.ldov = n; lo.orank = C.rlo(x);
+            lo.ou = C.loU(x); lo.ov = C.loV(x); lo.ldou = lo.ldov = n; lo.orank = C.rlo(x); lo.tag = 350000 + x;
             tasks.push_back(lo);
         }
         trunc(p, tasks);
@@ -593,12 +594,12 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
             TTask ql{};
             ql.p = s1; ql.s = s1; ql.ng = 1; ql.skipg = -1;
             ql.g[0] = TGroup{QP + t * slab + bl, B.loV(x), n, n, qpr + 2 * x, 0, 1.0, nullptr};
-            ql.ou = QU + t * slab + bl; ql.ov = QV + t * slab + bl; ql.ldou = ql.ldov = n; ql.orank = qr + 2 * x;
+            ql.tag = 400000 + x; ql.ou = QU + t * slab + bl; ql.ov = QV + t * slab + bl; ql.ldou = ql.ldov = n; ql.orank = qr + 2 * x;
             tasks.push_back(ql);
             TTask qrt{};
             qrt.p = s2; qrt.s = s2; qrt.ng = 1; qrt.skipg = -1;
             qrt.g[0] = TGroup{QP + t * slab + br, B.upV(x), n, n, qpr + 2 * x + 1, 0, 1.0, nullptr};
-            qrt.ou = QU + t * slab + br; qrt.ov = QV + t * slab + br; qrt.ldou = qrt.ldov = n; qrt.orank = qr + 2 * x + 1;
+            qrt.tag = 450000 + x; qrt.ou = QU + t * slab + br; qrt.ov = QV + t * slab + br; qrt.ldou = qrt.ldov = n; qrt.orank = qr + 2 * x + 1;
             tasks.push_back(qrt);
         }
         gemm(p, g1, c1);
@@ -620,6 +621,7 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
 
 // hodlr_cholesky (hodlr.hpp:540-574)
 void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work) {
+    cur_op_ = 6;
     op_copy(p, M, work);
     const DHodlr* Wp = &W;
     p.launches.push_back([Wp](cudaStream_t st) { Wp->zero(st); });
@@ -648,7 +650,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
         TTask tk{};
         tk.p = s1; tk.s = s2; tk.ng = 1; tk.skipg = -1;
         tk.g[0] = TGroup{P0 + bl, M.upV(x), n, n, M.rup(x), 0, 1.0, nullptr};
-        tk.ou = W.upU(x); tk.ov = W.upV(x); tk.ldou = tk.ldov = n; tk.orank = W.rup(x);
+        tk.ou = W.upU(x); tk.ov = W.upV(x); tk.ldou = tk.ldov = n; tk.orank = W.rup(x); tk.tag = 600000 + x;
         trunc(p, {tk});
     }
     // Schur: M22 -= V (U^T U) V^T
@@ -666,6 +668,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
 
 // solve_upper_right (hodlr.hpp:579-604, 641-647): Y W = B
 void Engine::op_solve_upper_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work) {
+    cur_op_ = 7;
     op_copy(p, B, work);
     sur_rec(p, 0, work, W, Y);
 }
@@ -706,7 +709,7 @@ void Engine::sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         tk.p = s1; tk.s = s2; tk.ng = 2; tk.skipg = -1;
         tk.g[0] = TGroup{B.upU(x), B.upV(x), n, n, B.rup(x), 0, 1.0, nullptr};
         tk.g[1] = TGroup{P0 + bl, W.upV(x), n, n, W.rup(x), 0, -1.0, nullptr};
-        tk.ou = Y.upU(x); tk.ov = Y.upV(x); tk.ldou = tk.ldov = n; tk.orank = Y.rup(x);
+        tk.ou = Y.upU(x); tk.ov = Y.upV(x); tk.ldou = tk.ldov = n; tk.orank = Y.rup(x); tk.tag = 700000 + x;
         trunc(p, {tk});
     }
     hsolve(p, W, {HSolveItem{r, Y.upV(x), n, Y.rup(x), 0, 0}});
@@ -726,7 +729,7 @@ void Engine::sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         TTask tk{};
         tk.p = s2; tk.s = s2; tk.ng = 1; tk.skipg = -1;
         tk.g[0] = TGroup{P1 + br, W.upV(x), n, n, q0, 0, 1.0, nullptr};
-        tk.ou = P2 + br; tk.ov = P3 + br; tk.ldou = tk.ldov = n; tk.orank = q1;
+        tk.ou = P2 + br; tk.ov = P3 + br; tk.ldou = tk.ldov = n; tk.orank = q1; tk.tag = 750000 + x;
         trunc(p, {tk});
         cascade(p, B, {Cascade{r, P2, P3, q1, -1.0}});
     }
@@ -735,6 +738,7 @@ void Engine::sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
 
 // solve_upperT_right (hodlr.hpp:607-636, 650-656): Y W^T = B
 void Engine::op_solve_upperT_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work) {
+    cur_op_ = 8;
     op_copy(p, B, work);
     surt_rec(p, 0, work, W, Y);
 }
@@ -783,7 +787,7 @@ void Engine::surt_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         TTask tk{};
         tk.p = s1; tk.s = s1; tk.ng = 1; tk.skipg = -1;
         tk.g[0] = TGroup{P1 + bl, W.upU(x), n, n, q0, 0, 1.0, nullptr};
-        tk.ou = P2 + bl; tk.ov = P3 + bl; tk.ldou = tk.ldov = n; tk.orank = q1;
+        tk.ou = P2 + bl; tk.ov = P3 + bl; tk.ldou = tk.ldov = n; tk.orank = q1; tk.tag = 850000 + x;
         trunc(p, {tk});
         cascade(p, B, {Cascade{l, P2, P3, q1, -1.0}});
     }
@@ -796,7 +800,7 @@ void Engine::surt_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         tk.p = s2; tk.s = s1; tk.ng = 2; tk.skipg = -1;
         tk.g[0] = TGroup{B.loU(x), B.loV(x), n, n, B.rlo(x), 0, 1.0, nullptr};
         tk.g[1] = TGroup{P0 + br, W.upU(x), n, n, W.rup(x), 0, -1.0, nullptr};
-        tk.ou = Y.loU(x); tk.ov = Y.loV(x); tk.ldou = tk.ldov = n; tk.orank = Y.rlo(x);
+        tk.ou = Y.loU(x); tk.ov = Y.loV(x); tk.ldou = tk.ldov = n; tk.orank = Y.rlo(x); tk.tag = 800000 + x;
         trunc(p, {tk});
     }
     hsolve(p, W, {HSolveItem{l, Y.loV(x), n, Y.rlo(x), 0, 1}});

@@ -181,6 +181,7 @@ private:
     double* coef_ = nullptr;    // per-node coefficient blocks (KCAP x KCAP)
     int* iranks_ = nullptr;     // scratch ranks (4 * nnodes)
     std::vector<std::unique_ptr<DHodlr>> owned_;
+    int cur_op_ = 0;
 };
 
 }  // namespace spg

@@ -149,12 +149,24 @@ __global__ void k_trace(DevTree t, DevHodlrView H, double* out) {
     *out = tr;
 }
 
-int check_status(unsigned st) {
+int check_status(const unsigned* blk) {
+    const unsigned st = blk[0];
+    const int* dbg = reinterpret_cast<const int*>(blk + 4);
     if (st & ST_NPD) throw StatusError(SPG_NOT_POSITIVE_DEFINITE, "hodlr_cholesky: leaf factorization failed");
     if (st & ST_SINGULAR) throw StatusError(SPG_SINGULAR, "triangular solve / banded LU: zero pivot");
     if (st & (ST_RANK_CAP | ST_KIN_CAP))
-        throw StatusError(SPG_RANK_CAPACITY, "off-diagonal rank exceeded the compiled capacity KCAP=" + std::to_string(KCAP));
+        throw StatusError(SPG_RANK_CAPACITY,
+                          "off-diagonal rank exceeded the compiled capacity KCAP=" + std::to_string(KCAP) +
+                              " (first overflow: tag " + std::to_string(dbg[0] - 1) + " p " + std::to_string(dbg[1]) +
+                              " s " + std::to_string(dbg[2]) + " k_in " + std::to_string(dbg[3]) + " r " +
+                              std::to_string(dbg[4]) + "; k_in overflow tag " + std::to_string(dbg[5] - 1) + " k " +
+                              std::to_string(dbg[6]) + ")");
     return 0;
+}
+int check_status_dev(const unsigned* d) {
+    unsigned blk[16];
+    SPG_CUDA(cudaMemcpy(blk, d, sizeof(blk), cudaMemcpyDeviceToHost));
+    return check_status(blk);
 }
 
 enum Phase { PH_SETUP, PH_FIRST, PH_MUL, PH_CHOL, PH_SOLVE, PH_SOLVET, PH_AXPBY, PH_NPH };
@@ -308,7 +320,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         p.launches.push_back([t_start](cudaStream_t s) { SPG_CUDA(cudaEventRecord(t_start, s)); });
         timed(p, PH_SETUP, [&]() {
             p.launches.push_back([=](cudaStream_t s) {
-                SPG_CUDA(cudaMemsetAsync(S.status, 0, sizeof(unsigned), s));
+                SPG_CUDA(cudaMemsetAsync(S.status, 0, 14 * sizeof(unsigned), s));
                 SPG_CUDA(cudaMemsetAsync(S.counter, 0, sizeof(int), s));
                 SPG_CUDA(cudaMemcpyAsync(d_bands, bands_host, sizeof(double) * blen, cudaMemcpyHostToDevice, s));
                 launch_estimate_2norm(n, b, d_bands, d_tmp, s);            // d_tmp[0] = alpha
@@ -424,8 +436,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     }
     SPG_CUDA(cudaStreamSynchronize(st));
     SPG_CUDA(cudaGetLastError());
-    SPG_CUDA(cudaMemcpy(&status, S.status, sizeof(unsigned), cudaMemcpyDeviceToHost));
-    check_status(status);
+    check_status_dev(S.status);
 
     // ---------------- report
     spg_info& I = R->info;
@@ -698,7 +709,7 @@ int spg_ctx_op(spg_ctx* c, int op, int dst, int a, int b, double alpha, double b
     return guarded([&]() {
         Engine& E = *c->eng;
         cudaStream_t st = E.stream();
-        SPG_CUDA(cudaMemsetAsync(E.sc().status, 0, sizeof(unsigned), st));
+        SPG_CUDA(cudaMemsetAsync(E.sc().status, 0, 14 * sizeof(unsigned), st));
         Plan p;
         DHodlr& D = *c->slots.at(dst);
         switch (op) {
@@ -714,9 +725,7 @@ int spg_ctx_op(spg_ctx* c, int op, int dst, int a, int b, double alpha, double b
         E.arena().commit(st);
         p.run(st);
         SPG_CUDA(cudaStreamSynchronize(st));
-        unsigned s = 0;
-        SPG_CUDA(cudaMemcpy(&s, E.sc().status, sizeof(unsigned), cudaMemcpyDeviceToHost));
-        check_status(s);
+        check_status_dev(E.sc().status);
     });
 }
 
@@ -738,7 +747,7 @@ int spg_truncate(int p, int s, int k, const double* U, const double* V, double e
         SPG_CUDA(cudaMalloc(&dr, sizeof(int)));
         SPG_CUDA(cudaMemcpy(du, cu.data(), sizeof(double) * cu.size(), cudaMemcpyHostToDevice));
         SPG_CUDA(cudaMemcpy(dv, cv.data(), sizeof(double) * cv.size(), cudaMemcpyHostToDevice));
-        SPG_CUDA(cudaMemset(E.sc().status, 0, sizeof(unsigned)));
+        SPG_CUDA(cudaMemset(E.sc().status, 0, 14 * sizeof(unsigned)));
         TTask t{};
         t.p = p; t.s = s; t.ng = 1; t.skipg = -1;
         t.g[0] = TGroup{du, dv, p, s, nullptr, k, 1.0, nullptr};
@@ -750,8 +759,7 @@ int spg_truncate(int p, int s, int k, const double* U, const double* V, double e
         SPG_CUDA(cudaStreamSynchronize(st));
         int rr = 0;
         SPG_CUDA(cudaMemcpy(&rr, dr, sizeof(int), cudaMemcpyDeviceToHost));
-        unsigned stt = 0;
-        SPG_CUDA(cudaMemcpy(&stt, E.sc().status, sizeof(unsigned), cudaMemcpyDeviceToHost));
+
         std::vector<double> hu((size_t)p * KCAP), hv((size_t)s * KCAP);
         SPG_CUDA(cudaMemcpy(hu.data(), ou, sizeof(double) * hu.size(), cudaMemcpyDeviceToHost));
         SPG_CUDA(cudaMemcpy(hv.data(), ov, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost));
@@ -759,7 +767,7 @@ int spg_truncate(int p, int s, int k, const double* U, const double* V, double e
         for (int i = 0; i < s; ++i) for (int j = 0; j < rr; ++j) Vo[(size_t)i * k + j] = hv[i + (size_t)j * s];
         *r = rr;
         cudaFree(du); cudaFree(dv); cudaFree(ou); cudaFree(ov); cudaFree(dr);
-        check_status(stt);
+        check_status_dev(E.sc().status);
     });
 }
 

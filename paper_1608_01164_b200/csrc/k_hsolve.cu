@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(HS_THREADS) k_hsolve(DevTree t, DevHodlrView W
                 __syncthreads();
                 for (int idx = tid; idx < nr * k; idx += blockDim.x) {
                     const int i = idx % nr, a = idx / nr;
-                    sU[i + a * HS_CH] = Pin[rin0 + ch + i + (long long)a * W.n];
+                    sU[i + a * HS_CH] = Pin[ch + i + (long long)a * W.n];   // Pin starts at row rin0
                 }
                 for (int idx = tid; idx < nr * ncols; idx += blockDim.x) {
                     const int i = idx % nr, c = idx / nr;
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(HS_THREADS) k_hsolve(DevTree t, DevHodlrView W
             for (int idx = tid; idx < nout * ncols; idx += blockDim.x) {
                 const int i = idx % nout, c = idx / nout;
                 double s = 0.0;
-                for (int a = 0; a < k; ++a) s += Pout[rout0 + i + (long long)a * W.n] * sG[a + c * KCAP];
+                for (int a = 0; a < k; ++a) s += Pout[i + (long long)a * W.n] * sG[a + c * KCAP];   // Pout starts at row rout0
                 X(rout0 + i, c) -= s;
             }
             __syncthreads();

@@ -142,7 +142,14 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
     const int side = it.y;
     if (task_skip(t)) return;
     int k = task_kin(t);
-    if (k > KIN_MAX) { if (threadIdx.x == 0) atomicOr(status, ST_KIN_CAP); k = KIN_MAX; }
+    if (k > KIN_MAX) {
+        if (threadIdx.x == 0) {
+            atomicOr(status, ST_KIN_CAP);
+            int* dbg = reinterpret_cast<int*>(status + 4);
+            dbg[5] = t.tag + 1; dbg[6] = k;
+        }
+        k = KIN_MAX;
+    }
     if (k == 0) return;
     const int rows = side == 0 ? t.p : t.s;
     if (!merge) {
@@ -200,6 +207,7 @@ __device__ __forceinline__ const double* final_R(const TTask& t, double* ws, int
 // one CTA per task: C = R_u R_v^T, parallel one-sided Jacobi, sort, threshold
 __global__ void __launch_bounds__(TS_THREADS) k_core(const TTask* __restrict__ tasks, double* __restrict__ ws,
                                                     double eps, unsigned* status) {
+    int* dbg = reinterpret_cast<int*>(status + 4);   // first overflow: tag, p, s, k_in, r_full
     extern __shared__ double smem[];
     double* sW = smem;                       // k x k (ld KIN_MAX)
     double* sV = sW + KIN_MAX * KIN_MAX;     // k x k
@@ -310,7 +318,12 @@ __global__ void __launch_bounds__(TS_THREADS) k_core(const TTask* __restrict__ t
     if (tid == 0) {
         int r = 0;
         while (r < k && sSig[sPerm[r]] > eps) ++r;
-        if (r > KCAP) { atomicOr(status, ST_RANK_CAP); r = KCAP; }
+        if (r > KCAP) {
+            if (atomicOr(status, ST_RANK_CAP) == 0 || dbg[0] == 0) {
+                dbg[0] = t.tag + 1; dbg[1] = t.p; dbg[2] = t.s; dbg[3] = k; dbg[4] = r;
+            }
+            r = KCAP;
+        }
         sR_ = r;
         hdr[0] = k; hdr[1] = r;
         if (!(sSig[sPerm[0]] == sSig[sPerm[0]])) atomicOr(status, ST_NONFINITE);
