@@ -63,6 +63,14 @@ typedef struct spg_info {
     long long memory_bytes;/* diagnostics(P).memory_bytes */
     double trace;          /* hodlr_trace(P) */
     int kcap;              /* compiled rank capacity */
+    /* device counters (always on) */
+    double trunc_bytes;    /* recompression algorithmic bytes: sum 8 (p+s)(k_in+k_out) */
+    double gemm_flops;     /* GEMM algorithmic flops: sum 2 M N K over batched GEMM items */
+    long long trunc_tasks; /* truncations executed */
+    /* profile mode only (spg_set_profile(1)): per-class device time from CUDA events */
+    int profiled;
+    double prof_ms_trunc, prof_ms_gemm, prof_ms_hsolve, prof_ms_leaf;
+    long long prof_batches_trunc, prof_batches_gemm, prof_batches_hsolve, prof_batches_leaf;
 } spg_info;
 
 /* Runs the hQDWH projector on device 0 (current device).  `bands` is host
@@ -81,6 +89,9 @@ int spg_result_export(const spg_result* r, int which, int* ranks, double* data);
 int spg_result_apply(const spg_result* r, int which, int m, const double* X, double* Y);
 void spg_result_free(spg_result* r);
 
+/* profile mode (process-wide): bracket every batched launch with CUDA events */
+void spg_set_profile(int on);
+
 /* thread-local message of the last failing call */
 const char* spg_last_error(void);
 
@@ -97,6 +108,8 @@ int spg_make_dimer_chain(int n, int b, double t1, double t2, double eps_dis, dou
                          double* bands);
 /* generic random banded input (test_hodlr.cpp:19-26 convention) */
 int spg_make_random_banded(int n, int b, unsigned long long seed, double* bands);
+/* FP64 tensor-pipe (DMMA) throughput probe on device 0, TFLOP/s (roofline denominator) */
+int spg_measure_dmma_tflops(double* out);
 /* compiled capacities */
 int spg_kcap(void);
 

@@ -32,7 +32,7 @@ __all__ = [
     "BandedSymmetric", "PartitionTree", "HodlrMatrix", "ProjectorResult", "IterationDiag",
     "hqdwh", "make_tree", "qdwh_params", "l_update", "truncate", "dimer_chain", "random_banded",
     "HodlrContext", "NotPositiveDefiniteError", "SingularMatrixError", "RankCapacityError",
-    "NoDeviceError", "lib_path", "load_library",
+    "NoDeviceError", "lib_path", "load_library", "set_profile",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -76,7 +76,12 @@ class _Info(C.Structure):
                 ("ms_setup", C.c_double), ("ms_first", C.c_double), ("ms_multiply", C.c_double),
                 ("ms_cholesky", C.c_double), ("ms_solve", C.c_double), ("ms_solveT", C.c_double),
                 ("ms_axpby_sym", C.c_double), ("launches", C.c_longlong), ("max_rank", C.c_int),
-                ("memory_bytes", C.c_longlong), ("trace", C.c_double), ("kcap", C.c_int)]
+                ("memory_bytes", C.c_longlong), ("trace", C.c_double), ("kcap", C.c_int),
+                ("trunc_bytes", C.c_double), ("gemm_flops", C.c_double), ("trunc_tasks", C.c_longlong),
+                ("profiled", C.c_int), ("prof_ms_trunc", C.c_double), ("prof_ms_gemm", C.c_double),
+                ("prof_ms_hsolve", C.c_double), ("prof_ms_leaf", C.c_double),
+                ("prof_batches_trunc", C.c_longlong), ("prof_batches_gemm", C.c_longlong),
+                ("prof_batches_hsolve", C.c_longlong), ("prof_batches_leaf", C.c_longlong)]
 
 
 class _Diag(C.Structure):
@@ -92,7 +97,7 @@ ABI_SYMBOLS = (
     "spg_result_apply", "spg_result_free", "spg_last_error", "spg_tree", "spg_qdwh_params", "spg_l_update",
     "spg_make_dimer_chain", "spg_make_random_banded", "spg_kcap", "spg_ctx_create", "spg_ctx_free",
     "spg_ctx_upload", "spg_ctx_flat_size", "spg_ctx_download", "spg_ctx_op", "spg_ctx_from_banded",
-    "spg_truncate",
+    "spg_truncate", "spg_set_profile", "spg_measure_dmma_tflops",
 )
 
 
@@ -130,6 +135,8 @@ def load_library(path: str | None = None):
         "spg_ctx_op": ([vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double], C.c_int),
         "spg_ctx_from_banded": ([vp, C.c_int, C.c_int, _dp], C.c_int),
         "spg_truncate": ([C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double, _dp, _dp, _ip], C.c_int),
+        "spg_set_profile": ([C.c_int], None),
+        "spg_measure_dmma_tflops": ([_dp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -416,14 +423,16 @@ class ProjectorResult:
             pass
 
 
-def hqdwh(A: BandedSymmetric, n_min: int, eps: float, delta: float = 1e-15) -> ProjectorResult:
+def hqdwh(A: BandedSymmetric, n_min: int, eps: float, delta: float = 1e-15, packed=None) -> ProjectorResult:
     """hqdwh (qdwh.hpp:196-241) on the B200: spectral projector onto the negative
-    eigenvalues of A.  Raises the reference's exception types."""
-    if not A.all_finite():
-        raise ValueError("hqdwh: nonfinite input")
+    eigenvalues of A.  Raises the reference's exception types.  ``packed`` may be
+    a caller-owned (e.g. pinned) float64 buffer already holding ``A.packed()``."""
     L = load_library()
     h = C.c_void_p()
-    packed = A.packed()
+    if packed is None:
+        if not A.all_finite():
+            raise ValueError("hqdwh: nonfinite input")
+        packed = A.packed()
     _raise(L.spg_hqdwh(A.n, A.b, _d(packed), n_min, eps, delta, C.byref(h)))
     info = _Info()
     _raise(L.spg_result_info(h, C.byref(info)))
@@ -432,6 +441,18 @@ def hqdwh(A: BandedSymmetric, n_min: int, eps: float, delta: float = 1e-15) -> P
     per = [IterationDiag(d.k, d.l, d.c, d.max_rank, d.memory_bytes, d.wall_ms) for d in diag[:info.iterations]]
     infod = {name: getattr(info, name) for name, _ in _Info._fields_}
     return ProjectorResult(info.iterations, info.alpha, info.l0, per, infod, h, PartitionTree(A.n, n_min))
+
+
+def set_profile(on: bool = True):
+    """Profile mode: bracket every batched launch with CUDA events (per-class device times in info)."""
+    load_library().spg_set_profile(1 if on else 0)
+
+
+def measure_dmma_tflops() -> float:
+    """Measured FP64 tensor-pipe (DMMA.8x8x4) throughput of device 0 in TFLOP/s."""
+    out = np.zeros(1)
+    _raise(load_library().spg_measure_dmma_tflops(_d(out)))
+    return float(out[0])
 
 
 def qdwh_params(l):

@@ -140,6 +140,7 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     sc_.count = reinterpret_cast<int*>(scalar_mem_ + 320);
     sc_.counter = sc_.count + 1;
     sc_.status = reinterpret_cast<unsigned*>(sc_.count + 2);
+    sc_.counters = reinterpret_cast<double*>(sc_.status + 16);
     // persistent panels and coefficient blocks
     for (int i = 0; i < 4; ++i) {
         double* p;
@@ -151,7 +152,34 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     arena_->commit(st_);
 }
 
+void Engine::push_timed(Plan& p, int cls, Launch l) {
+    if (!profile_) { p.launches.push_back(std::move(l)); return; }
+    cudaEvent_t a, b;
+    SPG_CUDA(cudaEventCreate(&a));
+    SPG_CUDA(cudaEventCreate(&b));
+    prof_.push_back({cls, a, b});
+    p.launches.push_back([a](cudaStream_t s) { SPG_CUDA(cudaEventRecord(a, s)); });
+    p.launches.push_back(std::move(l));
+    p.launches.push_back([b](cudaStream_t s) { SPG_CUDA(cudaEventRecord(b, s)); });
+}
+
+void Engine::prof_sum(double* ms, long long* nb) const {
+    for (int c = 0; c < PC_NCLS; ++c) { ms[c] = 0.0; nb[c] = 0; }
+    for (const auto& r : prof_) {
+        float t = 0.f;
+        SPG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        ms[r.cls] += t;
+        nb[r.cls] += 1;
+    }
+}
+
+void Engine::prof_clear() {
+    for (auto& r : prof_) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    prof_.clear();
+}
+
 Engine::~Engine() {
+    prof_clear();
     owned_.clear();
     for (double* p : panels_) cudaFree(p);
     if (coef_) cudaFree(coef_);
@@ -206,7 +234,7 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     double* ws = ws_->base();
     const double eps = eps_;
     unsigned* status = sc_.status;
-    p.launches.push_back([b, ws, eps, status](cudaStream_t st) { launch_truncate(b, ws, eps, status, st); });
+    push_timed(p, PC_TRUNC, [b, ws, eps, status](cudaStream_t st) { launch_truncate(b, ws, eps, status, st); });
     ws_->release(mark);
 }
 
@@ -240,7 +268,8 @@ void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>&
     b.nctas = (int)ctas.size();
     b.d_red_items = arena_->push(red);
     b.nred = (int)red.size();
-    p.launches.push_back([b](cudaStream_t st) { launch_gemm(b, st); });
+    b.flops = sc_.counters + 1;
+    push_timed(p, PC_GEMM, [b](cudaStream_t st) { launch_gemm(b, st); });
     ws_->release(mark);
 }
 
@@ -352,7 +381,7 @@ void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs) {
     if (!upd.empty()) {
         const LowRankUpd* d = arena_->push(upd);
         const int ni = (int)upd.size();
-        p.launches.push_back([d, ni, maxm](cudaStream_t st) { launch_lowrank_update(d, ni, maxm, st); });
+        push_timed(p, PC_LEAF, [d, ni, maxm](cudaStream_t st) { launch_lowrank_update(d, ni, maxm, st); });
     }
 }
 
@@ -367,7 +396,7 @@ void Engine::hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items) {
     const DevTree dt = dtree_;
     const DevHodlrView wv = W.view();
     unsigned* status = sc_.status;
-    p.launches.push_back([dt, wv, d, dc, nc, status](cudaStream_t st) { launch_hsolve(dt, wv, d, dc, nc, status, st); });
+    push_timed(p, PC_HSOLVE, [dt, wv, d, dc, nc, status](cudaStream_t st) { launch_hsolve(dt, wv, d, dc, nc, status, st); });
 }
 
 void Engine::copy(Plan& p, std::vector<CopyItem> items, int maxm, int maxk) {
@@ -635,7 +664,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
         std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s}};
         const CholItem* d = arena_->push(ci);
         unsigned* status = sc_.status;
-        p.launches.push_back([d, status](cudaStream_t st) { launch_leaf_cholesky(d, 1, status, st); });
+        push_timed(p, PC_LEAF, [d, status](cudaStream_t st) { launch_leaf_cholesky(d, 1, status, st); });
         return;
     }
     const int l = tree_.left[x], r = tree_.right[x];
@@ -689,7 +718,7 @@ void Engine::sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         const int2* dc = arena_->push(ct);
         const int nc = (int)ct.size();
         unsigned* status = sc_.status;
-        p.launches.push_back([=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
+        push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
         return;
     }
     const int l = tree_.left[x], r = tree_.right[x];
@@ -759,7 +788,7 @@ void Engine::surt_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         const int2* dc = arena_->push(ct);
         const int nc = (int)ct.size();
         unsigned* status = sc_.status;
-        p.launches.push_back([=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
+        push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
         return;
     }
     const int l = tree_.left[x], r = tree_.right[x];

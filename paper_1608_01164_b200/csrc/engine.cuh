@@ -122,8 +122,12 @@ struct Scalars {          // device scalar block
     double* sched;        // 4 * 64
     int* count;
     int* counter;
-    unsigned* status;
+    unsigned* status;     // status word + overflow diagnostics (16 ints)
+    double* counters;     // [0] recompression bytes 8(p+s)(k_in+k_out) [1] GEMM flops 2MNK [2] truncation tasks
 };
+
+// kernel classes timed with CUDA events in profile mode
+enum ProfClass { PC_TRUNC = 0, PC_GEMM, PC_HSOLVE, PC_LEAF, PC_NCLS };
 
 class Engine {
 public:
@@ -163,6 +167,13 @@ public:
 
     std::unique_ptr<DHodlr> new_hodlr();
 
+    // profile mode: every batch is bracketed by a pair of CUDA events (plans are then not replayed)
+    void set_profile(bool on) { profile_ = on; }
+    bool profile() const { return profile_; }
+    void prof_sum(double* ms_per_class, long long* batches_per_class) const;
+    void prof_clear();
+    void push_timed(Plan& p, int cls, Launch l);
+
 private:
     void chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W);
     void sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y);
@@ -182,6 +193,9 @@ private:
     int* iranks_ = nullptr;     // scratch ranks (4 * nnodes)
     std::vector<std::unique_ptr<DHodlr>> owned_;
     int cur_op_ = 0;
+    bool profile_ = false;
+    struct ProfRec { int cls; cudaEvent_t a, b; };
+    std::vector<ProfRec> prof_;
 };
 
 }  // namespace spg

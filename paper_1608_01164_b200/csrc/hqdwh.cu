@@ -22,7 +22,9 @@
 #include "engine.cuh"
 
 namespace spg {
+double measure_dmma_tflops();
 std::atomic<long long> g_launches{0};
+std::atomic<int> g_profile{0};
 }
 
 using namespace spg;
@@ -257,6 +259,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     auto R = std::make_unique<spg_result>();
     R->eng = std::make_unique<Engine>(n, n_min, eps);
     Engine& E = *R->eng;
+    E.set_profile(g_profile.load() != 0);
     check_tree(E.tree());
     cudaStream_t st = E.stream();
     const long long launches0 = g_launches.load();
@@ -322,6 +325,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
             p.launches.push_back([=](cudaStream_t s) {
                 SPG_CUDA(cudaMemsetAsync(S.status, 0, 14 * sizeof(unsigned), s));
                 SPG_CUDA(cudaMemsetAsync(S.counter, 0, sizeof(int), s));
+                SPG_CUDA(cudaMemsetAsync(S.counters, 0, 4 * sizeof(double), s));
                 SPG_CUDA(cudaMemcpyAsync(d_bands, bands_host, sizeof(double) * blen, cudaMemcpyHostToDevice, s));
                 launch_estimate_2norm(n, b, d_bands, d_tmp, s);            // d_tmp[0] = alpha
                 SPG_CUDA(cudaMemcpyAsync(S.scal, d_tmp, sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -396,25 +400,29 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         commit_run(p);
     }
 
-    // ---------------- k >= 1: Cholesky-based iterates (one plan, replayed)
+    // ---------------- k >= 1: Cholesky-based iterates (one plan, replayed; rebuilt per run in profile mode)
     if (count >= 2) {
+        auto build_iter = [&](Plan& p) {
+            timed(p, PH_MUL, [&]() {
+                p.launches.push_back([=](cudaStream_t s) { launch_iter_params(S.sched, S.counter, S.slots, S.scal, s); });
+                E.op_multiply(p, *X, *X, *Z);
+                E.op_scale_shift(p, *Z, 1.0, S.slots + 0, 1.0);
+            });
+            timed(p, PH_CHOL, [&]() { E.op_cholesky(p, *Z, *W, *WK); });
+            timed(p, PH_SOLVE, [&]() { E.op_solve_upper_right(p, *X, *W, *Y, *WK); });
+            timed(p, PH_SOLVET, [&]() { E.op_solve_upperT_right(p, *Y, *W, *V, *WK); });
+            timed(p, PH_AXPBY, [&]() {
+                E.op_axpby(p, 1.0, S.slots + 1, *X, 1.0, S.slots + 2, *V, *X);
+                E.op_symmetrize(p, *X);
+            });
+            push_diag(p);
+            E.arena().commit(st);
+        };
         Plan p;
-        timed(p, PH_MUL, [&]() {
-            p.launches.push_back([=](cudaStream_t s) { launch_iter_params(S.sched, S.counter, S.slots, S.scal, s); });
-            E.op_multiply(p, *X, *X, *Z);
-            E.op_scale_shift(p, *Z, 1.0, S.slots + 0, 1.0);
-        });
-        timed(p, PH_CHOL, [&]() { E.op_cholesky(p, *Z, *W, *WK); });
-        timed(p, PH_SOLVE, [&]() { E.op_solve_upper_right(p, *X, *W, *Y, *WK); });
-        timed(p, PH_SOLVET, [&]() { E.op_solve_upperT_right(p, *Y, *W, *V, *WK); });
-        timed(p, PH_AXPBY, [&]() {
-            E.op_axpby(p, 1.0, S.slots + 1, *X, 1.0, S.slots + 2, *V, *X);
-            E.op_symmetrize(p, *X);
-        });
-        push_diag(p);
-        E.arena().commit(st);
+        if (!E.profile()) build_iter(p);
         for (int k = 1; k < count; ++k) {
             cur_run = k;
+            if (E.profile()) { p = Plan(); build_iter(p); }
             cudaEvent_t e0 = mkev();
             it_ev.push_back(e0);
             SPG_CUDA(cudaEventRecord(e0, st));
@@ -477,6 +485,24 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         R->diag.push_back(d);
     }
     I.launches = g_launches.load() - launches0;
+    {
+        double ctr[3];
+        SPG_CUDA(cudaMemcpy(ctr, S.counters, sizeof(ctr), cudaMemcpyDeviceToHost));
+        I.trunc_bytes = ctr[0];
+        I.gemm_flops = ctr[1];
+        I.trunc_tasks = (long long)ctr[2];
+        if (E.profile()) {
+            double pm[PC_NCLS];
+            long long pb[PC_NCLS];
+            E.prof_sum(pm, pb);
+            I.profiled = 1;
+            I.prof_ms_trunc = pm[PC_TRUNC]; I.prof_ms_gemm = pm[PC_GEMM];
+            I.prof_ms_hsolve = pm[PC_HSOLVE]; I.prof_ms_leaf = pm[PC_LEAF];
+            I.prof_batches_trunc = pb[PC_TRUNC]; I.prof_batches_gemm = pb[PC_GEMM];
+            I.prof_batches_hsolve = pb[PC_HSOLVE]; I.prof_batches_leaf = pb[PC_LEAF];
+            E.prof_clear();
+        }
+    }
     // diagnostics of P
     {
         std::vector<int> rk(2 * E.tree().nnodes());
@@ -540,6 +566,14 @@ int ensure_device() {
 extern "C" {
 
 const char* spg_last_error(void) { return g_err.c_str(); }
+void spg_set_profile(int on) { g_profile.store(on ? 1 : 0); }
+
+int spg_measure_dmma_tflops(double* out) {
+    return guarded([&]() {
+        ensure_device();
+        *out = measure_dmma_tflops();
+    });
+}
 int spg_kcap(void) { return KCAP; }
 
 int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double delta, spg_result** out) {

@@ -22,13 +22,15 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 
 __device__ __forceinline__ int dimv(int c, const int* p) { return p ? *p : c; }
 
-__global__ void __launch_bounds__(G_THREADS) k_gemm(const GemmItem* __restrict__ items, const int4* __restrict__ ctas) {
+__global__ void __launch_bounds__(G_THREADS) k_gemm(const GemmItem* __restrict__ items, const int4* __restrict__ ctas,
+                                                  double* flops) {
     __shared__ double As[GBK][GBM + GPAD];
     __shared__ double Bs[GBK][GBN + GPAD];
     const int4 cm = ctas[blockIdx.x];
     const GemmItem& g = items[cm.x];
     const int M = dimv(g.M, g.Mp), N = dimv(g.N, g.Np), K = dimv(g.K, g.Kp);
     const int m0 = cm.y * GBM, n0 = cm.z * GBN;
+    if (flops && cm.y == 0 && cm.z == 0 && cm.w == 0 && threadIdx.x == 0) atomicAdd(flops, 2.0 * M * N * K);
     if (m0 >= M || n0 >= N) return;
     const bool split = g.nsplit > 1;
     int kbeg = 0, kend = K;
@@ -117,7 +119,7 @@ __global__ void k_gemm_reduce(const GemmItem* __restrict__ items, const int* __r
 
 void launch_gemm(const GemmBatch& b, cudaStream_t st) {
     if (b.nctas == 0) return;
-    k_gemm<<<b.nctas, G_THREADS, 0, st>>>(b.d_items, b.d_ctas);
+    k_gemm<<<b.nctas, G_THREADS, 0, st>>>(b.d_items, b.d_ctas, b.flops);
     SPG_LAUNCH_CHECK();
     if (b.nred) {
         k_gemm_reduce<<<b.nred, 256, 0, st>>>(b.d_items, b.d_red_items);
@@ -125,4 +127,44 @@ void launch_gemm(const GemmBatch& b, cudaStream_t st) {
     }
 }
 
+}  // namespace spg
+
+namespace spg {
+// FP64 tensor-pipe peak probe: independent DMMA chains per warp, all SMs busy.
+__global__ void __launch_bounds__(256) k_dmma_peak(double* out, int iters) {
+    double acc[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+    double a = 1.0 + 1e-3 * threadIdx.x, b = 1.0 - 1e-3 * threadIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma_8x8x4(acc[i][0], acc[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+    if (s == 12345.678) out[0] = s;   // keep the work alive
+}
+
+double measure_dmma_tflops() {
+    int nsm = 0;
+    SPG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    double* d;
+    SPG_CUDA(cudaMalloc(&d, sizeof(double)));
+    const int iters = 20000, blocks = nsm * 4;
+    k_dmma_peak<<<blocks, 256>>>(d, 100);
+    SPG_CUDA(cudaDeviceSynchronize());
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    k_dmma_peak<<<blocks, 256>>>(d, iters);
+    cudaEventRecord(b);
+    SPG_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    cudaFree(d);
+    const double flops = 2.0 * 8 * 8 * 4 * 8.0 * (double)iters * blocks * (256 / 32);
+    return flops / (ms * 1e-3) / 1e12;
+}
 }  // namespace spg

@@ -41,6 +41,7 @@ struct GemmBatch {
     int nctas = 0;
     const int* d_red_items = nullptr;  // items needing a split-K reduction
     int nred = 0;
+    double* flops = nullptr;           // device counter of algorithmic flops (2MNK)
 };
 void launch_gemm(const GemmBatch& b, cudaStream_t st);
 
