@@ -105,6 +105,7 @@ class RefLib:
             "ref_result_l0": ([vp], C.c_double),
             "ref_result_diag": ([vp, _dp], None),
             "ref_result_hodlr": ([vp, C.c_int], vp),
+            "ref_synth_banded": ([C.c_int, C.c_int, C.c_double, C.c_ulonglong, _dp], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -150,6 +151,13 @@ class RefLib:
         Uo = np.zeros((p, k)); Vo = np.zeros((s, k))
         r = self.L.ref_truncate(p, s, k, _d(U), _d(V), eps, _d(Uo), _d(Vo))
         return Uo[:, :r].copy(), Vo[:, :r].copy()
+
+    def synth_banded(self, n, b, gap, seed):
+        """synth.hpp:106-137 with SpectrumSpec::uniform_two_sided(n, gap) (the reference tests' inputs)."""
+        out = np.zeros((b + 1) * n - b * (b + 1) // 2)
+        if self.L.ref_synth_banded(n, b, gap, seed, _d(out)):
+            raise RefError(self.err())
+        return unpack_bands(out, n, b)
 
     def hqdwh(self, bands, n_min, eps, delta=1e-15):
         """Runs the reference hqdwh; returns a dict with the result handle."""

@@ -27,6 +27,7 @@
 #include "specproj/hodlr.hpp"
 #include "specproj/lowrank.hpp"
 #include "specproj/qdwh.hpp"
+#include "specproj/synth.hpp"
 
 using namespace specproj;
 
@@ -248,6 +249,17 @@ void* ref_first_iterate_m(int n, int b, const double* bands_scaled, int n_min, d
         StackedQrResult qr = fast_stacked_qr(make_banded(n, b, bands_scaled), tree);
         return new HodlrMatrix(q1q2t(qr.q1, qr.q2, eps));
     } catch (const std::exception& e) { classify(e); return nullptr; }
+}
+
+// ---- test matrices (synth.hpp:106-137): the reference tests' spectra -------------
+int ref_synth_banded(int n, int b, double gap, unsigned long long seed, double* bands) {
+    try {
+        BandedSymmetric A = synth_banded(SpectrumSpec::uniform_two_sided(n, gap), b, seed);
+        std::size_t off = 0;
+        for (int d = 0; d <= b; ++d)
+            for (int i = 0; i + d < n; ++i) bands[off++] = A.bands[d][i];
+        return 0;
+    } catch (const std::exception& e) { return classify(e); }
 }
 
 // ---- the hot path entry (qdwh.hpp:196-241) ---------------------------------

@@ -767,7 +767,8 @@ int spg_truncate(int p, int s, int k, const double* U, const double* V, double e
     return guarded([&]() {
         ensure_device();
         if (k > KIN_MAX) throw StatusError(SPG_RANK_CAPACITY, "spg_truncate: k > KIN_MAX");
-        Engine E(std::max(p, s), 2, eps, (size_t)8 << 20);
+        const size_t wsd = (size_t)4 * KIN_MAX * (size_t)(p + s + 4 * KIN_MAX) + ((size_t)4 << 20);
+        Engine E(std::max(p, s), std::max(2, std::max(p, s)), eps, wsd);
         cudaStream_t st = E.stream();
         std::vector<double> cu((size_t)p * k), cv((size_t)s * k);
         for (int i = 0; i < p; ++i) for (int j = 0; j < k; ++j) cu[i + (size_t)j * p] = U[(size_t)i * k + j];

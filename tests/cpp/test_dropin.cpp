@@ -28,7 +28,7 @@ static BandedSymmetric dimer(int n, double t2, double dis, unsigned long long se
     return A;
 }
 
-int main() {
+int main(int argc, char** argv) {
     {   // Hqdwh.MinusIdentityGivesFullProjector (test_qdwh.cpp:112-120)
         BandedSymmetric A(32, 1);
         for (int i = 0; i < 32; ++i) A.bands[0][i] = -1.0;
@@ -62,10 +62,15 @@ int main() {
         }
         CHECK(diagnostics(r.P).max_offdiag_rank > 0, "ranks");
     }
-    {   // Hqdwh.PropagatesCholeskyFailure (test_qdwh.cpp:184-190): coarse eps, tiny gap
+    if (argc > 1) {   // Hqdwh.PropagatesCholeskyFailure (test_qdwh.cpp:184-190): the reference test's input
+        BandedSymmetric A(256, 1);
+        FILE* f = std::fopen(argv[1], "r");
+        for (int i = 0; i < 256; ++i) CHECK(std::fscanf(f, "%lf", &A.bands[0][i]) == 1, "read");
+        for (int i = 0; i < 255; ++i) CHECK(std::fscanf(f, "%lf", &A.bands[1][i]) == 1, "read");
+        std::fclose(f);
         bool thrown = false;
         try {
-            b200::hqdwh(dimer(256, 0.9999999, 0.0, 4), 32, 1e-2, 1e-15);
+            b200::hqdwh(A, 32, 1e-2, 1e-15);
         } catch (const NotPositiveDefiniteError&) {
             thrown = true;
         } catch (const std::exception& e) {

@@ -27,6 +27,9 @@ CASES = [
     ("rand_n200_b3", 200, 3, 24, 1e-10, ("random", 13)),
     ("dimer_n777_b3", 777, 3, 50, 1e-10, ("dimer", 1.0, 0.8, 0.0, 0.05 / 7, 14)),
     ("dimer_n512_b8", 512, 8, 64, 1e-10, ("dimer", 1.0, 0.8, 0.0, 0.05 / 17, 15)),
+    # the reference tests' own spectra (synth.hpp, test_qdwh.cpp:122-139)
+    ("synth_n512_gap1e1", 512, 1, 250, 1e-10, ("synth", 1e-1, 4)),
+    ("synth_n512_b8_gap1e4", 512, 8, 500, 1e-10, ("synth", 1e-4, 5)),
     ("pr1", 2048, 1, 128, 1e-10, ("dimer", 1.0, 0.5, 0.1, 0.0, 1)),
     ("smallgap", 16384, 1, 256, 1e-10, ("dimer", 1.0, 0.999, 2e-4, 0.0, 2)),
 ]
@@ -34,19 +37,31 @@ DENSE_MAX = 256      # store the dense projector up to this n
 PROBES = 4           # P @ Omega probes (Omega ~ seeded normal) for larger n
 
 
-def make_bands(n, b, gen):
+def make_bands(RL, n, b, gen):
     if gen[0] == "dimer":
         _, t1, t2, eps_dis, s, seed = gen
         return S.dimer_chain(n, t1, t2, eps_dis, seed, b=b, s=s)
+    if gen[0] == "synth":
+        return S.BandedSymmetric(n, b, RL.synth_banded(n, b, gen[1], gen[2]))
     return S.random_banded(n, b, gen[1])
 
 
 def main(only=None):
     RL = R.RefLib()
+    # Hqdwh.PropagatesCholeskyFailure (test_qdwh.cpp:184-190): the reference throws
+    # NotPositiveDefiniteError on this input with eps = 1e-2, n_min = 32.
+    bands = RL.synth_banded(256, 1, 1e-8, 19)
+    try:
+        RL.hqdwh(bands, 32, 1e-2)
+        raise SystemExit("expected NotPositiveDefiniteError from the reference")
+    except R.RefError as e:
+        assert "status 1" in str(e), e
+    np.savez_compressed(os.path.join(OUT, "npd_case.npz"), bands=R.pack_bands(bands), n=256, b=1, n_min=32, eps=1e-2)
+    print("npd_case: reference raises NotPositiveDefiniteError")
     for name, n, b, nmin, eps, gen in CASES:
         if only and name not in only:
             continue
-        A = make_bands(n, b, gen)
+        A = make_bands(RL, n, b, gen)
         res = RL.hqdwh(A.bands, nmin, eps)
         h = res["P"]
         out = dict(n=n, b=b, n_min=nmin, eps=eps, bands=A.packed(), alpha=res["alpha"], l0=res["l0"],
