@@ -71,6 +71,9 @@ typedef struct spg_info {
     int profiled;
     double prof_ms_trunc, prof_ms_gemm, prof_ms_hsolve, prof_ms_leaf;
     long long prof_batches_trunc, prof_batches_gemm, prof_batches_hsolve, prof_batches_leaf;
+    /* CUDA graph of the Cholesky-based iteration (replayed iterations-1 times) */
+    int graph_used;
+    long long graph_nodes;
 } spg_info;
 
 /* Runs the hQDWH projector on device 0 (current device).  `bands` is host

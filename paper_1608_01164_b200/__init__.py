@@ -81,7 +81,8 @@ class _Info(C.Structure):
                 ("profiled", C.c_int), ("prof_ms_trunc", C.c_double), ("prof_ms_gemm", C.c_double),
                 ("prof_ms_hsolve", C.c_double), ("prof_ms_leaf", C.c_double),
                 ("prof_batches_trunc", C.c_longlong), ("prof_batches_gemm", C.c_longlong),
-                ("prof_batches_hsolve", C.c_longlong), ("prof_batches_leaf", C.c_longlong)]
+                ("prof_batches_hsolve", C.c_longlong), ("prof_batches_leaf", C.c_longlong),
+                ("graph_used", C.c_int), ("graph_nodes", C.c_longlong)]
 
 
 class _Diag(C.Structure):

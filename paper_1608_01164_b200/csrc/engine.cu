@@ -94,9 +94,16 @@ void DHodlr::alloc(const HTree& tree, Arena& arena) {
     V = U + slab_doubles;
     SPG_CUDA(cudaMalloc(&rank, sizeof(int) * 2 * tree.nnodes()));
     d_leaf_off = arena.push(leaf_off);
+    dinv_off.clear();
+    long long doff = 0;
+    for (int id : tree.leaves) { dinv_off.push_back(doff); doff += (long long)((tree.size[id] + 31) / 32) * 1024; }
+    SPG_CUDA(cudaMalloc(&dinv, sizeof(double) * std::max<long long>(doff, 1)));
+    d_dinv_off = arena.push(dinv_off);
 }
 
 void DHodlr::release() {
+    if (dinv) cudaFree(dinv);
+    dinv = nullptr;
     if (leaves) cudaFree(leaves);
     if (rank) cudaFree(rank);
     leaves = U = V = nullptr;
@@ -121,6 +128,8 @@ __global__ void k_rank_op(const RankOp* ops, int nops) {
 Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin), eps_(eps) {
     SPG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     trunc_init_attributes();
+    leaf_init_attributes();
+    hsolve_init_attributes();
     arena_ = std::make_unique<Arena>(size_t(512) << 20);
     if (!ws_doubles) ws_doubles = std::max<size_t>(size_t(64) << 20, (size_t)90 * n * KIN_MAX);
     ws_ = std::make_unique<Workspace>(ws_doubles);
@@ -389,7 +398,7 @@ void Engine::hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items) {
     if (items.empty()) return;
     std::vector<int2> ctas;
     for (size_t i = 0; i < items.size(); ++i)
-        for (int t = 0; t < (KCAP + 15) / 16; ++t) ctas.push_back(make_int2((int)i, t));
+        for (int t = 0; t < (KCAP + hsolve_tile_cols() - 1) / hsolve_tile_cols(); ++t) ctas.push_back(make_int2((int)i, t));
     const HSolveItem* d = arena_->push(items);
     const int2* dc = arena_->push(ctas);
     const int nc = (int)ctas.size();
@@ -529,6 +538,15 @@ void Engine::op_copy(Plan& p, const DHodlr& src, DHodlr& dst) {
     });
 }
 
+void Engine::op_leaf_dinv(Plan& p, DHodlr& W) {
+    std::vector<DinvItem> it;
+    for (int f : tree_.leaves) it.push_back(DinvItem{W.leaf(f), W.leaf_dinv(f), tree_.size[f], tree_.size[f]});
+    const DinvItem* d = arena_->push(it);
+    const int ni = (int)it.size();
+    unsigned* status = sc_.status;
+    push_timed(p, PC_LEAF, [d, ni, status](cudaStream_t st) { launch_leaf_dinv(d, ni, status, st); });
+}
+
 // hodlr_multiply (hodlr.hpp:409-451), level-batched in the reference's order:
 // (1) leaf products, (2) all own-term panels, (3) own-term truncations,
 // (4) ancestor products trunc(lr_multiply), (5) cascades nearest ancestor first.
@@ -661,10 +679,14 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     const int n = tree_.n;
     if (tree_.leaf(x)) {
         const int s = tree_.size[x];
-        std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s}};
+        std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s, W.leaf_dinv(x)}};
         const CholItem* d = arena_->push(ci);
         unsigned* status = sc_.status;
-        push_timed(p, PC_LEAF, [d, status](cudaStream_t st) { launch_leaf_cholesky(d, 1, status, st); });
+        push_timed(p, PC_LEAF, [d, status, s](cudaStream_t st) { launch_leaf_cholesky(d, 1, status, st, s); });
+        if (s > 576) {   // the large-leaf Cholesky path does not produce the block inverses itself
+            const DinvItem* di = arena_->push(std::vector<DinvItem>{DinvItem{W.leaf(x), W.leaf_dinv(x), s, s}});
+            push_timed(p, PC_LEAF, [di, status](cudaStream_t st) { launch_leaf_dinv(di, 1, status, st); });
+        }
         return;
     }
     const int l = tree_.left[x], r = tree_.right[x];
@@ -711,7 +733,7 @@ void Engine::sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         p.launches.push_back([=](cudaStream_t st) {
             SPG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, st));
         });
-        std::vector<TrsmItem> ti{TrsmItem{W.leaf(x), Y.leaf(x), s, s, s, nullptr, s, 0, 1}};
+        std::vector<TrsmItem> ti{TrsmItem{W.leaf(x), Y.leaf(x), s, s, s, nullptr, s, 0, 1, W.leaf_dinv(x)}};
         std::vector<int2> ct;
         for (int c = 0; c < (s + 15) / 16; ++c) ct.push_back(make_int2(0, c));
         const TrsmItem* d = arena_->push(ti);
@@ -781,7 +803,7 @@ void Engine::surt_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         p.launches.push_back([=](cudaStream_t st) {
             SPG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, st));
         });
-        std::vector<TrsmItem> ti{TrsmItem{W.leaf(x), Y.leaf(x), s, s, s, nullptr, s, 1, 1}};
+        std::vector<TrsmItem> ti{TrsmItem{W.leaf(x), Y.leaf(x), s, s, s, nullptr, s, 1, 1, W.leaf_dinv(x)}};
         std::vector<int2> ct;
         for (int c = 0; c < (s + 15) / 16; ++c) ct.push_back(make_int2(0, c));
         const TrsmItem* d = arena_->push(ti);

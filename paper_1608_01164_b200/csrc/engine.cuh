@@ -84,6 +84,9 @@ struct DHodlr {
     double* U = nullptr;
     double* V = nullptr;
     int* rank = nullptr;
+    double* dinv = nullptr;                 // diagonal-block inverses (used when this is a triangular factor)
+    long long* d_dinv_off = nullptr;
+    std::vector<long long> dinv_off;
     size_t leaf_doubles = 0, slab_doubles = 0;
     void alloc(const HTree& tree, Arena& arena);
     void release();
@@ -96,7 +99,8 @@ struct DHodlr {
     double* loV(int id) const { return slabV(t->level[id]) + t->begin[t->left[id]]; }
     int* rup(int id) const { return rank + 2 * id; }
     int* rlo(int id) const { return rank + 2 * id + 1; }
-    DevHodlrView view() const { return {leaves, d_leaf_off, U, V, rank, t->n}; }
+    double* leaf_dinv(int id) const { return dinv + dinv_off[t->leaf_ord[id]]; }
+    DevHodlrView view() const { return {leaves, d_leaf_off, U, V, rank, t->n, dinv, d_dinv_off}; }
     void zero(cudaStream_t st) const;
 };
 
@@ -160,6 +164,8 @@ public:
     void op_symmetrize(Plan& p, DHodlr& H);
     void op_scale_shift(Plan& p, DHodlr& H, double s, const double* sp, double mu);
     void op_copy(Plan& p, const DHodlr& src, DHodlr& dst);
+    // inverses of the 32x32 diagonal blocks of every leaf of an upper-triangular factor
+    void op_leaf_dinv(Plan& p, DHodlr& W);
     void op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C);
     void op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work);
     void op_solve_upper_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work);

@@ -294,7 +294,9 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     std::vector<int> used((size_t)nruns * nmarks, 0);
     int cur_run = 0;
     int* cur_run_p = &cur_run;
+    bool phase_events = true;   // off while building a plan that is captured into a CUDA graph
     auto timed = [&](Plan& p, int phase, const std::function<void()>& body) {
+        if (!phase_events) { body(); return; }
         cudaEvent_t* tab = evtab.data();
         int* up = used.data();
         p.launches.push_back([=](cudaStream_t s) {
@@ -390,6 +392,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
                 Zp->zero(s);
                 launch_from_band(dt, Zp->view(), 0, b, d_bands, S.slots + 5, 1.0, s);   // sqrt(c0) A / alpha
             });
+            E.op_leaf_dinv(p, *W);                         // diagonal-block inverses of R's leaves
             E.op_solve_upper_right(p, *Z, *W, *Y, *WK);    // Q1 = B R^{-1}
             E.op_solve_upperT_right(p, *Y, *W, *V, *WK);   // M  = Q1 R^{-T} = Q1 Q2^T
             E.op_symmetrize(p, *V);                        // q1q2t symmetrizes M (fast_qr.hpp:513)
@@ -418,15 +421,45 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
             push_diag(p);
             E.arena().commit(st);
         };
+        // Default: the iteration plan is captured once into a CUDA graph and replayed
+        // count-1 times (all per-iteration scalars are read from device memory, so the
+        // graph is iteration-invariant).  Profile mode rebuilds the plan per run so every
+        // batch keeps its own event pair; SPG_NO_GRAPH=1 replays the plan without a graph.
+        const bool use_graph = !E.profile() && !std::getenv("SPG_NO_GRAPH");
         Plan p;
-        if (!E.profile()) build_iter(p);
+        cudaGraphExec_t gexec = nullptr;
+        if (use_graph) {
+            phase_events = false;
+            build_iter(p);
+            phase_events = true;
+            cudaGraph_t g;
+            const long long l0c = g_launches.load();
+            SPG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            p.run(st);
+            SPG_CUDA(cudaStreamEndCapture(st, &g));
+            SPG_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+            size_t nn = 0;
+            SPG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+            SPG_CUDA(cudaGraphDestroy(g));
+            const long long per_iter = g_launches.load() - l0c;   // kernels captured once ...
+            g_launches += per_iter * (count - 2);                 // ... and replayed count-1 times
+            R->info.graph_nodes = (long long)nn;
+            R->info.graph_used = 1;
+        } else if (!E.profile()) {
+            build_iter(p);
+        }
         for (int k = 1; k < count; ++k) {
             cur_run = k;
             if (E.profile()) { p = Plan(); build_iter(p); }
             cudaEvent_t e0 = mkev();
             it_ev.push_back(e0);
             SPG_CUDA(cudaEventRecord(e0, st));
-            p.run(st);
+            if (gexec) SPG_CUDA(cudaGraphLaunch(gexec, st));
+            else p.run(st);
+        }
+        if (gexec) {
+            SPG_CUDA(cudaStreamSynchronize(st));
+            SPG_CUDA(cudaGraphExecDestroy(gexec));
         }
     }
     {
@@ -751,8 +784,14 @@ int spg_ctx_op(spg_ctx* c, int op, int dst, int a, int b, double alpha, double b
             case 2: E.op_axpby(p, alpha, nullptr, *c->slots.at(a), beta, nullptr, *c->slots.at(b), D); break;
             case 3: E.op_symmetrize(p, D); break;
             case 4: E.op_cholesky(p, *c->slots.at(a), D, *c->work); break;
-            case 5: E.op_solve_upper_right(p, *c->slots.at(a), *c->slots.at(b), D, *c->work); break;
-            case 6: E.op_solve_upperT_right(p, *c->slots.at(a), *c->slots.at(b), D, *c->work); break;
+            case 5:
+                E.op_leaf_dinv(p, *c->slots.at(b));   // uploaded factors carry no block inverses yet
+                E.op_solve_upper_right(p, *c->slots.at(a), *c->slots.at(b), D, *c->work);
+                break;
+            case 6:
+                E.op_leaf_dinv(p, *c->slots.at(b));
+                E.op_solve_upperT_right(p, *c->slots.at(a), *c->slots.at(b), D, *c->work);
+                break;
             case 7: E.op_scale_shift(p, D, alpha, nullptr, beta); break;
             default: throw StatusError(SPG_INVALID_ARGUMENT, "spg_ctx_op: unknown op");
         }

@@ -199,9 +199,140 @@ __global__ void __launch_bounds__(512) k_leaf_chol(const CholItem* __restrict__ 
     }
     if (tid == 0 && sFail) atomicOr(status, ST_NPD);
 }
-void launch_leaf_cholesky(const CholItem* d, int nitems, unsigned* status, cudaStream_t st) {
+// Blocked left-looking Cholesky (leaves n <= CH_NMAX), 32-column panels:
+//   (1) panel update P = M[J:, J:J+32] - L[J:, :J] L[J:J+32, :J]^T on the FP64
+//       tensor path (mma.sync m8n8k4 -> DMMA), L staged through shared memory
+//       in 16-column chunks (one tile feeds both operands);
+//   (2) right-looking elimination of the panel in shared memory (one barrier per
+//       column, unscaled Gaussian form, columns scaled by 1/sqrt(pivot) at the end);
+//   (3) L written transposed into W (= L^T, cholesky_upper, dense_factor.hpp:222).
+constexpr int CH_NB = 32, CH_KC = 16, CH_NMAX = 576, CH_THREADS = 512;
+__device__ __forceinline__ void dmma_leaf(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __restrict__ it, unsigned* status) {
+    extern __shared__ double sm[];
+    const CholItem C = it[blockIdx.x];
+    const int n = C.n;
+    const int ldp = n + 1;
+    double* sP = sm;                   // panel: (n - J) x CH_NB, col-major ld ldp
+    double* sL = sm + ldp * CH_NB;     // L chunk: (n - J) x CH_KC
+    __shared__ double sPiv[CH_NB];
+    __shared__ int sFail;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CH_THREADS / 32;
+    if (tid == 0) sFail = 0;
+    for (long long idx = tid; idx < (long long)n * n; idx += blockDim.x) {
+        const int i = idx % n, j = idx / n;
+        if (i > j) C.W[i + (long long)j * C.ldw] = 0.0;
+    }
+    for (int J = 0; J < n; J += CH_NB) {
+        const int nb = min(CH_NB, n - J), mr = n - J;           // panel columns / rows
+        const int nrt = (mr + 7) / 8;
+        double acc[5][4][2];
+#pragma unroll
+        for (int a = 0; a < 5; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+        // (1) S = L[J:, :J] L[J:J+nb, :J]^T
+        for (int l0 = 0; l0 < J; l0 += CH_KC) {
+            __syncthreads();
+            for (int idx = tid; idx < mr * CH_KC; idx += blockDim.x) {
+                const int kk = idx % CH_KC, i = idx / CH_KC;
+                sL[i + kk * ldp] = C.W[(l0 + kk) + (long long)(J + i) * C.ldw];   // L(J+i, l0+kk)
+            }
+            __syncthreads();
+#pragma unroll
+            for (int ks = 0; ks < CH_KC; ks += 4) {
+                double bf[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) bf[c] = sL[(c * 8 + (lane >> 2)) + (ks + (lane & 3)) * ldp];
+#pragma unroll
+                for (int a = 0; a < 5; ++a) {
+                    const int rt = warp + a * nw;
+                    if (rt < nrt) {
+                        const double af = sL[(rt * 8 + (lane >> 2)) + (ks + (lane & 3)) * ldp];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) dmma_leaf(acc[a][c][0], acc[a][c][1], af, bf[c]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // P = M[J+i, J+jj] - S  (lower part only is meaningful)
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            const int rt = warp + a * nw;
+            if (rt >= nrt) continue;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int i = rt * 8 + (lane >> 2), jj = c * 8 + 2 * (lane & 3) + v;
+                    if (i < mr && jj < nb && i >= jj)
+                        sP[i + jj * ldp] = C.M[(J + i) + (long long)(J + jj) * C.ldm] - acc[a][c][v];
+                }
+        }
+        __syncthreads();
+        // (2) right-looking elimination of the panel
+        for (int jj = 0; jj < nb; ++jj) {
+            double d = sP[jj + jj * ldp];
+            if (!(d > 0.0)) { if (tid == 0) sFail = 1; d = 1.0; }
+            if (tid == 0) sPiv[jj] = d;
+            const double inv = 1.0 / d;
+            const int rows = mr - jj - 1, cols = nb - jj - 1;
+            for (int idx = tid; idx < rows * cols; idx += blockDim.x) {
+                const int i = jj + 1 + idx % rows, kk = jj + 1 + idx / rows;
+                if (i >= kk) sP[i + kk * ldp] -= sP[i + jj * ldp] * sP[kk + jj * ldp] * inv;
+            }
+            __syncthreads();
+        }
+        // (3) L(J+i, J+jj) = P[i][jj] / sqrt(pivot_jj)  ->  W(J+jj, J+i)
+        for (int idx = tid; idx < mr * nb; idx += blockDim.x) {
+            const int jj = idx % nb, i = idx / nb;
+            if (i >= jj) C.W[(J + jj) + (long long)(J + i) * C.ldw] = sP[i + jj * ldp] / sqrt(sPiv[jj]);
+        }
+        __syncthreads();
+    }
+    if (C.D) {   // inverses of W's 32x32 diagonal blocks for trsm_tile_dinv, 4 warps
+        double* sT = sm;   // reuse the panel buffer (>= 4 x 32 x 33 doubles, see launcher)
+        bool sing = false;
+        if (warp < 4)
+            for (int blk = warp; blk * 32 < n; blk += 4)
+                sing |= invert_diag_block_warp(C.W, C.ldw, blk * 32, min(32, n - blk * 32),
+                                               C.D + (long long)blk * 1024, sT + warp * 32 * 33);
+        if (sing) atomicOr(status, ST_SINGULAR);
+    }
+    if (tid == 0 && sFail) atomicOr(status, ST_NPD);
+}
+
+__global__ void __launch_bounds__(512) k_leaf_dinv(const DinvItem* __restrict__ it, unsigned* status) {
+    extern __shared__ double sT[];   // 16 x 32 x 33
+    const DinvItem I = it[blockIdx.x];
+    const int warp = threadIdx.x >> 5;
+    bool sing = false;
+    for (int blk = warp; blk * 32 < I.n; blk += 16)
+        sing |= invert_diag_block_warp(I.W, I.ldw, blk * 32, min(32, I.n - blk * 32), I.D + (long long)blk * 1024,
+                                       sT + warp * 32 * 33);
+    if (sing) atomicOr(status, ST_SINGULAR);
+}
+
+void launch_leaf_dinv(const DinvItem* d, int nitems, unsigned* status, cudaStream_t st) {
     if (!nitems) return;
-    k_leaf_chol<<<nitems, 512, 0, st>>>(d, status);
+    k_leaf_dinv<<<nitems, 512, sizeof(double) * 16 * 32 * 33, st>>>(d, status);
+    SPG_LAUNCH_CHECK();
+}
+
+void launch_leaf_cholesky(const CholItem* d, int nitems, unsigned* status, cudaStream_t st, int maxn) {
+    if (!nitems) return;
+    if (maxn <= CH_NMAX) {
+        const size_t sm = sizeof(double) * std::max((maxn + 1) * (CH_NB + CH_KC), 4 * 32 * 33);
+        k_leaf_chol2<<<nitems, CH_THREADS, sm, st>>>(d, status);
+    } else {
+        k_leaf_chol<<<nitems, 512, 0, st>>>(d, status);   // no Dinv: k_leaf_dinv is launched separately
+    }
     SPG_LAUNCH_CHECK();
 }
 
@@ -227,7 +358,8 @@ __global__ void __launch_bounds__(512) k_leaf_trsm(const TrsmItem* __restrict__ 
         if (T.rhs_t) { c = idx % ncols; i = idx / ncols; } else { i = idx % n; c = idx / n; }
         sX[i + c * n] = *xg(i, c);
     }
-    const bool sing = trsm_tile(T.W, T.ldw, n, T.mode, sX, n, ncols, sW);
+    const bool sing = T.D ? (trsm_tile_dinv(T.W, T.ldw, T.D, n, T.mode, sX, n, ncols, &sW[0][0]), false)
+                          : trsm_tile(T.W, T.ldw, n, T.mode, sX, n, ncols, sW);
     __syncthreads();
     for (int idx = tid; idx < n * ncols; idx += blockDim.x) {
         int i, c;
@@ -238,14 +370,17 @@ __global__ void __launch_bounds__(512) k_leaf_trsm(const TrsmItem* __restrict__ 
 }
 void launch_leaf_trsm(const TrsmItem* d, const int2* d_ctas, int nctas, unsigned* status, cudaStream_t st) {
     if (!nctas) return;
-    static bool attr = false;
-    if (!attr) {
-        SPG_CUDA(cudaFuncSetAttribute(k_leaf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(sizeof(double) * TR_NMAX * TR_TC)));
-        attr = true;
-    }
     k_leaf_trsm<<<nctas, 512, sizeof(double) * TR_NMAX * TR_TC, st>>>(d, d_ctas, status);
     SPG_LAUNCH_CHECK();
+}
+
+void leaf_init_attributes() {
+    SPG_CUDA(cudaFuncSetAttribute(k_leaf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * TR_NMAX * TR_TC)));
+    SPG_CUDA(cudaFuncSetAttribute(k_leaf_chol2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * (CH_NMAX + 1) * (CH_NB + CH_KC))));
+    SPG_CUDA(cudaFuncSetAttribute(k_leaf_dinv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * 16 * 32 * 33)));
 }
 
 }  // namespace spg

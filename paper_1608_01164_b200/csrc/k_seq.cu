@@ -1,0 +1,398 @@
+// Sequential O(b n) .. O(b^2 n) recurrences of the setup phase, one warp each,
+// with the working arrays streamed through shared-memory sliding windows so the
+// dependent chain runs at shared-memory latency instead of L2 latency:
+//   * banded LU with partial pivoting + Hager 1-norm estimate -> l0
+//     (estimate_l0 / hager_norm1 / BandedLu, estimates.hpp:40-80, banded_lu.hpp:16-93)
+//   * Givens reduction of [s A; I] -> R (reduce_banded = reduce_tridiag for b = 1,
+//     fast_qr.hpp:83-232)
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spg {
+
+__device__ __forceinline__ long long boff(int n, int d) { return (long long)d * n - (long long)d * (d - 1) / 2; }
+
+__device__ __forceinline__ double wsum32(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// A warp-collective window over a global double array: ensure(lo, hi) makes
+// elements [lo, hi) resident; on a miss the window is written back and re-based
+// (forward passes base at lo, backward passes end at hi).
+template <class T>
+struct WinT {
+    T* g;               // global array
+    long long total;    // its length
+    T* s;               // shared buffer
+    int cap;            // window capacity
+    long long base;     // global index of s[0]
+    int len;            // resident length
+    __device__ void flush(int lane) {
+        for (int i = lane; i < len; i += 32) g[base + i] = s[i];
+        __syncwarp();
+    }
+    __device__ void load(long long b, int lane) {
+        base = b < 0 ? 0 : b;
+        long long e = base + cap;
+        if (e > total) e = total;
+        len = (int)(e - base);
+        for (int i = lane; i < len; i += 32) s[i] = g[base + i];
+        __syncwarp();
+    }
+    __device__ void ensure(long long lo, long long hi, bool forward, int lane) {
+        if (lo < 0) lo = 0;
+        if (hi > total) hi = total;
+        if (lo >= base && hi <= base + len) return;
+        flush(lane);
+        load(forward ? lo : hi - cap, lane);
+    }
+    __device__ T& at(long long i) { return s[i - base]; }
+};
+using Win = WinT<double>;
+using WinI = WinT<int>;
+
+// ------------------------------------------------------------ l0 estimate
+struct BLUw {
+    Win w;
+    int n, b, wd;
+    __device__ double& at(int i, int j) { return w.at((long long)j * wd + (i - j + 2 * b)); }
+};
+
+__device__ void lu_solve_w(BLUw& L, WinI& piv, Win& x, int lane) {
+    const int n = L.n, b = L.b, wd = L.wd;
+    for (int k = 0; k < n; ++k) {
+        L.w.ensure((long long)k * wd, (long long)(k + 1) * wd, true, lane);
+        x.ensure(k, k + b + 1, true, lane);
+        piv.ensure(k, k + 1, true, lane);
+        const int p = piv.at(k);
+        if (lane == 0 && p != k) { const double t = x.at(k); x.at(k) = x.at(p); x.at(p) = t; }
+        __syncwarp();
+        const double xk = x.at(k);
+        const int rend = min(n - 1, k + b);
+        for (int r = k + 1 + lane; r <= rend; r += 32) x.at(r) -= L.at(r, k) * xk;
+        __syncwarp();
+    }
+    for (int j = n - 1; j >= 0; --j) {
+        L.w.ensure((long long)j * wd, (long long)(j + 1) * wd, false, lane);
+        x.ensure(j - 2 * b, j + 1, false, lane);
+        if (lane == 0) x.at(j) /= L.at(j, j);
+        __syncwarp();
+        const double xj = x.at(j);
+        for (int r = max(0, j - 2 * b) + lane; r < j; r += 32) x.at(r) -= L.at(r, j) * xj;
+        __syncwarp();
+    }
+}
+
+__device__ void lu_solve_t_w(BLUw& L, WinI& piv, Win& x, int lane) {
+    const int n = L.n, b = L.b, wd = L.wd;
+    for (int j = 0; j < n; ++j) {
+        L.w.ensure((long long)j * wd, (long long)(j + 1) * wd, true, lane);
+        x.ensure(j - 2 * b, j + 1, true, lane);
+        double s = 0.0;
+        for (int r = max(0, j - 2 * b) + lane; r < j; r += 32) s += L.at(r, j) * x.at(r);
+        s = wsum32(s);
+        if (lane == 0) x.at(j) = (x.at(j) - s) / L.at(j, j);
+        __syncwarp();
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        L.w.ensure((long long)k * wd, (long long)(k + 1) * wd, false, lane);
+        x.ensure(k, k + b + 1, false, lane);
+        piv.ensure(k, k + 1, false, lane);
+        const int rend = min(n - 1, k + b);
+        double s = 0.0;
+        for (int r = k + 1 + lane; r <= rend; r += 32) s += L.at(r, k) * x.at(r);
+        s = wsum32(s);
+        if (lane == 0) {
+            x.at(k) = x.at(k) - s;
+            const int p = piv.at(k);
+            if (p != k) { const double t = x.at(k); x.at(k) = x.at(p); x.at(p) = t; }
+        }
+        __syncwarp();
+    }
+}
+
+constexpr int WIN_LU = 4096, WIN_X = 1024;
+
+__global__ void __launch_bounds__(32) k_est_l0_w(int n, int b, const double* __restrict__ bands, const double* alpha_p,
+                                                double* lu, int* piv, double* vecs, double* out, unsigned* status) {
+    __shared__ double sLU[WIN_LU];
+    __shared__ double sX[WIN_X];
+    __shared__ int sPv[WIN_X];
+    const int lane = threadIdx.x;
+    const double alpha = *alpha_p;
+    const double inv_alpha = 1.0 / alpha;
+    const int wd = 3 * b + 1;
+    // norm1 (banded.hpp:94-106) -> n1 = ||A||_1 / alpha
+    double m = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        double cs = fabs(bands[i]);
+        for (int d = 1; d <= b; ++d) {
+            const double* dg = bands + boff(n, d);
+            if (i + d < n) cs += fabs(dg[i]);
+            if (i - d >= 0) cs += fabs(dg[i - d]);
+        }
+        m = fmax(m, cs);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const double n1 = m / alpha;
+    // fill (banded_lu.hpp:18-25): column j keeps rows [j-2b, j+b]
+    for (long long idx = lane; idx < (long long)n * wd; idx += 32) {
+        const int j = (int)(idx / wd), o = (int)(idx % wd);
+        const int i = j + o - 2 * b;
+        double v = 0.0;
+        if (i >= 0 && i < n) {
+            const int d = i >= j ? i - j : j - i;
+            if (d <= b) v = bands[boff(n, d) + (i < j ? i : j)] * inv_alpha;
+        }
+        lu[idx] = v;
+    }
+    __syncwarp();
+    BLUw L{Win{lu, (long long)n * wd, sLU, (WIN_LU / wd) * wd, 0, 0}, n, b, wd};
+    L.w.load(0, lane);
+    // factor (banded_lu.hpp:66-88)
+    bool singular = false;
+    for (int k = 0; k < n; ++k) {
+        L.w.ensure((long long)k * wd, (long long)min(n, k + 2 * b + 1) * wd, true, lane);
+        const int rend = min(n - 1, k + b);
+        double best = -1.0;
+        int p = k;
+        for (int r = k + lane; r <= rend; r += 32) {
+            const double v = fabs(L.at(r, k));
+            if (v > best) { best = v; p = r; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int op = __shfl_xor_sync(0xffffffffu, p, o);
+            if (ob > best || (ob == best && op < p)) { best = ob; p = op; }
+        }
+        if (lane == 0) piv[k] = p;
+        if (best == 0.0) { singular = true; break; }
+        const int cend = min(n - 1, k + 2 * b);
+        if (p != k)
+            for (int c = k + lane; c <= cend; c += 32) {
+                const double t = L.at(k, c); L.at(k, c) = L.at(p, c); L.at(p, c) = t;
+            }
+        __syncwarp();
+        const double inv = 1.0 / L.at(k, k);
+        for (int r = k + 1 + lane; r <= rend; r += 32) L.at(r, k) = L.at(r, k) * inv;
+        __syncwarp();
+        const int nr = rend - k, ncl = cend - k;
+        for (int idx = lane; idx < nr * ncl; idx += 32) {
+            const int r = k + 1 + idx % nr, c = k + 1 + idx / nr;
+            const double mm = L.at(r, k);
+            if (mm != 0.0) L.at(r, c) -= mm * L.at(k, c);
+        }
+        __syncwarp();
+    }
+    L.w.flush(lane);
+    if (singular) {
+        if (lane == 0) { atomicOr(status, ST_SINGULAR); out[0] = 0.0; }
+        return;
+    }
+    __threadfence_block();
+    // hager_norm1 (estimates.hpp:40-68)
+    double* x = vecs;
+    double* y = vecs + n;
+    double* z = vecs + 2 * n;
+    for (int i = lane; i < n; i += 32) x[i] = 1.0 / n;
+    __syncwarp();
+    double est = 0.0;
+    for (int it = 0; it < 5; ++it) {
+        for (int i = lane; i < n; i += 32) y[i] = x[i];
+        __syncwarp();
+        Win wy{y, n, sX, WIN_X, 0, 0};
+        WinI wp{piv, n, sPv, WIN_X, 0, 0};
+        L.w.load(0, lane);
+        wy.load(0, lane);
+        wp.load(0, lane);
+        lu_solve_w(L, wp, wy, lane);
+        wy.flush(lane);
+        double e = 0.0;
+        for (int i = lane; i < n; i += 32) e += fabs(y[i]);
+        e = wsum32(e);
+        if (it > 0 && e <= est) break;
+        est = e;
+        for (int i = lane; i < n; i += 32) z[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+        __syncwarp();
+        Win wz{z, n, sX, WIN_X, 0, 0};
+        WinI wq{piv, n, sPv, WIN_X, 0, 0};
+        L.w.load(0, lane);
+        wz.load(0, lane);
+        wq.load(0, lane);
+        lu_solve_t_w(L, wq, wz, lane);
+        wz.flush(lane);
+        double zmax = 0.0, ztx = 0.0;
+        int j = 0x7fffffff;
+        for (int i = lane; i < n; i += 32) {
+            const double a = fabs(z[i]);
+            if (a > zmax) { zmax = a; j = i; }
+            ztx += z[i] * x[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double oz = __shfl_xor_sync(0xffffffffu, zmax, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+            if (oz > zmax || (oz == zmax && oj < j)) { zmax = oz; j = oj; }
+        }
+        ztx = wsum32(ztx);
+        if (j == 0x7fffffff) j = 0;
+        if (zmax <= ztx) break;
+        for (int i = lane; i < n; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        const double cond1 = n1 * est;
+        out[0] = n1 / (sqrt((double)n) * cond1);
+    }
+}
+
+void launch_estimate_l0(int n, int b, const double* bands, const double* alpha, double* lu_work, int* piv,
+                        double* vecs, double* out_l0, unsigned* status, cudaStream_t st) {
+    k_est_l0_w<<<1, 32, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status);
+    SPG_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------ Givens reduction
+__device__ __forceinline__ void givens_cs(double f, double g, double& c, double& s) {   // givens.hpp:27-36
+    if (g == 0.0) { c = 1.0; s = 0.0; return; }
+    if (f == 0.0) { c = 0.0; s = 1.0; return; }
+    const double af = fabs(f), ag = fabs(g);
+    const double scale = af + ag;
+    const double fs = f / scale, gs = g / scale;
+    double r = scale * sqrt(fs * fs + gs * gs);
+    if (f < 0.0) r = -r;
+    c = f / r; s = g / r;
+}
+
+constexpr int WIN_R = 2048, WIN_V = 1024, WIN_J = 1024;
+
+__global__ void k_givens_fill(int n, int b, const double* __restrict__ bands, const double* slots, double* R,
+                              double* rowN, double* aux, double* junk) {
+    const double sA = slots[5];   // sqrt(c0)/alpha
+    const int w = 3 * b + 1, jw = b > 1 ? b - 1 : 1;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * w;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / w), k = (int)(idx % w) + i - b;   // row i, column k in [i-b, i+2b]
+        double v = 0.0;
+        if (k >= 0 && k < n) {
+            const int d = i >= k ? i - k : k - i;
+            if (d <= b) v = bands[boff(n, d) + (i < k ? i : k)] * sA;
+        }
+        R[idx] = v;
+        if (idx < n) { rowN[idx] = idx == 0 ? 1.0 : 0.0; aux[idx] = 1.0; }
+        if (idx < (long long)n * jw) junk[idx] = 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(32) k_givens_w(int n, int b, double* R, double* rowNg, double* auxg, double* junkg,
+                                                double* rdiag) {
+    __shared__ double sR[WIN_R];
+    __shared__ double sN[WIN_V];
+    __shared__ double sA[WIN_V];
+    __shared__ double sJ[WIN_J];
+    const int lane = threadIdx.x;
+    const int w = 3 * b + 1, jw = b > 1 ? b - 1 : 1;
+    Win wr{R, (long long)n * w, sR, (WIN_R / w) * w, 0, 0};
+    Win wn{rowNg, n, sN, WIN_V, 0, 0};
+    Win wa{auxg, n, sA, WIN_V, 0, 0};
+    Win wj{junkg, (long long)n * jw, sJ, (WIN_J / jw) * jw, 0, 0};
+    wr.load(0, lane); wn.load(0, lane); wa.load(0, lane); wj.load(0, lane);
+    auto RA = [&](int i, int k) -> double& { return wr.at((long long)i * w + (k - i + b)); };
+    auto JK = [&](int t, int k) -> double& { return wj.at((long long)t * jw + (k - (t + 1))); };
+    auto rowN = [&](int i) -> double& { return wn.at(i); };
+    auto aux = [&](int i) -> double& { return wa.at(i); };
+    double c, s;
+    // step 0 (fast_qr.hpp:104-122)
+    wr.ensure(0, (long long)min(n, 2 * b + 1) * w, true, lane);
+    wn.ensure(0, min(n, 2 * b + 1), true, lane);
+    givens_cs(RA(0, 0), rowN(0), c, s);
+    __syncwarp();
+    if (lane == 0) { RA(0, 0) = c * RA(0, 0) + s * rowN(0); rowN(0) = 0.0; }
+    __syncwarp();
+    for (int k = 1 + lane; k <= min(n - 1, b); k += 32) {
+        const double x = RA(0, k), y = rowN(k);
+        RA(0, k) = c * x + s * y; rowN(k) = -s * x + c * y;
+    }
+    __syncwarp();
+    for (int j = 1; j <= min(n - 1, b); ++j) {
+        givens_cs(RA(0, 0), RA(j, 0), c, s);
+        __syncwarp();
+        for (int k = lane; k <= min(n - 1, 2 * b); k += 32) {
+            const double x = RA(0, k), y = RA(j, k);
+            RA(0, k) = c * x + s * y; RA(j, k) = -s * x + c * y;
+        }
+        __syncwarp();
+        if (lane == 0) RA(j, 0) = 0.0;
+        __syncwarp();
+    }
+    for (int t = 1; t < n; ++t) {
+        // rows t .. t+b of R, rowN/aux t .. t+2b, junk rows t .. t+b-1
+        wr.ensure((long long)t * w, (long long)min(n, t + b + 1) * w, true, lane);
+        wn.ensure(t, min(n, t + 2 * b + 1), true, lane);
+        wa.ensure(t, min(n, t + b + 1), true, lane);
+        wj.ensure((long long)t * jw, (long long)min(n, t + b) * jw, true, lane);
+        const int lim1 = min(n - 1, t + b - 1);
+        givens_cs(rowN(t), aux(t), c, s);                       // alpha_{t,t}
+        __syncwarp();
+        if (lane == 0) { rowN(t) = c * rowN(t) + s * aux(t); aux(t) = 0.0; }
+        for (int k = t + 1 + lane; k <= lim1; k += 32) {
+            const double x = rowN(k), y = JK(t, k);
+            rowN(k) = c * x + s * y; JK(t, k) = -s * x + c * y;
+        }
+        __syncwarp();
+        for (int j = t + 1; j <= lim1; ++j) {                   // alpha_{t,j}
+            givens_cs(aux(j), JK(t, j), c, s);
+            __syncwarp();
+            if (lane == 0) { aux(j) = c * aux(j) + s * JK(t, j); JK(t, j) = 0.0; }
+            for (int k = j + 1 + lane; k <= lim1; k += 32) {
+                const double x = JK(j, k), y = JK(t, k);
+                JK(j, k) = c * x + s * y; JK(t, k) = -s * x + c * y;
+            }
+            __syncwarp();
+        }
+        givens_cs(RA(t, t), rowN(t), c, s);                     // beta_t
+        __syncwarp();
+        if (lane == 0) { RA(t, t) = c * RA(t, t) + s * rowN(t); rowN(t) = 0.0; }
+        for (int k = t + 1 + lane; k <= min(n - 1, t + b); k += 32) {
+            const double x = RA(t, k), y = rowN(k);
+            RA(t, k) = c * x + s * y; rowN(k) = -s * x + c * y;
+        }
+        __syncwarp();
+        for (int j = t + 1; j <= min(n - 1, t + b); ++j) {      // gamma_{t,j}
+            givens_cs(RA(t, t), RA(j, t), c, s);
+            __syncwarp();
+            for (int k = t + lane; k <= min(n - 1, t + 2 * b); k += 32) {
+                const double x = RA(t, k), y = RA(j, k);
+                RA(t, k) = c * x + s * y; RA(j, k) = -s * x + c * y;
+            }
+            __syncwarp();
+            if (lane == 0) RA(j, t) = 0.0;
+            __syncwarp();
+        }
+    }
+    wr.flush(lane);
+    __threadfence_block();
+    for (int d = 0; d <= 2 * b; ++d)
+        for (int i = lane; i < n; i += 32) rdiag[(long long)d * n + i] = i + d < n ? R[(long long)i * w + (d + b)] : 0.0;
+}
+
+void launch_givens_reduce(int n, int b, const double* bands, const double* slots, double* work, double* rdiag,
+                          cudaStream_t st) {
+    const int w = 3 * b + 1, jw = b > 1 ? b - 1 : 1;
+    double* R = work;
+    double* rowN = R + (long long)n * w;
+    double* aux = rowN + n;
+    double* junk = aux + n;
+    const long long tot = (long long)n * w;
+    k_givens_fill<<<(int)std::min<long long>(1024, (tot + 255) / 256), 256, 0, st>>>(n, b, bands, slots, R, rowN, aux, junk);
+    SPG_LAUNCH_CHECK();
+    k_givens_w<<<1, 32, 0, st>>>(n, b, R, rowN, aux, junk, rdiag);
+    SPG_LAUNCH_CHECK();
+    (void)jw;
+}
+
+}  // namespace spg

@@ -240,54 +240,58 @@ __global__ void __launch_bounds__(TS_THREADS) k_core(const TTask* __restrict__ t
     }
     const int kk = k + (k & 1);   // even number of slots; slot k (if odd) is a dummy
     const int npairs = kk / 2;
-    if (tid < npairs) { sTop[tid] = 2 * tid; sBot[tid] = 2 * tid + 1; }
+    const int mrr = kk - 1;                       // rounds per sweep (circle method)
+    constexpr int GL = 8;                         // lanes per pair: 4 pairs per warp in flight
+    const int gid = lane / GL, gl = lane % GL;
+    const int slots = nwarps * (32 / GL);
+    const int slot = warp * (32 / GL) + gid;
+    (void)sTop; (void)sBot;
     __syncthreads();
     const double tol = 1e-15;
     for (int sweep = 0; sweep < 60; ++sweep) {
         if (tid == 0) sRot = 0;
         __syncthreads();
         int rotated = 0;
-        for (int round = 0; round < kk - 1; ++round) {
-            for (int pi = warp; pi < npairs; pi += nwarps) {
-                int p = sTop[pi], q = sBot[pi];
-                if (p > q) { const int tmp = p; p = q; q = tmp; }
-                if (q >= k) continue;
+        for (int round = 0; round < mrr; ++round) {
+            // pairs of round `round`: (round, kk-1) and ((round+i) mod m, (round-i) mod m), i = 1..kk/2-1
+            for (int base = 0; base < npairs; base += slots) {
+                const int pi = base + slot;
+                int p = 0, q = 0;
+                if (pi < npairs) {
+                    if (pi == 0) { p = round; q = kk - 1; }
+                    else { p = (round + pi) % mrr; q = (round - pi + mrr) % mrr; }
+                    if (p > q) { const int tmp = p; p = q; q = tmp; }
+                }
+                const bool act = pi < npairs && q < k;
                 double* wp = sW + p * KIN_MAX;
                 double* wq = sW + q * KIN_MAX;
                 double app = 0.0, aqq = 0.0, apq = 0.0;
-                for (int i = lane; i < k; i += 32) {
-                    const double a = wp[i], b = wq[i];
-                    app += a * a; aqq += b * b; apq += a * b;
+                if (act)
+                    for (int i = gl; i < k; i += GL) {
+                        const double a = wp[i], b = wq[i];
+                        app += a * a; aqq += b * b; apq += a * b;
+                    }
+#pragma unroll
+                for (int o = GL / 2; o > 0; o >>= 1) {   // group-local reductions (all 32 lanes shuffle)
+                    app += __shfl_xor_sync(0xffffffffu, app, o);
+                    aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
+                    apq += __shfl_xor_sync(0xffffffffu, apq, o);
                 }
-                app = warp_sum(app); aqq = warp_sum(aqq); apq = warp_sum(apq);
-                if (app == 0.0 || aqq == 0.0) continue;
+                if (!act || app == 0.0 || aqq == 0.0) continue;
                 if (fabs(apq) <= tol * sqrt(app * aqq)) continue;
                 rotated = 1;
                 const double zeta = (aqq - app) / (2.0 * apq);
                 const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 const double c = 1.0 / sqrt(1.0 + tt * tt);
                 const double s = c * tt;
-                for (int i = lane; i < k; i += 32) {
-                    const double x = wp[i], y = wq[i];
-                    wp[i] = c * x - s * y; wq[i] = s * x + c * y;
-                }
                 double* vp = sV + p * KIN_MAX;
                 double* vq = sV + q * KIN_MAX;
-                for (int i = lane; i < k; i += 32) {
-                    const double x = vp[i], y = vq[i];
-                    vp[i] = c * x - s * y; vq[i] = s * x + c * y;
+                for (int i = gl; i < k; i += GL) {
+                    const double x = wp[i], y = wq[i];
+                    wp[i] = c * x - s * y; wq[i] = s * x + c * y;
+                    const double xv = vp[i], yv = vq[i];
+                    vp[i] = c * xv - s * yv; vq[i] = s * xv + c * yv;
                 }
-            }
-            __syncthreads();
-            // round-robin tournament rotation (slot top[0] fixed)
-            if (tid == 0) {
-                const int lastTop = sTop[npairs - 1];
-                const int firstBot = sBot[0];
-                for (int i = npairs - 1; i >= 2; --i) sTop[i] = sTop[i - 1];
-                if (npairs > 1) sTop[1] = firstBot;
-                for (int i = 0; i < npairs - 1; ++i) sBot[i] = sBot[i + 1];
-                sBot[npairs - 1] = lastTop;
-                if (npairs == 1) { sBot[0] = firstBot; }
             }
             __syncthreads();
         }

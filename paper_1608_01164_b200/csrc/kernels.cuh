@@ -87,8 +87,19 @@ struct CholItem {
     const double* M;
     double* W;
     int n, ldm, ldw;
+    double* D;         // optional: inverses of W's 32x32 diagonal blocks (for trsm_tile_dinv)
 };
-void launch_leaf_cholesky(const CholItem* d, int nitems, unsigned* status, cudaStream_t st);
+// inverses of the 32x32 diagonal blocks of upper-triangular leaves (W or R)
+struct DinvItem {
+    const double* W;
+    double* D;
+    int n, ldw;
+};
+void launch_leaf_dinv(const DinvItem* d, int nitems, unsigned* status, cudaStream_t st);
+void launch_leaf_cholesky(const CholItem* d, int nitems, unsigned* status, cudaStream_t st, int maxn);
+void leaf_init_attributes();
+void hsolve_init_attributes();
+int hsolve_tile_cols();
 
 // triangular solves with a dense upper-triangular leaf W (n x n):
 //  mode 0: X <- W^{-T} X   (forward, solve_WT leaf, hodlr.hpp:459-476)
@@ -101,6 +112,7 @@ struct TrsmItem {
     const int* ncp;    // number of right-hand sides (device) or nc
     int nc;
     int mode, rhs_t;
+    const double* D;   // optional diagonal-block inverses of W (trsm_tile_dinv)
 };
 void launch_leaf_trsm(const TrsmItem* d, const int2* d_ctas, int nctas, unsigned* status, cudaStream_t st);
 
@@ -121,6 +133,8 @@ struct DevHodlrView {
     double* V;
     int* rank;             // [2 * nnodes]
     int n;
+    double* dinv;          // per leaf: inverses of the 32x32 diagonal blocks (triangular factors only)
+    const long long* dinv_off;
 };
 // X (rows of subtree `root`, column-major, ld) <- W_sub^{-T} X (fwd) or W_sub^{-1} X (bwd)
 struct HSolveItem {
