@@ -7,6 +7,7 @@ Seeds: PR1 = 1, small-gap = 2, banded = 3, sweep = 40 + j, large = 5 (SURVEY.md 
 """
 CONFIGS = {
     "pr1": dict(n=2048, b=1, t1=1.0, t2=0.5, eps_dis=0.1, s=0.0, nmin=128, eps=1e-10, seed=1),
+    "sg4096": dict(n=4096, b=1, t1=1.0, t2=0.999, eps_dis=2e-4, s=0.0, nmin=256, eps=1e-10, seed=2),  # profiling
     "smallgap": dict(n=16384, b=1, t1=1.0, t2=0.999, eps_dis=2e-4, s=0.0, nmin=256, eps=1e-10, seed=2),
     "banded": dict(n=32768, b=8, t1=1.0, t2=0.8, eps_dis=0.0, s=0.05 / 17, nmin=256, eps=1e-10, seed=3),
     "sweep0.5": dict(n=65536, b=1, t1=1.0, t2=0.5, eps_dis=0.1, s=0.0, nmin=256, eps=1e-10, seed=40),

@@ -75,6 +75,7 @@ struct TTask {
     int nseg[2];       // segments per side
     long long ws;      // workspace base (doubles)
     long long wsz[2];  // workspace offsets of side 0/1 areas (relative to ws)
+    long long wcore;   // core-SVD scratch (KIN_MAX^2 doubles, relative to ws)
 };
 
 // Workspace layout of one task, per side (offsets in doubles, relative to the side base):

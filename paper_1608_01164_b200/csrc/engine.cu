@@ -227,7 +227,8 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
         }
         t.wsz[0] = 0;
         t.wsz[1] = ts_side_doubles(t.p, t.seg[0], t.nseg[0]);
-        t.ws = ws_->alloc(TS_HEADER + t.wsz[1] + ts_side_doubles(t.s, t.seg[1], t.nseg[1]));
+        t.wcore = TS_HEADER + t.wsz[1] + ts_side_doubles(t.s, t.seg[1], t.nseg[1]);
+        t.ws = ws_->alloc(t.wcore + (long long)KIN_MAX * KIN_MAX);
         for (int side = 0; side < 2; ++side) {
             for (int s = 0; s < t.nseg[side]; ++s) it0.push_back(make_int3((int)i, side, s));
             if (t.nseg[side] > 1) itm.push_back(make_int3((int)i, side, -1));

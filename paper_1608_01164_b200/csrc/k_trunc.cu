@@ -8,6 +8,8 @@
 //
 // Five launches per batch: tsqr(level 0) -> tsqr(merge) -> core -> apply(merge) -> apply(level 0).
 // Ranks are read from / written to device memory, so a batch never syncs the host.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -461,7 +463,11 @@ void trunc_init_attributes() {
     SPG_CUDA(cudaFuncSetAttribute(k_tsqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_tsqr()));
     SPG_CUDA(cudaFuncSetAttribute(k_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_core()));
     SPG_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_apply()));
+    core2_init_attributes();
 }
+
+// SPG_CORE_JACOBI=1 selects the unpreconditioned full-size Jacobi core (A/B checks)
+static const bool g_core_jacobi = std::getenv("SPG_CORE_JACOBI") != nullptr;
 
 void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* status, cudaStream_t st) {
     if (b.ntasks == 0) return;
@@ -471,8 +477,12 @@ void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* stat
         k_tsqr<<<b.n_itemsm, TS_THREADS, trunc_smem_tsqr(), st>>>(b.d_tasks, b.d_itemsm, ws, status, 1);
         SPG_LAUNCH_CHECK();
     }
-    k_core<<<b.ntasks, TS_THREADS, trunc_smem_core(), st>>>(b.d_tasks, ws, eps, status);
-    SPG_LAUNCH_CHECK();
+    if (g_core_jacobi) {
+        k_core<<<b.ntasks, TS_THREADS, trunc_smem_core(), st>>>(b.d_tasks, ws, eps, status);
+        SPG_LAUNCH_CHECK();
+    } else {
+        launch_core2(b.d_tasks, b.ntasks, ws, eps, status, st);
+    }
     if (b.n_itemsm) {
         k_apply<<<b.n_itemsm, TS_THREADS, trunc_smem_apply(), st>>>(b.d_tasks, b.d_itemsm, ws, 1);
         SPG_LAUNCH_CHECK();

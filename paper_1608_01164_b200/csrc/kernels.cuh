@@ -13,6 +13,8 @@ struct TruncBatch {
     int ntasks = 0, n_items0 = 0, n_itemsm = 0;
 };
 void trunc_init_attributes();
+void core2_init_attributes();
+void launch_core2(const TTask* tasks, int ntasks, double* ws, double eps, unsigned* status, cudaStream_t st);
 void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* status, cudaStream_t st);
 
 // ------------------------------------------------------------ batched DMMA GEMM
