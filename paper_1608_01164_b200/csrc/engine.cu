@@ -719,10 +719,114 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
 }
 
 // solve_upper_right (hodlr.hpp:579-604, 641-647): Y W = B
+// SPG_SOLVE_RECURSIVE=1 runs the solves in the reference's recursion order (one node per step)
+static const bool g_solve_recursive = std::getenv("SPG_SOLVE_RECURSIVE") != nullptr;
+
 void Engine::op_solve_upper_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work) {
     cur_op_ = 7;
     op_copy(p, B, work);
-    sur_rec(p, 0, work, W, Y);
+    if (g_solve_recursive) sur_rec(p, 0, work, W, Y);
+    else sur_levels(p, work, W, Y);
+}
+
+// Level-batched solve_ur_rec (hodlr.hpp:579-604).  Per node x the recursion does
+//   Y21 = B21 W11^{-1};  t = Y11 C12;  Y12 = trunc(B12 - t) W22^{-1};  B22 -= trunc(Y21 C12)
+// where Y21 / the cascade depend only on cascades from x's ancestors and Y12 only
+// on the finished left subtree.  So: phase A (top-down, all nodes of a depth in one
+// batch) computes every Y21 and cascade -- each block still receives its cascades
+// from the root downwards, exactly the recursion's order -- and phase B (bottom-up)
+// solves all leaves at once, then per depth the applies, rhs truncations and Y12.
+void Engine::sur_levels(Plan& p, DHodlr& B, const DHodlr& W, DHodlr& Y) {
+    const int n = tree_.n;
+    double* P0 = panel(0);
+    double* P1 = panel(1);
+    double* P2 = panel(2);
+    double* P3 = panel(3);
+    for (int t = 0; t < tree_.depth; ++t) {   // ---- phase A
+        const auto& xs = tree_.internal_at[t];
+        std::vector<CopyItem> cp;
+        std::vector<HSolveItem> hs;
+        std::vector<GemmItem> g1, g2;
+        std::vector<int3> c1, c2;
+        std::vector<RankOp> ro;
+        std::vector<TTask> tasks;
+        std::vector<Cascade> cs;
+        int maxm = 0;
+        for (int x : xs) {
+            const int l = tree_.left[x], r = tree_.right[x];
+            const int br = tree_.begin[r], s1 = tree_.size[l], s2 = tree_.size[r];
+            maxm = std::max(maxm, std::max(s1, s2));
+            cp.push_back(CopyItem{B.loU(x), Y.loU(x), s2, n, n, B.rlo(x), 0, 1.0, Y.rlo(x)});
+            cp.push_back(CopyItem{B.loV(x), Y.loV(x), s1, n, n, B.rlo(x), 0, 1.0, nullptr});
+            hs.push_back(HSolveItem{l, Y.loV(x), n, Y.rlo(x), 0, 0});
+            double* G = coef_ + (size_t)(4 * x + 3) * KCAP * KCAP;
+            int* q0 = iranks_ + 4 * x;
+            int* q1 = iranks_ + 4 * x + 1;
+            g1.push_back(gitem(Y.loV(x), n, 1, W.upU(x), n, 0, G, KCAP, 0, Y.rlo(x), 0, W.rup(x), s1, nullptr, 1.0, 0.0));
+            c1.push_back(make_int3(KCAP, KCAP, s1));
+            g2.push_back(gitem(Y.loU(x), n, 0, G, KCAP, 0, P1 + br, n, s2, nullptr, 0, W.rup(x), 0, Y.rlo(x), 1.0, 0.0));
+            c2.push_back(make_int3(s2, KCAP, KCAP));
+            ro.push_back(RankOp{q0, Y.rlo(x), W.rup(x)});
+            TTask tk{};
+            tk.p = s2; tk.s = s2; tk.ng = 1; tk.skipg = -1; tk.tag = 750000 + x;
+            tk.g[0] = TGroup{P1 + br, W.upV(x), n, n, q0, 0, 1.0, nullptr};
+            tk.ou = P2 + br; tk.ov = P3 + br; tk.ldou = tk.ldov = n; tk.orank = q1;
+            tasks.push_back(tk);
+            cs.push_back(Cascade{r, P2, P3, q1, -1.0});
+        }
+        copy(p, cp, maxm, KCAP);
+        hsolve(p, W, hs);
+        gemm(p, g1, c1);
+        gemm(p, g2, c2);
+        push_rankops(p, *arena_, ro);
+        trunc(p, tasks);
+        cascade(p, B, cs);
+    }
+    {   // ---- phase B: all leaves
+        std::vector<TrsmItem> ti;
+        std::vector<int2> ct;
+        std::vector<std::pair<const double*, double*>> cps;
+        std::vector<size_t> bytes;
+        for (int f : tree_.leaves) {
+            const int s = tree_.size[f];
+            cps.push_back({B.leaf(f), Y.leaf(f)});
+            bytes.push_back(sizeof(double) * s * s);
+            for (int c = 0; c < (s + 15) / 16; ++c) ct.push_back(make_int2((int)ti.size(), c));
+            ti.push_back(TrsmItem{W.leaf(f), Y.leaf(f), s, s, s, nullptr, s, 0, 1, W.leaf_dinv(f)});
+        }
+        const double* src = B.leaves;
+        double* dst = Y.leaves;
+        const size_t lb = sizeof(double) * B.leaf_doubles;
+        p.launches.push_back([=](cudaStream_t st) {
+            SPG_CUDA(cudaMemcpyAsync(dst, src, lb, cudaMemcpyDeviceToDevice, st));
+        });
+        const TrsmItem* d = arena_->push(ti);
+        const int2* dc = arena_->push(ct);
+        const int nc = (int)ct.size();
+        unsigned* status = sc_.status;
+        push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
+    }
+    for (int t = tree_.depth - 1; t >= 0; --t) {   // ---- phase B: internal levels, bottom-up
+        const auto& xs = tree_.internal_at[t];
+        std::vector<ApplyReq> rq;
+        std::vector<TTask> tasks;
+        std::vector<HSolveItem> hs;
+        for (int x : xs) {
+            const int l = tree_.left[x], r = tree_.right[x];
+            const int bl = tree_.begin[l], s1 = tree_.size[l], s2 = tree_.size[r];
+            rq.push_back(ApplyReq{&Y, l, 0, W.slabU(t), W.rup(x), P0});
+            TTask tk{};
+            tk.p = s1; tk.s = s2; tk.ng = 2; tk.skipg = -1; tk.tag = 700000 + x;
+            tk.g[0] = TGroup{B.upU(x), B.upV(x), n, n, B.rup(x), 0, 1.0, nullptr};
+            tk.g[1] = TGroup{P0 + bl, W.upV(x), n, n, W.rup(x), 0, -1.0, nullptr};
+            tk.ou = Y.upU(x); tk.ov = Y.upV(x); tk.ldou = tk.ldov = n; tk.orank = Y.rup(x);
+            tasks.push_back(tk);
+            hs.push_back(HSolveItem{r, Y.upV(x), n, Y.rup(x), 0, 0});
+        }
+        apply(p, rq);
+        trunc(p, tasks);
+        hsolve(p, W, hs);
+    }
 }
 
 void Engine::sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
@@ -792,7 +896,100 @@ void Engine::sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
 void Engine::op_solve_upperT_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work) {
     cur_op_ = 8;
     op_copy(p, B, work);
-    surt_rec(p, 0, work, W, Y);
+    if (g_solve_recursive) surt_rec(p, 0, work, W, Y);
+    else surt_levels(p, work, W, Y);
+}
+
+// Level-batched solve_urt_rec (hodlr.hpp:607-636), same reordering as sur_levels:
+// phase A (top-down): Y12 = B12 W22^{-T} and the cascade B11 -= trunc(Y12 C12^T);
+// phase B (bottom-up): leaves, then per depth t = Y22 C12^T, rhs, Y21 = rhs W11^{-T}.
+void Engine::surt_levels(Plan& p, DHodlr& B, const DHodlr& W, DHodlr& Y) {
+    const int n = tree_.n;
+    double* P0 = panel(0);
+    double* P1 = panel(1);
+    double* P2 = panel(2);
+    double* P3 = panel(3);
+    for (int t = 0; t < tree_.depth; ++t) {   // ---- phase A
+        const auto& xs = tree_.internal_at[t];
+        std::vector<CopyItem> cp;
+        std::vector<HSolveItem> hs;
+        std::vector<GemmItem> g1, g2;
+        std::vector<int3> c1, c2;
+        std::vector<RankOp> ro;
+        std::vector<TTask> tasks;
+        std::vector<Cascade> cs;
+        int maxm = 0;
+        for (int x : xs) {
+            const int l = tree_.left[x], r = tree_.right[x];
+            const int bl = tree_.begin[l], s1 = tree_.size[l], s2 = tree_.size[r];
+            maxm = std::max(maxm, std::max(s1, s2));
+            cp.push_back(CopyItem{B.upU(x), Y.upU(x), s1, n, n, B.rup(x), 0, 1.0, Y.rup(x)});
+            cp.push_back(CopyItem{B.upV(x), Y.upV(x), s2, n, n, B.rup(x), 0, 1.0, nullptr});
+            hs.push_back(HSolveItem{r, Y.upV(x), n, Y.rup(x), 0, 1});
+            double* G = coef_ + (size_t)(4 * x + 3) * KCAP * KCAP;
+            int* q0 = iranks_ + 4 * x + 2;
+            int* q1 = iranks_ + 4 * x + 3;
+            g1.push_back(gitem(Y.upV(x), n, 1, W.upV(x), n, 0, G, KCAP, 0, Y.rup(x), 0, W.rup(x), s2, nullptr, 1.0, 0.0));
+            c1.push_back(make_int3(KCAP, KCAP, s2));
+            g2.push_back(gitem(Y.upU(x), n, 0, G, KCAP, 0, P1 + bl, n, s1, nullptr, 0, W.rup(x), 0, Y.rup(x), 1.0, 0.0));
+            c2.push_back(make_int3(s1, KCAP, KCAP));
+            ro.push_back(RankOp{q0, Y.rup(x), W.rup(x)});
+            TTask tk{};
+            tk.p = s1; tk.s = s1; tk.ng = 1; tk.skipg = -1; tk.tag = 850000 + x;
+            tk.g[0] = TGroup{P1 + bl, W.upU(x), n, n, q0, 0, 1.0, nullptr};
+            tk.ou = P2 + bl; tk.ov = P3 + bl; tk.ldou = tk.ldov = n; tk.orank = q1;
+            tasks.push_back(tk);
+            cs.push_back(Cascade{l, P2, P3, q1, -1.0});
+        }
+        copy(p, cp, maxm, KCAP);
+        hsolve(p, W, hs);
+        gemm(p, g1, c1);
+        gemm(p, g2, c2);
+        push_rankops(p, *arena_, ro);
+        trunc(p, tasks);
+        cascade(p, B, cs);
+    }
+    {   // ---- phase B: all leaves
+        std::vector<TrsmItem> ti;
+        std::vector<int2> ct;
+        for (int f : tree_.leaves) {
+            const int s = tree_.size[f];
+            for (int c = 0; c < (s + 15) / 16; ++c) ct.push_back(make_int2((int)ti.size(), c));
+            ti.push_back(TrsmItem{W.leaf(f), Y.leaf(f), s, s, s, nullptr, s, 1, 1, W.leaf_dinv(f)});
+        }
+        const double* src = B.leaves;
+        double* dst = Y.leaves;
+        const size_t lb = sizeof(double) * B.leaf_doubles;
+        p.launches.push_back([=](cudaStream_t st) {
+            SPG_CUDA(cudaMemcpyAsync(dst, src, lb, cudaMemcpyDeviceToDevice, st));
+        });
+        const TrsmItem* d = arena_->push(ti);
+        const int2* dc = arena_->push(ct);
+        const int nc = (int)ct.size();
+        unsigned* status = sc_.status;
+        push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
+    }
+    for (int t = tree_.depth - 1; t >= 0; --t) {   // ---- phase B: internal levels, bottom-up
+        const auto& xs = tree_.internal_at[t];
+        std::vector<ApplyReq> rq;
+        std::vector<TTask> tasks;
+        std::vector<HSolveItem> hs;
+        for (int x : xs) {
+            const int l = tree_.left[x], r = tree_.right[x];
+            const int br = tree_.begin[r], s1 = tree_.size[l], s2 = tree_.size[r];
+            rq.push_back(ApplyReq{&Y, r, 0, W.slabV(t), W.rup(x), P0});
+            TTask tk{};
+            tk.p = s2; tk.s = s1; tk.ng = 2; tk.skipg = -1; tk.tag = 800000 + x;
+            tk.g[0] = TGroup{B.loU(x), B.loV(x), n, n, B.rlo(x), 0, 1.0, nullptr};
+            tk.g[1] = TGroup{P0 + br, W.upU(x), n, n, W.rup(x), 0, -1.0, nullptr};
+            tk.ou = Y.loU(x); tk.ov = Y.loV(x); tk.ldou = tk.ldov = n; tk.orank = Y.rlo(x);
+            tasks.push_back(tk);
+            hs.push_back(HSolveItem{l, Y.loV(x), n, Y.rlo(x), 0, 1});
+        }
+        apply(p, rq);
+        trunc(p, tasks);
+        hsolve(p, W, hs);
+    }
 }
 
 void Engine::surt_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {

@@ -184,6 +184,8 @@ private:
     void chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W);
     void sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y);
     void surt_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y);
+    void sur_levels(Plan& p, DHodlr& B, const DHodlr& W, DHodlr& Y);
+    void surt_levels(Plan& p, DHodlr& B, const DHodlr& W, DHodlr& Y);
     double* panel(int which);   // persistent global-row panels (n x KCAP)
 
     HTree tree_;
