@@ -5,7 +5,10 @@
 // replayed or captured into a CUDA graph.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 
 #include "engine.cuh"
 
@@ -166,7 +169,7 @@ void Engine::push_timed(Plan& p, int cls, Launch l) {
     cudaEvent_t a, b;
     SPG_CUDA(cudaEventCreate(&a));
     SPG_CUDA(cudaEventCreate(&b));
-    prof_.push_back({cls, a, b});
+    prof_.push_back({cls, cur_op_, a, b});
     p.launches.push_back([a](cudaStream_t s) { SPG_CUDA(cudaEventRecord(a, s)); });
     p.launches.push_back(std::move(l));
     p.launches.push_back([b](cudaStream_t s) { SPG_CUDA(cudaEventRecord(b, s)); });
@@ -179,6 +182,20 @@ void Engine::prof_sum(double* ms, long long* nb) const {
         SPG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
         ms[r.cls] += t;
         nb[r.cls] += 1;
+    }
+    if (std::getenv("SPG_PROF_DUMP")) {   // per (operation, kernel class) breakdown on stderr
+        static const char* cn[PC_NCLS] = {"trunc", "gemm", "hsolve", "leaf"};
+        std::map<std::pair<int, int>, std::pair<double, int>> agg;
+        for (const auto& r : prof_) {
+            float t = 0.f;
+            SPG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            auto& e = agg[{r.op, r.cls}];
+            e.first += t;
+            e.second += 1;
+        }
+        for (const auto& kv : agg)
+            std::fprintf(stderr, "prof op=%d cls=%s ms=%.2f batches=%d\n", kv.first.first, cn[kv.first.second],
+                         kv.second.first, kv.second.second);
     }
 }
 

@@ -202,7 +202,7 @@ private:
     std::vector<std::unique_ptr<DHodlr>> owned_;
     int cur_op_ = 0;
     bool profile_ = false;
-    struct ProfRec { int cls; cudaEvent_t a, b; };
+    struct ProfRec { int cls, op; cudaEvent_t a, b; };
     std::vector<ProfRec> prof_;
 };
 

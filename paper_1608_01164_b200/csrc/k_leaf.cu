@@ -203,8 +203,10 @@ __global__ void __launch_bounds__(512) k_leaf_chol(const CholItem* __restrict__ 
 //   (1) panel update P = M[J:, J:J+32] - L[J:, :J] L[J:J+32, :J]^T on the FP64
 //       tensor path (mma.sync m8n8k4 -> DMMA), L staged through shared memory
 //       in 16-column chunks (one tile feeds both operands);
-//   (2) right-looking elimination of the panel in shared memory (one barrier per
-//       column, unscaled Gaussian form, columns scaled by 1/sqrt(pivot) at the end);
+//   (2) the 32x32 diagonal block factored by one warp in registers (rows per lane,
+//       columns broadcast by shuffles), then the rows below solved against it one
+//       row per thread (L21 = P21 L11^{-T}) while warp 0 forms W_bb^{-1} = L11^{-T}
+//       for the subtree solves -- two CTA barriers per panel;
 //   (3) L written transposed into W (= L^T, cholesky_upper, dense_factor.hpp:222).
 constexpr int CH_NB = 32, CH_KC = 16, CH_NMAX = 576, CH_THREADS = 512;
 __device__ __forceinline__ void dmma_leaf(double& d0, double& d1, double a, double b) {
@@ -220,7 +222,8 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
     const int ldp = n + 1;
     double* sP = sm;                   // panel: (n - J) x CH_NB, col-major ld ldp
     double* sL = sm + ldp * CH_NB;     // L chunk: (n - J) x CH_KC
-    __shared__ double sPiv[CH_NB];
+    __shared__ double sL11[32 * 33];
+    __shared__ double sInv[32];
     __shared__ int sFail;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CH_THREADS / 32;
     if (tid == 0) sFail = 0;
@@ -276,34 +279,97 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
                 }
         }
         __syncthreads();
-        // (2) right-looking elimination of the panel
-        for (int jj = 0; jj < nb; ++jj) {
-            double d = sP[jj + jj * ldp];
-            if (!(d > 0.0)) { if (tid == 0) sFail = 1; d = 1.0; }
-            if (tid == 0) sPiv[jj] = d;
-            const double inv = 1.0 / d;
-            const int rows = mr - jj - 1, cols = nb - jj - 1;
-            for (int idx = tid; idx < rows * cols; idx += blockDim.x) {
-                const int i = jj + 1 + idx % rows, kk = jj + 1 + idx / rows;
-                if (i >= kk) sP[i + kk * ldp] -= sP[i + jj * ldp] * sP[kk + jj * ldp] * inv;
+        // (2a) warp 0: Cholesky of the nb x nb diagonal block, lane i holding row i
+        //      in registers (column j of L broadcast by shuffles)
+        if (warp == 0) {
+            double r[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) r[c] = (lane < nb && c <= lane && c < nb) ? sP[lane + c * ldp] : 0.0;
+            bool fail = false;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j < nb) {
+                    double d = __shfl_sync(0xffffffffu, r[j], j);
+                    if (!(d > 0.0)) { fail = true; d = 1.0; }
+                    // sqrt and 1/sqrt by Newton steps on the MUFU seed (no slow-path calls,
+                    // which would spill the register rows)
+                    double y;
+                    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+                    y = fma(0.5 * y, fma(-d * y, y, 1.0), y);
+                    y = fma(0.5 * y, fma(-d * y, y, 1.0), y);
+                    double ljj = d * y;
+                    ljj = fma(0.5 * y, fma(-ljj, ljj, d), ljj);
+                    const double lij = lane == j ? ljj : r[j] * y;
+                    if (lane == 0) sInv[j] = y;
+                    r[j] = lij;
+#pragma unroll
+                    for (int k = j + 1; k < 32; ++k) {
+                        const double lkj = __shfl_sync(0xffffffffu, lij, k);
+                        if (lane >= k) r[k] -= lij * lkj;
+                    }
+                }
             }
-            __syncthreads();
-        }
-        // (3) L(J+i, J+jj) = P[i][jj] / sqrt(pivot_jj)  ->  W(J+jj, J+i)
-        for (int idx = tid; idx < mr * nb; idx += blockDim.x) {
-            const int jj = idx % nb, i = idx / nb;
-            if (i >= jj) C.W[(J + jj) + (long long)(J + i) * C.ldw] = sP[i + jj * ldp] / sqrt(sPiv[jj]);
+            if (fail && lane == 0) sFail = 1;
+            // L11 (row lane) into sL11 (identity-padded) and back into the panel
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const bool in = lane < nb && c < nb;
+                sL11[lane * 33 + c] = in ? (c <= lane ? r[c] : 0.0) : (c == lane ? 1.0 : 0.0);
+                if (in && c <= lane) sP[lane + c * ldp] = r[c];
+            }
+            if (lane >= nb) sInv[lane] = 1.0;
         }
         __syncthreads();
-    }
-    if (C.D) {   // inverses of W's 32x32 diagonal blocks for trsm_tile_dinv, 4 warps
-        double* sT = sm;   // reuse the panel buffer (>= 4 x 32 x 33 doubles, see launcher)
-        bool sing = false;
-        if (warp < 4)
-            for (int blk = warp; blk * 32 < n; blk += 4)
-                sing |= invert_diag_block_warp(C.W, C.ldw, blk * 32, min(32, n - blk * 32),
-                                               C.D + (long long)blk * 1024, sT + warp * 32 * 33);
-        if (sing) atomicOr(status, ST_SINGULAR);
+        if (warp == 0) {
+            // (2c) D = W_bb^{-1} = (L11^{-1})^T: lane i forms row i of L11^{-1} (t L11 = e_i,
+            //      solved right-looking from the last column) = column i of D
+            if (C.D) {
+                double tv[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) tv[c] = c == lane ? 1.0 : 0.0;
+                bool sing = false;
+#pragma unroll
+                for (int j = 31; j >= 0; --j) {
+                    if (sL11[j * 33 + j] == 0.0) sing = true;
+                    tv[j] = tv[j] * sInv[j];
+#pragma unroll
+                    for (int k = 0; k < j; ++k) tv[k] -= tv[j] * sL11[j * 33 + k];
+                }
+                double* D = C.D + (long long)(J / 32) * 1024;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) D[c + 32 * lane] = (lane < nb && c < nb) ? tv[c] : 0.0;
+                if (sing) atomicOr(status, ST_SINGULAR);
+            }
+        } else {
+            // (2b) rows below the diagonal block: L21 = P21 L11^{-T}, one row per thread
+            // volatile: keeps the compiler from hoisting all 528 L11 loads out of the row loop
+            const volatile double* vL11 = sL11;
+            const volatile double* vInv = sInv;
+#pragma unroll 1
+            for (int i = nb + tid - 32; i < mr; i += blockDim.x - 32) {
+                double r[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) r[c] = c < nb ? sP[i + c * ldp] : 0.0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (j < nb) {
+                        r[j] = r[j] * vInv[j];
+#pragma unroll
+                        for (int k = j + 1; k < 32; ++k) r[k] -= r[j] * vL11[k * 33 + j];
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    if (c < nb) sP[i + c * ldp] = r[c];
+            }
+        }
+        __syncthreads();
+        // (3) L(J+i, J+jj) -> W(J+jj, J+i)
+        for (int idx = tid; idx < mr * nb; idx += blockDim.x) {
+            const int jj = idx % nb, i = idx / nb;
+            if (i >= jj) C.W[(J + jj) + (long long)(J + i) * C.ldw] = sP[i + jj * ldp];
+        }
+        __syncthreads();
     }
     if (tid == 0 && sFail) atomicOr(status, ST_NPD);
 }

@@ -252,6 +252,10 @@ __global__ void __launch_bounds__(32) k_est_l0_w(int n, int b, const double* __r
 
 void launch_estimate_l0(int n, int b, const double* bands, const double* alpha, double* lu_work, int* piv,
                         double* vecs, double* out_l0, unsigned* status, cudaStream_t st) {
+    if (b == 1 && n >= 2) {   // tridiagonal: k_tri.cu (caller provides >= 9 n doubles at lu_work)
+        launch_est_l0_tri(n, bands, alpha, lu_work, out_l0, status, st);
+        return;
+    }
     k_est_l0_w<<<1, 32, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status);
     SPG_LAUNCH_CHECK();
 }
@@ -382,6 +386,10 @@ __global__ void __launch_bounds__(32) k_givens_w(int n, int b, double* R, double
 
 void launch_givens_reduce(int n, int b, const double* bands, const double* slots, double* work, double* rdiag,
                           cudaStream_t st) {
+    if (b == 1 && n >= 2) {   // tridiagonal: k_tri.cu
+        launch_givens_tri(n, bands, slots, rdiag, st);
+        return;
+    }
     const int w = 3 * b + 1, jw = b > 1 ? b - 1 : 1;
     double* R = work;
     double* rowN = R + (long long)n * w;

@@ -1,0 +1,313 @@
+// Setup recurrences for tridiagonal inputs (b = 1), the BASELINE dimer chains:
+//   * banded LU with partial pivoting + Hager 1-norm estimate -> l0
+//     (estimate_l0 / hager_norm1 / BandedLu, estimates.hpp:40-80, banded_lu.hpp:16-93)
+//   * reduce_tridiag: Givens reduction of [s A; I] -> R (fast_qr.hpp:177-232)
+// Each is a dependent chain over the rows, so one warp runs it with every value
+// carried in registers.  All 32 lanes execute the recurrence redundantly (warp-
+// uniform control flow); lane 0 stores.  The inputs are streamed into a ring of
+// shared-memory chunks by cp.async several chunks ahead of the recurrence, so the
+// chain never waits on L2/HBM latency -- without this a lone thread streaming
+// through global memory stalls on every cache-line miss.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spg {
+
+constexpr int PCH = 128;   // elements per chunk
+constexpr int PST = 4;     // ring stages: PST - 1 chunks in flight ahead of the one being consumed
+constexpr int PNA = 4;     // max streams per loop
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// NA input streams read in step order kk = 0, 1, ...: stream a at step kk is
+// p[a][(rev ? hi - kk : kk) + off[a]], 0 outside [0, len[a]).
+template <int NA>
+struct Ring {
+    const double* p[NA];
+    long long off[NA];
+    long long len[NA];
+    long long hi;
+    bool rev;
+    double* buf;   // PST * NA * PCH doubles of shared memory
+    __device__ void issue(long long q, int lane) {
+        double* sb = buf + (q % PST) * NA * PCH;
+#pragma unroll
+        for (int a = 0; a < NA; ++a)
+            for (int e = lane; e < PCH; e += 32) {
+                const long long kk = q * PCH + e;
+                const long long idx = (rev ? hi - kk : kk) + off[a];
+                if (idx >= 0 && idx < len[a]) cp_async8(sb + a * PCH + e, p[a] + idx);
+                else sb[a * PCH + e] = 0.0;
+            }
+        cp_commit();
+    }
+};
+
+// body(k, v): step k with the NA stream values v[0..NA)
+template <int NA, class Body>
+__device__ __forceinline__ void run_ring(Ring<NA>& R, long long count, int lane, Body&& body) {
+    __syncwarp();
+    const long long nq = (count + PCH - 1) / PCH;
+#pragma unroll 1
+    for (int q = 0; q < PST - 1; ++q) R.issue(q, lane);
+#pragma unroll 1
+    for (long long q = 0; q < nq; ++q) {
+        cp_wait<PST - 2>();
+        __syncwarp();
+        R.issue(q + PST - 1, lane);   // refills the slot consumed in step q - 1
+        const double* sb = R.buf + (q % PST) * NA * PCH;
+        const long long k0 = q * PCH;
+#pragma unroll 1
+        for (int e0 = 0; e0 < PCH; e0 += 8) {
+            double v[8][NA];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int a = 0; a < NA; ++a) v[u][a] = sb[a * PCH + e0 + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const long long k = k0 + e0 + u;
+                if (k < count) body(k, v[u]);
+            }
+        }
+    }
+    cp_wait<0>();
+    __syncwarp();
+}
+
+struct TriLU {   // factor of A / alpha, column j: U(j-2,j), U(j-1,j), U(j,j), 1/U(j,j), L(j+1,j), interchange
+    double *u2, *u1, *u0, *ri, *lm, *sw;
+};
+
+// x = A^{-1} in: interchanges + L forward, then U backward (BandedLu::solve)
+__device__ void tri_solve(const TriLU& F, int n, const double* in, double* out, double* sbuf, int lane) {
+    double cur = in[0];
+    {
+        Ring<3> R{{in, F.sw, F.lm}, {1, 0, 0}, {n, n, n}, 0, false, sbuf};
+        run_ring(R, n - 1, lane, [&](long long k, const double* v) {
+            double nxt = v[0];
+            if (v[1] != 0.0) { const double t = cur; cur = nxt; nxt = t; }
+            if (lane == 0) out[k] = cur;
+            cur = nxt - v[2] * cur;
+        });
+    }
+    if (lane == 0) out[n - 1] = cur;
+    __syncwarp();
+    double a = cur;           // current x[j]
+    double bq = out[n - 2];   // current x[j-1]
+    {
+        Ring<4> R{{F.ri, F.u1, F.u2, out}, {0, 0, 0, -2}, {n, n, n, n}, n - 1, true, sbuf};
+        run_ring(R, n, lane, [&](long long jj, const double* v) {
+            const long long j = n - 1 - jj;
+            const double xj = a * v[0];
+            if (lane == 0) out[j] = xj;
+            a = bq - v[1] * xj;
+            bq = v[3] - v[2] * xj;
+        });
+    }
+}
+
+// x = A^{-T} in: U^T forward, then L^T backward with the interchanges (BandedLu::solve_transposed)
+__device__ void tri_solve_t(const TriLU& F, int n, const double* in, double* out, double* sbuf, int lane) {
+    double xm2 = 0.0, xm1 = 0.0;
+    {
+        Ring<4> R{{F.u2, F.u1, F.ri, in}, {0, 0, 0, 0}, {n, n, n, n}, 0, false, sbuf};
+        run_ring(R, n, lane, [&](long long j, const double* v) {
+            const double s = v[0] * xm2 + v[1] * xm1;
+            const double xj = (v[3] - s) * v[2];
+            if (lane == 0) out[j] = xj;
+            xm2 = xm1;
+            xm1 = xj;
+        });
+    }
+    double c1 = xm1;   // current x[k+1]
+    {
+        Ring<3> R{{out, F.lm, F.sw}, {0, 0, 0}, {n, n, n}, n - 2, true, sbuf};
+        run_ring(R, n - 1, lane, [&](long long kk, const double* v) {
+            const long long k = n - 2 - kk;
+            const double nv = v[0] - v[1] * c1;
+            if (v[2] != 0.0) {
+                if (lane == 0) out[k + 1] = nv;   // x[k] keeps the carried x[k+1]
+            } else {
+                if (lane == 0) out[k + 1] = c1;
+                c1 = nv;
+            }
+        });
+    }
+    if (lane == 0) out[0] = c1;
+    __syncwarp();
+}
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(32) k_est_l0_tri(int n, const double* __restrict__ bands, const double* alpha_p,
+                                                  double* work, double* vecs, double* out, unsigned* status) {
+    __shared__ __align__(16) double sbuf[PST * PNA * PCH];
+    const int lane = threadIdx.x;
+    const double alpha = *alpha_p;
+    const double ia = 1.0 / alpha;
+    const double* dg = bands;
+    const double* of = bands + n;
+    TriLU F{work, work + n, work + 2 * (size_t)n, work + 3 * (size_t)n, work + 4 * (size_t)n, work + 5 * (size_t)n};
+    // norm1 (banded.hpp:94-106): max column sum (order independent)
+    double m = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        double cs = fabs(dg[i]);
+        if (i + 1 < n) cs += fabs(of[i]);
+        if (i >= 1) cs += fabs(of[i - 1]);
+        m = fmax(m, cs);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const double n1 = m / alpha;
+    // factor (banded_lu.hpp:66-88, b = 1): row k = (a0, a1, 0) carried, row k+1 original
+    for (int i = lane; i < 2; i += 32) { F.u1[i] = 0.0; F.u2[i] = 0.0; }
+    double a0 = dg[0] * ia, a1 = of[0] * ia;
+    bool singular = false;
+    {
+        Ring<3> R{{of, dg, of}, {0, 1, 1}, {n - 1, n, n - 1}, 0, false, sbuf};
+        run_ring(R, n - 1, lane, [&](long long k, const double* v) {
+            const double e = v[0] * ia, d1 = v[1] * ia, e1 = v[2] * ia;
+            const bool swp = fabs(e) > fabs(a0);
+            double p0 = a0, p1 = a1, p2 = 0.0, q0 = e, q1 = d1, q2 = e1;
+            if (swp) { p0 = e; p1 = d1; p2 = e1; q0 = a0; q1 = a1; q2 = 0.0; }
+            if (p0 == 0.0) singular = true;
+            const double inv = 1.0 / p0;
+            const double mm = q0 * inv;
+            if (mm != 0.0) { q1 -= mm * p1; q2 -= mm * p2; }
+            if (lane == 0) {
+                F.u0[k] = p0; F.ri[k] = inv; F.lm[k] = mm; F.sw[k] = swp ? 1.0 : 0.0;
+                F.u1[k + 1] = p1;
+                if (k + 2 < n) F.u2[k + 2] = p2;
+            }
+            a0 = q1; a1 = q2;
+        });
+    }
+    if (a0 == 0.0) singular = true;
+    if (lane == 0) { F.u0[n - 1] = a0; F.ri[n - 1] = 1.0 / a0; F.lm[n - 1] = 0.0; F.sw[n - 1] = 0.0; }
+    if (singular) {
+        if (lane == 0) { atomicOr(status, ST_SINGULAR); out[0] = 0.0; }
+        return;
+    }
+    __syncwarp();
+    // hager_norm1 (estimates.hpp:40-68)
+    double* x = vecs;
+    double* y = vecs + n;
+    double* z = vecs + 2 * (size_t)n;
+    for (int i = lane; i < n; i += 32) x[i] = 1.0 / n;
+    __syncwarp();
+    double est = 0.0;
+    for (int it = 0; it < 5; ++it) {
+        tri_solve(F, n, x, y, sbuf, lane);
+        __syncwarp();
+        double e = 0.0;
+        for (int i = lane; i < n; i += 32) e += fabs(y[i]);
+        e = wsum(e);
+        if (it > 0 && e <= est) break;
+        est = e;
+        for (int i = lane; i < n; i += 32) z[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+        __syncwarp();
+        tri_solve_t(F, n, z, y, sbuf, lane);   // y <- A^{-T} z
+        double zmax = 0.0, ztx = 0.0;
+        int j = 0x7fffffff;
+        for (int i = lane; i < n; i += 32) {
+            const double a = fabs(y[i]);
+            if (a > zmax) { zmax = a; j = i; }
+            ztx += y[i] * x[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double oz = __shfl_xor_sync(0xffffffffu, zmax, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+            if (oz > zmax || (oz == zmax && oj < j)) { zmax = oz; j = oj; }
+        }
+        ztx = wsum(ztx);
+        if (j == 0x7fffffff) j = 0;
+        if (zmax <= ztx) break;
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) x[i] = i == j ? 1.0 : 0.0;
+        __syncwarp();
+    }
+    if (lane == 0) out[0] = n1 / (sqrt((double)n) * (n1 * est));
+}
+
+__device__ __forceinline__ void givens_cs_t(double f, double g, double& c, double& s) {   // givens.hpp:27-36
+    if (g == 0.0) { c = 1.0; s = 0.0; return; }
+    if (f == 0.0) { c = 0.0; s = 1.0; return; }
+    const double af = fabs(f), ag = fabs(g);
+    const double scale = af + ag;
+    const double fs = f / scale, gs = g / scale;
+    double r = scale * sqrt(fs * fs + gs * gs);
+    if (f < 0.0) r = -r;
+    c = f / r;
+    s = g / r;
+}
+
+// reduce_tridiag: per row t the rotations alpha_{t,t} (rowN_t against aux_t = 1),
+// beta_t (R_tt against rowN_t, carrying R_{t,t+1} into rowN_{t+1}) and gamma_t
+// (row t against the original row t+1, filling R_{t,t+2}); row t of R is final
+// after gamma_t.  Same rotations and arithmetic as the band kernel (k_seq.cu).
+__global__ void __launch_bounds__(32) k_givens_tri(int n, const double* __restrict__ bands, const double* slots,
+                                                  double* __restrict__ rdiag) {
+    __shared__ __align__(16) double sbuf[PST * PNA * PCH];
+    const int lane = threadIdx.x;
+    const double sA = slots[5];
+    const double* dg = bands;
+    const double* of = bands + n;
+    double* r0 = rdiag;
+    double* r1 = rdiag + n;
+    double* r2 = rdiag + 2 * (size_t)n;
+    double a0 = dg[0] * sA, a1 = of[0] * sA, a2 = 0.0;
+    double rn = 1.0;   // rowN_t
+    Ring<3> R{{of, dg, of}, {0, 1, 1}, {n - 1, n, n - 1}, 0, false, sbuf};
+    run_ring(R, n, lane, [&](long long t, const double* v) {
+        double c, s;
+        if (t > 0) {   // alpha_{t,t}
+            givens_cs_t(rn, 1.0, c, s);
+            rn = c * rn + s * 1.0;
+        }
+        double rn1 = 0.0;
+        givens_cs_t(a0, rn, c, s);   // beta_t
+        a0 = c * a0 + s * rn;
+        if (t + 1 < n) {
+            const double x = a1;
+            a1 = c * x + s * 0.0;
+            rn1 = -s * x + c * 0.0;
+            const double b0 = v[0] * sA, b1 = v[1] * sA, b2 = v[2] * sA;   // original row t+1
+            givens_cs_t(a0, b0, c, s);                                     // gamma_{t,t+1}
+            const double n0 = c * a0 + s * b0;
+            const double n1 = c * a1 + s * b1;
+            const double q1 = -s * a1 + c * b1;
+            double n2 = 0.0, q2 = b2;
+            if (t + 2 < n) { n2 = c * a2 + s * b2; q2 = -s * a2 + c * b2; }
+            if (lane == 0) { r0[t] = n0; r1[t] = n1; r2[t] = n2; }
+            a0 = q1; a1 = q2; a2 = 0.0;
+        } else {
+            if (lane == 0) { r0[t] = a0; r1[t] = 0.0; r2[t] = 0.0; }
+        }
+        rn = rn1;
+    });
+}
+
+void launch_est_l0_tri(int n, const double* bands, const double* alpha, double* work, double* out_l0,
+                       unsigned* status, cudaStream_t st) {
+    k_est_l0_tri<<<1, 32, 0, st>>>(n, bands, alpha, work, work + 6 * (size_t)n, out_l0, status);
+    SPG_LAUNCH_CHECK();
+}
+
+void launch_givens_tri(int n, const double* bands, const double* slots, double* rdiag, cudaStream_t st) {
+    k_givens_tri<<<1, 32, 0, st>>>(n, bands, slots, rdiag);
+    SPG_LAUNCH_CHECK();
+}
+
+}  // namespace spg

@@ -162,6 +162,10 @@ void launch_iter_params(const double* sched, int* counter, double* slots, const 
 // mode 1: upper-banded R with diags rdiag[d*n+i] = R(i, i+d), d = 0..bu)
 void launch_from_band(DevTree t, DevHodlrView H, int mode, int b, const double* bands, const double* scalep,
                       double scale_mult, cudaStream_t st);
+// b = 1 specialisations (k_tri.cu): work >= 9 n doubles
+void launch_est_l0_tri(int n, const double* bands, const double* alpha, double* work, double* out_l0,
+                       unsigned* status, cudaStream_t st);
+void launch_givens_tri(int n, const double* bands, const double* slots, double* rdiag, cudaStream_t st);
 // work: n*(3b+1) + 2n + n*max(b-1,1) doubles; slots[5] = sqrt(c0)/alpha
 void launch_givens_reduce(int n, int b, const double* bands, const double* slots, double* work, double* rdiag,
                           cudaStream_t st);
