@@ -609,6 +609,13 @@ int spg_measure_dmma_tflops(double* out) {
 }
 int spg_kcap(void) { return KCAP; }
 
+int spg_micro_kernel(int which, int n, int reps, double* out, int nout) {
+    return guarded([&]() {
+        ensure_device();
+        if (micro_kernel(which, n, reps, out, nout) != 0) throw std::invalid_argument("spg_micro_kernel: unknown kernel");
+    });
+}
+
 int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double delta, spg_result** out) {
     *out = nullptr;
     return guarded([&]() {

@@ -12,11 +12,16 @@
 // so B' = (Q_u Zu)(Q_v Zv)^T.  The rotations are accumulated exactly and the
 // sigma-carrying side is W itself, so |B - B'| stays at u |C| + dropped part.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace spg {
+
+__device__ long long* g_core_trace = nullptr;   // micro-benchmarks: clock64 per phase of task 0
+void set_core_trace(long long* p) { SPG_CUDA(cudaMemcpyToSymbol(g_core_trace, &p, sizeof(p))); }
+#define CORE_TRACE(k) do { if (g_core_trace && blockIdx.x == 0 && threadIdx.x == 0) g_core_trace[k] = clock64(); } while (0)
 
 
 __device__ __forceinline__ double csum(double v) {
@@ -52,9 +57,8 @@ __device__ __forceinline__ double* core_z(const TTask& t, double* ws, int side) 
            (long long)KIN_MAX * KCAP;
 }
 
-__global__ void __launch_bounds__(TS_THREADS) k_core2(const TTask* __restrict__ tasks, double* __restrict__ ws,
-                                                     double eps, unsigned* status) {
-    extern __shared__ double smem[];
+__device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double* __restrict__ ws, double eps,
+                                       unsigned* status, double* smem) {
     double* sA = smem;                       // k x k, ld KIN_MAX: C -> QR; later V_J (r' x r')
     double* sZ = sA + KIN_MAX * KIN_MAX;     // k x r', ld KIN_MAX: Z = R'^T -> W -> Zu
     __shared__ double sCn[KIN_MAX], sTau[KIN_MAX], sSig[KIN_MAX], sRed[32];
@@ -75,6 +79,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_core2(const TTask* __restrict__ 
         if (tid == 0) { hdr[0] = 0; hdr[1] = 0; *t.orank = 0; }
         return;
     }
+    CORE_TRACE(0);
     const double* Ru = core_final_R(t, ws, 0);
     const double* Rv = core_final_R(t, ws, 1);
     // C[i][j] = sum_l Ru[i][l] Rv[j][l], l >= max(i, j); Frobenius norm for the noise floor
@@ -103,6 +108,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_core2(const TTask* __restrict__ 
     }
     __syncthreads();
     const double delta = sDelta;
+    CORE_TRACE(1);
     // ---- Householder QR with column pivoting (stop at small remaining norms)
     int rr = 0;
     for (int j = 0; j < k; ++j) {
@@ -174,6 +180,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_core2(const TTask* __restrict__ 
         rr = j + 1;
     }
     const int rp = rr;
+    CORE_TRACE(2);
     // ---- spill the reflectors (needed for Zu) to the task's core scratch, Z = R'^T (k x rp), V_J = I
     double* gR = ws + t.ws + t.wcore;
     for (int idx = tid; idx < k * k; idx += blockDim.x) {
@@ -191,6 +198,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_core2(const TTask* __restrict__ 
         sJ[i + j * KIN_MAX] = i == j ? 1.0 : 0.0;
     }
     __syncthreads();
+    CORE_TRACE(3);
+    int nsweeps = 0;
     // ---- one-sided Jacobi on the columns of Z (circle-method rounds, 8-lane groups)
     if (rp > 1) {
         const int kk = rp + (rp & 1);
@@ -250,10 +259,13 @@ __global__ void __launch_bounds__(TS_THREADS) k_core2(const TTask* __restrict__ 
             }
             if (rotated) sRot = 1;
             __syncthreads();
+            ++nsweeps;
             if (!sRot) break;
             __syncthreads();
         }
     }
+    CORE_TRACE(4);
+    if (g_core_trace && blockIdx.x == 0 && tid == 0) { g_core_trace[8] = nsweeps; g_core_trace[9] = rp; g_core_trace[10] = k; }
     // ---- singular values, ordering, rank
     for (int j = warp; j < rp; j += nwarps) {
         double s = 0.0;
@@ -326,16 +338,391 @@ __global__ void __launch_bounds__(TS_THREADS) k_core2(const TTask* __restrict__ 
     }
     __syncthreads();
     if (tid == 0) *t.orank = r;
+    CORE_TRACE(5);
+}
+
+// ---------------------------------------------------------------------------
+// k <= 64 core, latency-optimised (the Cholesky critical path truncates one block
+// at a time, so this kernel's latency is the cost that matters):
+//   * R_u, R_v staged once into shared memory, C = R_u R_v^T on DMMA 8x8 tiles;
+//   * QRCP with ONE barrier per column: every warp recomputes the pivot (argmax
+//     of the column norms) and the reflector redundantly, then updates the
+//     columns it owns (physical column c belongs to warp c mod 16) and their
+//     norms; pivoted columns stay in place (logical order in sPerm);
+//   * one-sided Jacobi with a half-warp per column pair (circle-method round
+//     schedule precomputed), one barrier per round (__syncthreads_or doubles as
+//     the convergence vote), rotation parameters from MUFU seeds + Newton steps;
+//   * Zu = Q_c V_J by reflectors from shared memory, four columns per warp.
+constexpr int K3 = 64, L3 = 65;
+
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr3(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
+    return fma(0.5 * y, fma(-x * y, y, 1.0), y);
+}
+__device__ __forceinline__ double sqrt_nr(double x) {
+    const double y = rsqrt_nr3(x);
+    const double r = x * y;
+    return fma(0.5 * y, fma(-r, r, x), r);
+}
+__device__ __forceinline__ void dmma_c(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, double eps, unsigned* status,
+                           double* smem) {
+    double* sZ = smem;                 // R_u, then Z (k x rp)
+    double* sJ = smem + K3 * L3;       // R_v, then V_J (rp x rp)
+    double* sC = smem + 2 * K3 * L3;   // C, then R (rows) + reflectors (below the diagonal)
+    __shared__ double sCn2[2][K3], sBeta[K3], sTau[K3], sScal[K3], sSig[K3], sRed3[16];
+    __shared__ int sPerm3[K3], sAct[K3], sOrd3[K3], sR3;
+    __shared__ double sDelta3;
+    __shared__ unsigned short sPairs[63 * 32];
+    int* dbg = reinterpret_cast<int*>(status + 4);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gi = lane >> 2, gk = lane & 3;
+    double* hdr = ws + t.ws;
+    CORE_TRACE(0);
+    const double* Ru = core_final_R(t, ws, 0);
+    const double* Rv = core_final_R(t, ws, 1);
+    for (int idx = tid; idx < K3 * K3; idx += TS_THREADS) {
+        const int i = idx & 63, j = idx >> 6;
+        const bool in = i < k && j < k && i <= j;
+        sZ[i + j * L3] = in ? Ru[i + (long long)j * KIN_MAX] : 0.0;
+        sJ[i + j * L3] = in ? Rv[i + (long long)j * KIN_MAX] : 0.0;
+    }
+    if (tid < K3) { sAct[tid] = 1; sCn2[0][tid] = -1.0; sCn2[1][tid] = -1.0; }
+    __syncthreads();
+    // C[i][j] = sum_l Ru[i][l] Rv[j][l]
+    const int nt8 = (k + 7) / 8, nks = (k + 3) / 4;
+    double fro = 0.0;
+    for (int tile = warp; tile < 64; tile += 16) {
+        const int mt = tile & 7, nt = tile >> 3;
+        double c0 = 0.0, c1 = 0.0;
+        if (mt < nt8 && nt < nt8)
+            for (int ks = 0; ks < nks; ++ks)
+                dmma_c(c0, c1, sZ[(mt * 8 + gi) + (ks * 4 + gk) * L3], sJ[(nt * 8 + gi) + (ks * 4 + gk) * L3]);
+        const int i = mt * 8 + gi, j = nt * 8 + 2 * gk;
+        sC[i + j * L3] = c0;
+        sC[i + (j + 1) * L3] = c1;
+        fro += c0 * c0 + c1 * c1;
+    }
+    fro = csum(fro);
+    if (lane == 0) sRed3[warp] = fro;
+    __syncthreads();
+    if (warp == 0) {
+        double v = lane < 16 ? sRed3[lane] : 0.0;
+        v = csum(v);
+        if (lane == 0) sDelta3 = fmax(1e-3 * eps / sqrt((double)k), 16.0 * DBL_EPSILON * sqrt(v));
+    }
+    for (int c = warp; c < k; c += 16) {
+        const double a0 = sC[lane + c * L3], a1 = sC[lane + 32 + c * L3];
+        const double s = csum(a0 * a0 + a1 * a1);
+        if (lane == 0) sCn2[0][c] = sqrt(s);
+    }
+    __syncthreads();
+    const double delta = sDelta3;
+    CORE_TRACE(1);
+    // ---- QRCP
+    // column norms double-buffered (read cur, write nxt; -1 = pivoted or absent) so
+    // that the redundant per-warp pivot search never races with the updates
+    int rp = 0, pprev = -1;
+    for (int j = 0; j < k; ++j) {
+        const double* cur = sCn2[j & 1];
+        double* nxt = sCn2[(j + 1) & 1];
+        double best = cur[lane];
+        if (!(best == best)) best = -1.0;   // NaN (non-finite input) counts as pivoted: keeps every warp's pivot identical
+        int p = lane;
+        {
+            double b1 = cur[lane + 32];
+            if (!(b1 == b1)) b1 = -1.0;
+            if (b1 > best) { best = b1; p = lane + 32; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int op = __shfl_xor_sync(0xffffffffu, p, o);
+            if (ob > best || (ob == best && op < p)) { best = ob; p = op; }
+        }
+        if (best <= delta) break;
+        const double* xp = sC + p * L3;
+        const double x0 = (lane > j && lane < k) ? xp[lane] : 0.0;
+        const double x1 = (lane + 32 > j && lane + 32 < k) ? xp[lane + 32] : 0.0;
+        const double s2 = csum(x0 * x0 + x1 * x1);
+        const double alpha = xp[j];
+        double tau = 0.0, scal = 0.0, beta = alpha;
+        if (s2 > 0.0) {
+            const double nrm = sqrt(alpha * alpha + s2);
+            beta = alpha > 0.0 ? -nrm : nrm;
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        const double v0 = x0 * scal, v1 = x1 * scal;
+        double a0[4], a1[4], aj[4], d[4];
+        bool act[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int c = warp + 16 * m;
+            act[m] = c < k && c != p && cur[c] >= 0.0;
+            const double* col = sC + c * L3;
+            a0[m] = (act[m] && lane > j && lane < k) ? col[lane] : 0.0;
+            a1[m] = (act[m] && lane + 32 > j && lane + 32 < k) ? col[lane + 32] : 0.0;
+            aj[m] = act[m] ? col[j] : 0.0;
+            d[m] = v0 * a0[m] + v1 * a1[m];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) d[m] += __shfl_xor_sync(0xffffffffu, d[m], o);
+        double ns[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const double w = tau * (d[m] + aj[m]);
+            aj[m] -= w;
+            a0[m] -= w * v0;
+            a1[m] -= w * v1;
+            ns[m] = a0[m] * a0[m] + a1[m] * a1[m];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) ns[m] += __shfl_xor_sync(0xffffffffu, ns[m], o);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            if (!act[m]) continue;
+            double* col = sC + (warp + 16 * m) * L3;
+            if (lane > j && lane < k) col[lane] = a0[m];
+            if (lane + 32 > j && lane + 32 < k) col[lane + 32] = a1[m];
+            if (lane == 0) { col[j] = aj[m]; nxt[warp + 16 * m] = sqrt(ns[m]); }
+        }
+        if (tid == 0) {
+            sPerm3[j] = p; sBeta[j] = beta; sTau[j] = tau; sScal[j] = scal;
+            nxt[p] = -1.0;
+            if (pprev >= 0) nxt[pprev] = -1.0;
+        }
+        pprev = p;
+        __syncthreads();
+        rp = j + 1;
+    }
+    CORE_TRACE(2);
+    // reflector tails scaled in place, R(j, j) = beta_j; unpivoted columns appended to the order
+    for (int j = warp; j < rp; j += 16) {
+        double* col = sC + sPerm3[j] * L3;
+        const double sc = sScal[j];
+        if (lane > j && lane < k) col[lane] *= sc;
+        if (lane + 32 > j && lane + 32 < k) col[lane + 32] *= sc;
+        if (lane == 0) col[j] = sBeta[j];
+    }
+    if (tid == 0) {
+        for (int j = 0; j < rp; ++j) sAct[sPerm3[j]] = 0;
+        int q = rp;
+        for (int c = 0; c < k; ++c) if (sAct[c]) sPerm3[q++] = c;
+    }
+    __syncthreads();
+    // Z = R'^T (k x rp), V_J = I, round schedule
+    for (int idx = tid; idx < K3 * K3; idx += TS_THREADS) {
+        const int c = idx & 63, a = idx >> 6;
+        if (a < rp) sZ[c + a * L3] = (c < k && a <= c) ? sC[a + sPerm3[c] * L3] : 0.0;
+        if (c < rp && a < rp) sJ[c + a * L3] = c == a ? 1.0 : 0.0;
+    }
+    const int kk = rp + (rp & 1), npairs = kk / 2, mrr = kk - 1;
+    for (int idx = tid; idx < mrr * npairs; idx += TS_THREADS) {
+        const int r = idx / npairs, pi = idx % npairs;
+        int p, q;
+        if (pi == 0) { p = r; q = kk - 1; }
+        else { p = (r + pi) % mrr; q = (r - pi + mrr) % mrr; }
+        if (p > q) { const int tmp = p; p = q; q = tmp; }
+        sPairs[r * 32 + pi] = (unsigned short)(p | (q << 8));
+    }
+    __syncthreads();
+    CORE_TRACE(3);
+    int nsweeps = 0;
+    if (rp > 1) {
+        const int h = tid >> 4, hl = tid & 15;
+        const unsigned hmask = 0xFFFFu << (lane & 16);
+        const double tol = 1e-15;
+        for (int sweep = 0; sweep < 60; ++sweep) {
+            int any = 0;
+            for (int r = 0; r < mrr; ++r) {
+                int rot = 0;
+                if (h < npairs) {
+                    const unsigned pq = sPairs[r * 32 + h];
+                    const int p = pq & 255, q = pq >> 8;
+                    if (q < rp) {
+                        double zp[4], zq[4];
+                        double app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int i = hl + 16 * m;
+                            zp[m] = i < k ? sZ[i + p * L3] : 0.0;
+                            zq[m] = i < k ? sZ[i + q * L3] : 0.0;
+                            app += zp[m] * zp[m];
+                            aqq += zq[m] * zq[m];
+                            apq += zp[m] * zq[m];
+                        }
+#pragma unroll
+                        for (int o = 8; o > 0; o >>= 1) {
+                            app += __shfl_xor_sync(hmask, app, o);
+                            aqq += __shfl_xor_sync(hmask, aqq, o);
+                            apq += __shfl_xor_sync(hmask, apq, o);
+                        }
+                        if (app > 0.0 && aqq > 0.0 && fabs(apq) > tol * sqrt_nr(app * aqq)) {
+                            rot = 1;
+                            const double zeta = (aqq - app) * rcp_nr(2.0 * apq);
+                            const double az = fabs(zeta);
+                            double tt;
+                            if (az > 1e100) tt = 0.5 * rcp_nr(zeta);
+                            else tt = copysign(1.0, zeta) * rcp_nr(az + sqrt_nr(fma(zeta, zeta, 1.0)));
+                            const double c = rsqrt_nr3(fma(tt, tt, 1.0));
+                            const double s = c * tt;
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const int i = hl + 16 * m;
+                                if (i < k) {
+                                    sZ[i + p * L3] = c * zp[m] - s * zq[m];
+                                    sZ[i + q * L3] = s * zp[m] + c * zq[m];
+                                }
+                                if (i < rp) {
+                                    const double x = sJ[i + p * L3], y = sJ[i + q * L3];
+                                    sJ[i + p * L3] = c * x - s * y;
+                                    sJ[i + q * L3] = s * x + c * y;
+                                }
+                            }
+                        }
+                    }
+                }
+                any |= __syncthreads_or(rot);
+            }
+            ++nsweeps;
+            if (!any) break;
+        }
+    }
+    CORE_TRACE(4);
+    if (g_core_trace && blockIdx.x == 0 && tid == 0) { g_core_trace[8] = nsweeps; g_core_trace[9] = rp; g_core_trace[10] = k; }
+    // ---- singular values, order, rank
+    for (int j = warp; j < rp; j += 16) {
+        const double a0 = lane < k ? sZ[lane + j * L3] : 0.0;
+        const double a1 = lane + 32 < k ? sZ[lane + 32 + j * L3] : 0.0;
+        const double s = csum(a0 * a0 + a1 * a1);
+        if (lane == 0) {
+            if (!(s == s)) atomicOr(status, ST_NONFINITE);
+            sSig[j] = s == s ? sqrt(s) : -1.0;   // NaN sorts last (total order keeps sOrd a permutation)
+        }
+    }
+    __syncthreads();
+    if (tid < rp) {
+        const double sj = sSig[tid];
+        int pos = 0;
+        for (int i = 0; i < rp; ++i) {
+            const double si = sSig[i];
+            pos += (si > sj) || (si == sj && i < tid);
+        }
+        sOrd3[pos] = tid;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int r = 0;
+        while (r < rp && sSig[sOrd3[r]] > eps) ++r;
+        if (r > KCAP) {
+            if (atomicOr(status, ST_RANK_CAP) == 0 || dbg[0] == 0) {
+                dbg[0] = t.tag + 1; dbg[1] = t.p; dbg[2] = t.s; dbg[3] = k; dbg[4] = r;
+            }
+            r = KCAP;
+        }
+        sR3 = r;
+        hdr[0] = k; hdr[1] = r;
+        if (rp > 0 && !(sSig[sOrd3[0]] == sSig[sOrd3[0]])) atomicOr(status, ST_NONFINITE);
+        double* ctr = reinterpret_cast<double*>(status + 16);
+        atomicAdd(ctr, 8.0 * (double)(t.p + t.s) * (double)(k + r));
+        atomicAdd(ctr + 2, 1.0);
+    }
+    __syncthreads();
+    const int r = sR3;
+    double* Zu = core_z(t, ws, 0);
+    double* Zv = core_z(t, ws, 1);
+    for (int idx = tid; idx < k * r; idx += TS_THREADS) {   // Zv[perm[c]][j] = W[c][ord_j] (carries sigma)
+        const int c = idx % k, j = idx / k;
+        Zv[sPerm3[c] + (long long)j * KIN_MAX] = sZ[c + sOrd3[j] * L3];
+    }
+    // Zu = Q_c [V_J(:, ord); 0]: four columns per warp, reflectors rp-1 .. 0
+    {
+        double x0[4], x1[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int j = warp + 16 * m;
+            const int oj = j < r ? sOrd3[j] : 0;
+            x0[m] = (j < r && lane < rp) ? sJ[lane + oj * L3] : 0.0;
+            x1[m] = (j < r && lane + 32 < rp) ? sJ[lane + 32 + oj * L3] : 0.0;
+        }
+        if (warp < r)
+            for (int hh = rp - 1; hh >= 0; --hh) {
+                const double tau = sTau[hh];
+                if (tau == 0.0) continue;
+                const double* col = sC + sPerm3[hh] * L3;
+                const double v0 = lane == hh ? 1.0 : ((lane > hh && lane < k) ? col[lane] : 0.0);
+                const double v1 = lane + 32 == hh ? 1.0 : ((lane + 32 > hh && lane + 32 < k) ? col[lane + 32] : 0.0);
+                double d[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) d[m] = v0 * x0[m] + v1 * x1[m];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) d[m] += __shfl_xor_sync(0xffffffffu, d[m], o);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const double w = tau * d[m];
+                    x0[m] -= w * v0;
+                    x1[m] -= w * v1;
+                }
+            }
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int j = warp + 16 * m;
+            if (j < r) {
+                if (lane < k) Zu[lane + (long long)j * KIN_MAX] = x0[m];
+                if (lane + 32 < k) Zu[lane + 32 + (long long)j * KIN_MAX] = x1[m];
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) *t.orank = r;
+    CORE_TRACE(5);
+}
+
+__global__ void __launch_bounds__(TS_THREADS) k_core_any(const TTask* __restrict__ tasks, double* __restrict__ ws,
+                                                        double eps, unsigned* status, int use3) {
+    extern __shared__ double smem[];
+    const TTask& t = tasks[blockIdx.x];
+    if (use3 && !core_skip(t)) {
+        int k = core_kin(t);
+        if (k > 0 && k <= K3) {
+            core3_body(t, k, ws, eps, status, smem);
+            return;
+        }
+    }
+    core2_body(tasks, ws, eps, status, smem);
 }
 
 size_t core2_smem() { return sizeof(double) * (2 * KIN_MAX * KIN_MAX); }
+static const bool g_core2_only = std::getenv("SPG_CORE2") != nullptr;
 
 void core2_init_attributes() {
-    SPG_CUDA(cudaFuncSetAttribute(k_core2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)core2_smem()));
+    SPG_CUDA(cudaFuncSetAttribute(k_core_any, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)core2_smem()));
 }
 
 void launch_core2(const TTask* tasks, int ntasks, double* ws, double eps, unsigned* status, cudaStream_t st) {
-    k_core2<<<ntasks, TS_THREADS, core2_smem(), st>>>(tasks, ws, eps, status);
+    k_core_any<<<ntasks, TS_THREADS, core2_smem(), st>>>(tasks, ws, eps, status, g_core2_only ? 0 : 1);
     SPG_LAUNCH_CHECK();
 }
 

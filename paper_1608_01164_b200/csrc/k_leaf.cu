@@ -1,4 +1,6 @@
 // Dense-leaf and elementwise kernels of the HODLR arithmetic (sm_100a, FP64).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "leaf_dev.cuh"
@@ -215,55 +217,96 @@ __device__ __forceinline__ void dmma_leaf(double& d0, double& d1, double a, doub
                  : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async8_l(double* dst, const double* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit_l() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait_l() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr int CH_STG = 3;   // cp.async ring stages of the panel-update K loop
+template <int KC>
+struct CholCfg {
+    static constexpr int KCP = KC == 16 ? 20 : KC;   // chunk row pitch: conflict-free m8n8k4 fragment reads
+};
+__host__ __device__ inline int chol_ldp(int n) { return ((n + 15) / 16) * 16 + 4; }
+
+template <int KC>
 __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __restrict__ it, unsigned* status) {
     extern __shared__ double sm[];
+    constexpr int KCP = CholCfg<KC>::KCP;
     const CholItem C = it[blockIdx.x];
     const int n = C.n;
-    const int ldp = n + 1;
+    const int ldp = chol_ldp(n);
     double* sP = sm;                   // panel: (n - J) x CH_NB, col-major ld ldp
-    double* sL = sm + ldp * CH_NB;     // L chunk: (n - J) x CH_KC
+    double* sRing = sm + ldp * CH_NB;  // CH_STG chunks of L: (n - J) rows x KC, row pitch KCP
+    const int ring_stride = n * KCP;
     __shared__ double sL11[32 * 33];
     __shared__ double sInv[32];
     __shared__ int sFail;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CH_THREADS / 32;
+    const int gi = lane >> 2, gk = lane & 3;
     if (tid == 0) sFail = 0;
     for (long long idx = tid; idx < (long long)n * n; idx += blockDim.x) {
         const int i = idx % n, j = idx / n;
         if (i > j) C.W[i + (long long)j * C.ldw] = 0.0;
     }
+    long long* tr = C.trace;
+#define CH_TRACE(k) if (tr && tid == 0) tr[(J / CH_NB) * 8 + (k)] = clock64()
     for (int J = 0; J < n; J += CH_NB) {
         const int nb = min(CH_NB, n - J), mr = n - J;           // panel columns / rows
         const int nrt = (mr + 7) / 8;
+        const int nch = J / KC;
+        CH_TRACE(0);
+        // group 0 also carries the M panel: sP[i + jj ld] = M[J+i, J+jj]
+        for (int idx = tid; idx < mr * nb; idx += CH_THREADS) {
+            const int i = idx % mr, jj = idx / mr;
+            cp_async8_l(sP + i + jj * ldp, C.M + (J + i) + (long long)(J + jj) * C.ldm);
+        }
+        auto issue = [&](int c) {
+            if (c < nch) {
+                double* dst = sRing + (c % CH_STG) * ring_stride;
+                const int l0 = c * KC;
+                for (int idx = tid; idx < mr * KC; idx += CH_THREADS) {
+                    const int kk = idx % KC, i = idx / KC;
+                    cp_async8_l(dst + i * KCP + kk, C.W + (l0 + kk) + (long long)(J + i) * C.ldw);   // L(J+i, l0+kk)
+                }
+            }
+            cp_commit_l();
+        };
+        issue(0);
+        issue(1);
         double acc[5][4][2];
 #pragma unroll
         for (int a = 0; a < 5; ++a)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
-        // (1) S = L[J:, :J] L[J:J+nb, :J]^T
-        for (int l0 = 0; l0 < J; l0 += CH_KC) {
+        // (1) S = L[J:, :J] L[J:J+nb, :J]^T, K pipelined through the ring
+        for (int c = 0; c < nch; ++c) {
+            cp_wait_l<1>();
             __syncthreads();
-            for (int idx = tid; idx < mr * CH_KC; idx += blockDim.x) {
-                const int kk = idx % CH_KC, i = idx / CH_KC;
-                sL[i + kk * ldp] = C.W[(l0 + kk) + (long long)(J + i) * C.ldw];   // L(J+i, l0+kk)
-            }
-            __syncthreads();
+            issue(c + 2);
+            const double* sL = sRing + (c % CH_STG) * ring_stride;
 #pragma unroll
-            for (int ks = 0; ks < CH_KC; ks += 4) {
+            for (int ks = 0; ks < KC; ks += 4) {
                 double bf[4];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) bf[c] = sL[(c * 8 + (lane >> 2)) + (ks + (lane & 3)) * ldp];
+                for (int cc = 0; cc < 4; ++cc) bf[cc] = sL[(cc * 8 + gi) * KCP + ks + gk];
 #pragma unroll
                 for (int a = 0; a < 5; ++a) {
                     const int rt = warp + a * nw;
                     if (rt < nrt) {
-                        const double af = sL[(rt * 8 + (lane >> 2)) + (ks + (lane & 3)) * ldp];
+                        const double af = sL[(rt * 8 + gi) * KCP + ks + gk];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) dmma_leaf(acc[a][c][0], acc[a][c][1], af, bf[c]);
+                        for (int cc = 0; cc < 4; ++cc) dmma_leaf(acc[a][cc][0], acc[a][cc][1], af, bf[cc]);
                     }
                 }
             }
         }
+        cp_wait_l<0>();
         __syncthreads();
+        CH_TRACE(1);
         // P = M[J+i, J+jj] - S  (lower part only is meaningful)
 #pragma unroll
         for (int a = 0; a < 5; ++a) {
@@ -273,12 +316,12 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
             for (int c = 0; c < 4; ++c)
 #pragma unroll
                 for (int v = 0; v < 2; ++v) {
-                    const int i = rt * 8 + (lane >> 2), jj = c * 8 + 2 * (lane & 3) + v;
-                    if (i < mr && jj < nb && i >= jj)
-                        sP[i + jj * ldp] = C.M[(J + i) + (long long)(J + jj) * C.ldm] - acc[a][c][v];
+                    const int i = rt * 8 + gi, jj = c * 8 + 2 * gk + v;
+                    if (i < mr && jj < nb && i >= jj) sP[i + jj * ldp] -= acc[a][c][v];
                 }
         }
         __syncthreads();
+        CH_TRACE(2);
         // (2a) warp 0: Cholesky of the nb x nb diagonal block, lane i holding row i
         //      in registers (column j of L broadcast by shuffles)
         if (warp == 0) {
@@ -320,6 +363,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
             if (lane >= nb) sInv[lane] = 1.0;
         }
         __syncthreads();
+        CH_TRACE(3);
         if (warp == 0) {
             // (2c) D = W_bb^{-1} = (L11^{-1})^T: lane i forms row i of L11^{-1} (t L11 = e_i,
             //      solved right-looking from the last column) = column i of D
@@ -364,13 +408,16 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
             }
         }
         __syncthreads();
+        CH_TRACE(4);
         // (3) L(J+i, J+jj) -> W(J+jj, J+i)
         for (int idx = tid; idx < mr * nb; idx += blockDim.x) {
             const int jj = idx % nb, i = idx / nb;
             if (i >= jj) C.W[(J + jj) + (long long)(J + i) * C.ldw] = sP[i + jj * ldp];
         }
         __syncthreads();
+        CH_TRACE(5);
     }
+#undef CH_TRACE
     if (tid == 0 && sFail) atomicOr(status, ST_NPD);
 }
 
@@ -391,11 +438,217 @@ void launch_leaf_dinv(const DinvItem* d, int nitems, unsigned* status, cudaStrea
     SPG_LAUNCH_CHECK();
 }
 
+// Leaf Cholesky v3 (leaves n <= C3_NMAX), 32-column panels, left-looking; per panel
+//   (1) S = L[J:, :J] L[J:J+32, :J]^T split over warps as (8-row tile, K segment)
+//       tasks (every warp busy whatever the panel), fragments loaded straight from
+//       the already-written W (L2) with 8 k-steps of loads in flight, partial tiles
+//       reduced in a fixed order (deterministic) into P = M - S (M panel prefetched
+//       by cp.async at the panel start);
+//   (2) warp 0 factors the 32x32 diagonal block, rows in registers, the new column
+//       broadcast through shared memory; then the rows below are solved one row per
+//       thread (L21 = P21 L11^{-T}) while warp 0 forms W_bb^{-1} = L11^{-T};
+//   each thread writes its finished row of L straight into W (= L^T).
+// Three CTA barriers per panel.
+constexpr int C3_NMAX = 288, C3_TASKS = 40;
+__device__ __forceinline__ double rsqrt_nr(double d, double& root) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    y = fma(0.5 * y, fma(-d * y, y, 1.0), y);
+    y = fma(0.5 * y, fma(-d * y, y, 1.0), y);
+    double l = d * y;
+    root = fma(0.5 * y, fma(-l, l, d), l);
+    return y;
+}
+
+__global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __restrict__ it, unsigned* status) {
+    extern __shared__ double sm[];
+    const CholItem C = it[blockIdx.x];
+    const int n = C.n;
+    const int ldp = chol_ldp(n);
+    double* sP = sm;                     // panel (n - J) x 32, col-major ld ldp
+    double* sPart = sm + ldp * CH_NB;    // C3_TASKS partial 8 x 32 tiles (row-major)
+    __shared__ double sL11[32 * 33];
+    __shared__ double sInv[32];
+    __shared__ double sCol[32];
+    __shared__ int sFail;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gi = lane >> 2, gk = lane & 3;
+    const long long ldw = C.ldw;
+    if (tid == 0) sFail = 0;
+    for (long long idx = tid; idx < (long long)n * n; idx += CH_THREADS) {
+        const int i = idx % n, j = idx / n;
+        if (i > j) C.W[i + (long long)j * ldw] = 0.0;
+    }
+    long long* tr = C.trace;
+#define C3_TRACE(k) if (tr && tid == 0) tr[(J / CH_NB) * 8 + (k)] = clock64()
+    for (int J = 0; J < n; J += CH_NB) {
+        const int nb = min(CH_NB, n - J), mr = n - J;
+        const int nrt = (mr + 7) / 8;
+        C3_TRACE(0);
+        for (int idx = tid; idx < mr * nb; idx += CH_THREADS) {
+            const int i = idx % mr, jj = idx / mr;
+            cp_async8_l(sP + i + jj * ldp, C.M + (J + i) + (long long)(J + jj) * C.ldm);
+        }
+        cp_commit_l();
+        // (1) partial S tiles
+        const int nks = J / 4;
+        int nseg = nks > 0 ? max(1, min(nks / 8, C3_TASKS / nrt)) : 0;
+        const int ntask = nrt * nseg;
+        for (int task = warp; task < ntask; task += CH_THREADS / 32) {
+            const int rt = task / nseg, seg = task % nseg;
+            const int ks0 = seg * nks / nseg, ks1 = (seg + 1) * nks / nseg;
+            const int row = J + rt * 8 + gi;
+            const double* pa = C.W + (long long)min(row, n - 1) * ldw + gk;   // L(row, k) = W(k, row)
+            const double* pb[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) pb[c] = C.W + (long long)(J + min(c * 8 + gi, nb - 1)) * ldw + gk;
+            double acc[4][2];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+            int ks = ks0;
+            for (; ks + 8 <= ks1; ks += 8) {
+                double a[8], b[8][4];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    a[u] = pa[4 * (ks + u)];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) b[u][c] = pb[c][4 * (ks + u)];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) dmma_leaf(acc[c][0], acc[c][1], a[u], b[u][c]);
+            }
+            for (; ks < ks1; ++ks) {
+                const double a = pa[4 * ks];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) dmma_leaf(acc[c][0], acc[c][1], a, pb[c][4 * ks]);
+            }
+            double* pt = sPart + task * 256 + gi * 32;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                pt[c * 8 + 2 * gk] = acc[c][0];
+                pt[c * 8 + 2 * gk + 1] = acc[c][1];
+            }
+        }
+        cp_wait_l<0>();
+        __syncthreads();
+        C3_TRACE(1);
+        if (nseg > 0)
+            for (int idx = tid; idx < mr * nb; idx += CH_THREADS) {
+                const int i = idx % mr, jj = idx / mr;
+                if (i < jj) continue;
+                const int rt = i >> 3;
+                const double* pt = sPart + (rt * nseg) * 256 + (i & 7) * 32 + jj;
+                double s = 0.0;
+                for (int sg = 0; sg < nseg; ++sg) s += pt[sg * 256];
+                sP[i + jj * ldp] -= s;
+            }
+        __syncthreads();
+        C3_TRACE(2);
+        // (2a) diagonal block, warp 0
+        if (warp == 0) {
+            double r[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) r[c] = (lane < nb && c <= lane && c < nb) ? sP[lane + c * ldp] : 0.0;
+            bool fail = false;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j < nb) {
+                    double d = __shfl_sync(0xffffffffu, r[j], j);
+                    if (!(d > 0.0)) { fail = true; d = 1.0; }
+                    double ljj;
+                    const double y = rsqrt_nr(d, ljj);
+                    const double lij = lane == j ? ljj : r[j] * y;
+                    r[j] = lij;
+                    sCol[lane] = lij;
+                    if (lane == 0) sInv[j] = y;
+                    __syncwarp();
+#pragma unroll
+                    for (int k = j + 1; k < 32; ++k) r[k] -= lij * sCol[k];
+                    __syncwarp();
+                }
+            }
+            if (fail && lane == 0) sFail = 1;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const bool in = lane < nb && c < nb;
+                sL11[lane * 33 + c] = in ? (c <= lane ? r[c] : 0.0) : (c == lane ? 1.0 : 0.0);
+            }
+            if (lane < nb) {
+                double* wcol = C.W + J + (long long)(J + lane) * ldw;   // W(J.., J+lane) = L(J+lane, J..)
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    if (c <= lane) wcol[c] = r[c];
+            }
+            if (lane >= nb) sInv[lane] = 1.0;
+        }
+        __syncthreads();
+        C3_TRACE(3);
+        if (warp == 0) {
+            if (C.D) {   // (2c) D = W_bb^{-1} = (L11^{-1})^T, lane i -> row i of L11^{-1} = column i of D
+                double tv[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) tv[c] = c == lane ? 1.0 : 0.0;
+                bool sing = false;
+#pragma unroll
+                for (int j = 31; j >= 0; --j) {
+                    if (sL11[j * 33 + j] == 0.0) sing = true;
+                    tv[j] = tv[j] * sInv[j];
+#pragma unroll
+                    for (int k = 0; k < j; ++k) tv[k] -= tv[j] * sL11[j * 33 + k];
+                }
+                double* D = C.D + (long long)(J / 32) * 1024;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) D[c + 32 * lane] = (lane < nb && c < nb) ? tv[c] : 0.0;
+                if (sing) atomicOr(status, ST_SINGULAR);
+            }
+        } else {
+            // (2b) L21 = P21 L11^{-T}, one row per thread, written straight to W
+            const volatile double* vL11 = sL11;
+            const volatile double* vInv = sInv;
+#pragma unroll 1
+            for (int i = nb + tid - 32; i < mr; i += CH_THREADS - 32) {
+                double r[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) r[c] = c < nb ? sP[i + c * ldp] : 0.0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (j < nb) {
+                        r[j] = r[j] * vInv[j];
+#pragma unroll
+                        for (int k = j + 1; k < 32; ++k) r[k] -= r[j] * vL11[k * 33 + j];
+                    }
+                }
+                double* wcol = C.W + J + (long long)(J + i) * ldw;
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    if (c < nb) wcol[c] = r[c];
+            }
+        }
+        __syncthreads();
+        C3_TRACE(4);
+        C3_TRACE(5);
+    }
+#undef C3_TRACE
+    if (tid == 0 && sFail) atomicOr(status, ST_NPD);
+}
+
+static size_t chol3_smem(int n) { return sizeof(double) * ((size_t)chol_ldp(n) * CH_NB + (size_t)C3_TASKS * 256); }
+
+static size_t chol2_smem(int kc, int n) {
+    const int kcp = kc == 16 ? 20 : kc;
+    return sizeof(double) * ((size_t)chol_ldp(n) * CH_NB + (size_t)CH_STG * n * kcp);
+}
+
 void launch_leaf_cholesky(const CholItem* d, int nitems, unsigned* status, cudaStream_t st, int maxn) {
     if (!nitems) return;
-    if (maxn <= CH_NMAX) {
-        const size_t sm = sizeof(double) * std::max((maxn + 1) * (CH_NB + CH_KC), 4 * 32 * 33);
-        k_leaf_chol2<<<nitems, CH_THREADS, sm, st>>>(d, status);
+    if (maxn <= C3_NMAX && !std::getenv("SPG_CHOL_V2")) {
+        k_leaf_chol3<<<nitems, CH_THREADS, chol3_smem(maxn), st>>>(d, status);
+    } else if (maxn <= 256) {
+        k_leaf_chol2<16><<<nitems, CH_THREADS, chol2_smem(16, maxn), st>>>(d, status);
+    } else if (maxn <= CH_NMAX) {
+        k_leaf_chol2<4><<<nitems, CH_THREADS, chol2_smem(4, maxn), st>>>(d, status);
     } else {
         k_leaf_chol<<<nitems, 512, 0, st>>>(d, status);   // no Dinv: k_leaf_dinv is launched separately
     }
@@ -443,8 +696,12 @@ void launch_leaf_trsm(const TrsmItem* d, const int2* d_ctas, int nctas, unsigned
 void leaf_init_attributes() {
     SPG_CUDA(cudaFuncSetAttribute(k_leaf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(double) * TR_NMAX * TR_TC)));
-    SPG_CUDA(cudaFuncSetAttribute(k_leaf_chol2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * (CH_NMAX + 1) * (CH_NB + CH_KC))));
+    SPG_CUDA(cudaFuncSetAttribute(k_leaf_chol2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)chol2_smem(16, 256)));
+    SPG_CUDA(cudaFuncSetAttribute(k_leaf_chol3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)chol3_smem(C3_NMAX)));
+    SPG_CUDA(cudaFuncSetAttribute(k_leaf_chol2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)chol2_smem(4, CH_NMAX)));
     SPG_CUDA(cudaFuncSetAttribute(k_leaf_dinv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(double) * 16 * 32 * 33)));
 }

@@ -469,26 +469,33 @@ void trunc_init_attributes() {
 // SPG_CORE_JACOBI=1 selects the unpreconditioned full-size Jacobi core (A/B checks)
 static const bool g_core_jacobi = std::getenv("SPG_CORE_JACOBI") != nullptr;
 
+cudaEvent_t* g_trunc_events = nullptr;   // micro-benchmarks: events around tsqr | core | apply
+void set_trunc_events(cudaEvent_t* ev) { g_trunc_events = ev; }
+
 void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* status, cudaStream_t st) {
     if (b.ntasks == 0) return;
+    if (g_trunc_events) SPG_CUDA(cudaEventRecord(g_trunc_events[0], st));
     k_tsqr<<<b.n_items0, TS_THREADS, trunc_smem_tsqr(), st>>>(b.d_tasks, b.d_items0, ws, status, 0);
     SPG_LAUNCH_CHECK();
     if (b.n_itemsm) {
         k_tsqr<<<b.n_itemsm, TS_THREADS, trunc_smem_tsqr(), st>>>(b.d_tasks, b.d_itemsm, ws, status, 1);
         SPG_LAUNCH_CHECK();
     }
+    if (g_trunc_events) SPG_CUDA(cudaEventRecord(g_trunc_events[1], st));
     if (g_core_jacobi) {
         k_core<<<b.ntasks, TS_THREADS, trunc_smem_core(), st>>>(b.d_tasks, ws, eps, status);
         SPG_LAUNCH_CHECK();
     } else {
         launch_core2(b.d_tasks, b.ntasks, ws, eps, status, st);
     }
+    if (g_trunc_events) SPG_CUDA(cudaEventRecord(g_trunc_events[2], st));
     if (b.n_itemsm) {
         k_apply<<<b.n_itemsm, TS_THREADS, trunc_smem_apply(), st>>>(b.d_tasks, b.d_itemsm, ws, 1);
         SPG_LAUNCH_CHECK();
     }
     k_apply<<<b.n_items0, TS_THREADS, trunc_smem_apply(), st>>>(b.d_tasks, b.d_items0, ws, 0);
     SPG_LAUNCH_CHECK();
+    if (g_trunc_events) SPG_CUDA(cudaEventRecord(g_trunc_events[3], st));
 }
 
 }  // namespace spg

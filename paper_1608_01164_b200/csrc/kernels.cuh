@@ -16,6 +16,8 @@ void trunc_init_attributes();
 void core2_init_attributes();
 void launch_core2(const TTask* tasks, int ntasks, double* ws, double eps, unsigned* status, cudaStream_t st);
 void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* status, cudaStream_t st);
+void set_trunc_events(cudaEvent_t* ev);   // micro-benchmarks (4 events: tsqr | core | apply)
+void set_core_trace(long long* p);        // micro-benchmarks (clock64 per core phase, task 0)
 
 // ------------------------------------------------------------ batched DMMA GEMM
 // C = alpha * op(A) op(B) + beta * C, column-major.  Dimensions are constants
@@ -90,6 +92,7 @@ struct CholItem {
     double* W;
     int n, ldm, ldw;
     double* D;         // optional: inverses of W's 32x32 diagonal blocks (for trsm_tile_dinv)
+    long long* trace;  // optional (micro-benchmarks): clock64 per panel phase, 8 per panel
 };
 // inverses of the 32x32 diagonal blocks of upper-triangular leaves (W or R)
 struct DinvItem {
@@ -100,6 +103,9 @@ struct DinvItem {
 void launch_leaf_dinv(const DinvItem* d, int nitems, unsigned* status, cudaStream_t st);
 void launch_leaf_cholesky(const CholItem* d, int nitems, unsigned* status, cudaStream_t st, int maxn);
 void leaf_init_attributes();
+// micro-benchmarks of single kernels (k_micro.cu): which 0 = leaf Cholesky; returns
+// us per launch in out[0] and, for the Cholesky, mean cycles per panel phase in out[1..6]
+int micro_kernel(int which, int n, int reps, double* out, int nout);
 void hsolve_init_attributes();
 int hsolve_tile_cols();
 
