@@ -80,25 +80,28 @@ struct TTask {
 
 // Workspace layout of one task, per side (offsets in doubles, relative to the side base):
 //   per segment s: refl[s]  : nsub*SB*KIN_MAX  reflector tails, column-major (SB rows)
-//                  tau[s]   : nsub*KIN_MAX
+//                  tau[s]   : nsub*TS_TAUT  (per sub-block: KIN_MAX taus, then the 8x8
+//                             compact-WY T factor of each 8-column panel)
 //                  R[s]     : KIN_MAX*KIN_MAX  (column-major, ld KIN_MAX)
 //   merge (nseg > 1): refl   : nsubm*SB*KIN_MAX over the stacked R rows (nseg*k rows)
-//                     tau    : nsubm*KIN_MAX
+//                     tau    : nsubm*TS_TAUT
 //                     R      : KIN_MAX*KIN_MAX
 //                     Zst    : nseg*KIN_MAX*KCAP stacked coefficient blocks
 //   Z (core output, KIN_MAX x KCAP)
 // plus a task header of 8 ints at ws (k_in, r, flags) stored as doubles.
+constexpr int TS_NB = 8;                                          // panel width of the blocked TSQR
+constexpr int TS_TAUT = KIN_MAX + ((KIN_MAX + TS_NB - 1) / TS_NB) * TS_NB * TS_NB;   // taus + panel T's
 __host__ __device__ inline long long ts_nsub(int rows) { return (rows + SB - 1) / SB; }
 __host__ __device__ inline long long ts_seg_doubles(int seglen) {
     const long long ns = ts_nsub(seglen);
-    return ns * SB * KIN_MAX + ns * KIN_MAX + (long long)KIN_MAX * KIN_MAX;
+    return ns * SB * KIN_MAX + ns * TS_TAUT + (long long)KIN_MAX * KIN_MAX;
 }
 __host__ __device__ inline long long ts_side_doubles(int rows, int seglen, int nseg) {
     long long tot = (long long)nseg * ts_seg_doubles(seglen);
     if (nseg > 1) {
         const int mrows = nseg * KIN_MAX;
         const long long ns = ts_nsub(mrows);
-        tot += ns * SB * KIN_MAX + ns * KIN_MAX + (long long)KIN_MAX * KIN_MAX + (long long)nseg * KIN_MAX * KCAP;
+        tot += ns * SB * KIN_MAX + ns * TS_TAUT + (long long)KIN_MAX * KIN_MAX + (long long)nseg * KIN_MAX * KCAP;
     }
     tot += (long long)KIN_MAX * KCAP;  // Z
     (void)rows;

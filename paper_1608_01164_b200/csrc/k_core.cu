@@ -46,9 +46,9 @@ __device__ __forceinline__ const double* core_final_R(const TTask& t, double* ws
     const double* base = ws + t.ws + TS_HEADER + t.wsz[side];
     if (t.nseg[side] > 1) {
         const long long nsubm = ts_nsub(t.nseg[side] * KIN_MAX);
-        return base + (long long)t.nseg[side] * ts_seg_doubles(t.seg[side]) + nsubm * (SB * KIN_MAX + KIN_MAX);
+        return base + (long long)t.nseg[side] * ts_seg_doubles(t.seg[side]) + nsubm * (SB * KIN_MAX + TS_TAUT);
     }
-    return base + ts_nsub(t.seg[side]) * (SB * KIN_MAX + KIN_MAX);
+    return base + ts_nsub(t.seg[side]) * (SB * KIN_MAX + TS_TAUT);
 }
 
 __device__ __forceinline__ double* core_z(const TTask& t, double* ws, int side) {

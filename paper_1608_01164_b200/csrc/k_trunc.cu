@@ -64,66 +64,151 @@ __device__ __forceinline__ double* z_area(const TTask& t, double* ws, int side) 
 // ------------------------------------------------------------------ TSQR
 // Streaming Householder QR of the rows [r0, r0+nrows) of an implicit matrix with
 // k columns, starting from R = 0:  [0_k; A] = Q [R; 0].  Each 128-row sub-block
-// is folded into R by k reflectors acting on (R row j, block rows); reflector
-// tails and taus are stored for the later Q application.
+// is folded into R by k reflectors y_j = [e_j; v_j] acting on (R row j, block
+// rows), blocked by TS_NB = 8 columns (compact WY, Q_panel = I - Y T Y^T):
+//   * warp 0 factors the panel with the panel columns in registers (no CTA
+//     barrier inside the panel) and builds T column by column from the Gram
+//     entries v_a . v_j, reduced together with the panel updates;
+//   * every warp then applies Q_panel^T to the columns it owns (c = warp mod 16):
+//     w = Y^T a, w = T^T w, a -= Y w -- two CTA barriers per 8 columns.
+// Reflector tails, taus and the panel T's are stored for the Q application.
 //
 // Loader: fills Bk (SB x k, col-major ld SB) with rows [row0, row0+SB) (zero padded).
 template <class Loader>
-__device__ void stream_qr(int k, int nrows, double* refl, double* tau_out, double* Rout,
-                          double* sR, double* sB, double* sTau, const Loader& load) {
+__device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, double* Rout,
+                          double* sR, double* sB, double* sTT, const Loader& load) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = blockDim.x >> 5;
     for (int i = tid; i < KIN_MAX * KIN_MAX; i += blockDim.x) sR[i] = 0.0;
     const int nsub = (nrows + SB - 1) / SB;
+    const int npan = (k + TS_NB - 1) / TS_NB;
     for (int b = 0; b < nsub; ++b) {
         __syncthreads();
         load(b * SB, sB);
+        for (int i = tid; i < TS_TAUT; i += blockDim.x) sTT[i] = 0.0;
         __syncthreads();
-        for (int j = 0; j < k; ++j) {
+        for (int pn = 0; pn < npan; ++pn) {
+            const int j0 = pn * TS_NB, nb = min(TS_NB, k - j0);
+            double* Tp = sTT + KIN_MAX + pn * TS_NB * TS_NB;   // T (column-major 8 x 8)
             if (warp == 0) {
-                double* x = sB + (long long)j * SB;
-                double s2 = 0.0;
+                double x[TS_NB][SB / 32];
 #pragma unroll
-                for (int t = 0; t < SB / 32; ++t) { const double v = x[lane + 32 * t]; s2 += v * v; }
-                s2 = warp_sum(s2);
-                const double alpha = sR[j + j * KIN_MAX];
-                double tau = 0.0, scal = 0.0;
-                if (s2 > 0.0) {
-                    const double nrm = sqrt(alpha * alpha + s2);
-                    const double beta = alpha > 0.0 ? -nrm : nrm;
-                    tau = (beta - alpha) / beta;
-                    scal = 1.0 / (alpha - beta);
-                    if (lane == 0) sR[j + j * KIN_MAX] = beta;
+                for (int a = 0; a < TS_NB; ++a)
+#pragma unroll
+                    for (int t = 0; t < SB / 32; ++t) x[a][t] = a < nb ? sB[(lane + 32 * t) + (j0 + a) * SB] : 0.0;
+#pragma unroll
+                for (int jj = 0; jj < TS_NB; ++jj) {
+                    if (jj >= nb) break;
+                    const int j = j0 + jj;
+                    double s2 = 0.0;
+#pragma unroll
+                    for (int t = 0; t < SB / 32; ++t) s2 += x[jj][t] * x[jj][t];
+                    s2 = warp_sum(s2);
+                    const double alpha = sR[j + j * KIN_MAX];
+                    double tau = 0.0, scal = 0.0;
+                    if (s2 > 0.0) {
+                        const double nrm = sqrt(alpha * alpha + s2);
+                        const double beta = alpha > 0.0 ? -nrm : nrm;
+                        tau = (beta - alpha) / beta;
+                        scal = 1.0 / (alpha - beta);
+                        __syncwarp();
+                        if (lane == 0) sR[j + j * KIN_MAX] = beta;
+                    }
+#pragma unroll
+                    for (int t = 0; t < SB / 32; ++t) x[jj][t] *= scal;   // scal = 0 -> v = 0
+                    // d[c] = v_jj . x_c (c > jj, panel update) and g[a] = v_a . v_jj (a < jj, T column)
+                    double d[TS_NB];
+#pragma unroll
+                    for (int c = 0; c < TS_NB; ++c) {
+                        double s = 0.0;
+                        if (c != jj)
+#pragma unroll
+                            for (int t = 0; t < SB / 32; ++t) s += x[jj][t] * x[c][t];
+                        d[c] = s;
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                        for (int c = 0; c < TS_NB; ++c) d[c] += __shfl_xor_sync(0xffffffffu, d[c], o);
+                    double rjc[TS_NB];
+#pragma unroll
+                    for (int c = 0; c < TS_NB; ++c) rjc[c] = (c > jj && c < nb) ? sR[j + (j0 + c) * KIN_MAX] : 0.0;
+                    __syncwarp();
+#pragma unroll
+                    for (int c = 0; c < TS_NB; ++c) {
+                        if (c <= jj || c >= nb) continue;
+                        const double w = tau * (d[c] + rjc[c]);
+#pragma unroll
+                        for (int t = 0; t < SB / 32; ++t) x[c][t] -= w * x[jj][t];
+                        if (lane == 0) sR[j + (j0 + c) * KIN_MAX] = rjc[c] - w;
+                    }
+                    // T(:, jj) = [-tau T(0:jj, 0:jj) g(0:jj); tau]; lane a < jj owns row a
+                    double z = 0.0;
+#pragma unroll
+                    for (int bq = 0; bq < TS_NB; ++bq)
+                        if (bq < jj && bq >= lane) z += Tp[lane + bq * TS_NB] * d[bq];
+                    if (lane < jj) Tp[lane + jj * TS_NB] = -tau * z;
+                    if (lane == jj) Tp[jj + jj * TS_NB] = tau;
+                    if (lane == 0) sTT[j] = tau;
+                    __syncwarp();
                 }
 #pragma unroll
-                for (int t = 0; t < SB / 32; ++t) x[lane + 32 * t] *= scal;   // scal = 0 -> v = 0
-                if (lane == 0) sTau[j] = tau;
+                for (int a = 0; a < TS_NB; ++a)
+                    if (a < nb)
+#pragma unroll
+                        for (int t = 0; t < SB / 32; ++t) sB[(lane + 32 * t) + (j0 + a) * SB] = x[a][t];
             }
             __syncthreads();
-            const double tau = sTau[j];
-            if (tau != 0.0) {
-                const double* v = sB + (long long)j * SB;
-                double vr[SB / 32];
+            // Q_panel^T on the remaining columns: w = Y^T a, w = T^T w, a -= Y w
+            for (int c = j0 + nb + warp; c < k; c += nwarps) {
+                double av[SB / 32], w[TS_NB];
 #pragma unroll
-                for (int t = 0; t < SB / 32; ++t) vr[t] = v[lane + 32 * t];
-                for (int c = j + 1 + warp; c < k; c += nwarps) {
-                    double* a = sB + (long long)c * SB;
-                    double d = 0.0;
+                for (int t = 0; t < SB / 32; ++t) av[t] = sB[(lane + 32 * t) + c * SB];
 #pragma unroll
-                    for (int t = 0; t < SB / 32; ++t) d += vr[t] * a[lane + 32 * t];
-                    d = warp_sum(d) + sR[j + c * KIN_MAX];
-                    const double w = tau * d;
+                for (int a = 0; a < TS_NB; ++a) {
+                    double s = 0.0;
+                    if (a < nb)
 #pragma unroll
-                    for (int t = 0; t < SB / 32; ++t) a[lane + 32 * t] -= w * vr[t];
-                    if (lane == 0) sR[j + c * KIN_MAX] -= w;
+                        for (int t = 0; t < SB / 32; ++t) s += sB[(lane + 32 * t) + (j0 + a) * SB] * av[t];
+                    w[a] = s;
                 }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int a = 0; a < TS_NB; ++a) w[a] += __shfl_xor_sync(0xffffffffu, w[a], o);
+                double ra[TS_NB];
+#pragma unroll
+                for (int a = 0; a < TS_NB; ++a) {
+                    ra[a] = a < nb ? sR[(j0 + a) + c * KIN_MAX] : 0.0;
+                    w[a] += ra[a];
+                }
+                double wt[TS_NB];
+#pragma unroll
+                for (int i = 0; i < TS_NB; ++i) {   // (T^T w)_i = sum_{a <= i} T(a, i) w_a
+                    double s = 0.0;
+#pragma unroll
+                    for (int a = 0; a <= i; ++a) s += Tp[a + i * TS_NB] * w[a];
+                    wt[i] = s;
+                }
+#pragma unroll
+                for (int t = 0; t < SB / 32; ++t) {
+                    double s = av[t];
+#pragma unroll
+                    for (int a = 0; a < TS_NB; ++a)
+                        if (a < nb) s -= sB[(lane + 32 * t) + (j0 + a) * SB] * wt[a];
+                    sB[(lane + 32 * t) + c * SB] = s;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int a = 0; a < TS_NB; ++a)
+                    if (lane == a && a < nb) sR[(j0 + a) + c * KIN_MAX] = ra[a] - wt[a];
             }
             __syncthreads();
         }
-        // store reflector tails (SB x k) and taus for this sub-block
+        // store reflector tails (SB x k), taus and the panel T's of this sub-block
         double* dst = refl + (long long)b * SB * KIN_MAX;
         for (int i = tid; i < SB * k; i += blockDim.x) dst[i] = sB[i];
-        for (int i = tid; i < k; i += blockDim.x) tau_out[(long long)b * KIN_MAX + i] = sTau[i];
+        for (int i = tid; i < TS_TAUT; i += blockDim.x) taut_out[(long long)b * TS_TAUT + i] = sTT[i];
     }
     __syncthreads();
     for (int i = tid; i < KIN_MAX * KIN_MAX; i += blockDim.x) {
@@ -138,7 +223,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
     extern __shared__ double smem[];
     double* sR = smem;                        // KIN_MAX^2
     double* sB = sR + KIN_MAX * KIN_MAX;      // SB * KIN_MAX
-    double* sTau = sB + SB * KIN_MAX;         // KIN_MAX
+    double* sTau = sB + SB * KIN_MAX;         // TS_TAUT: taus + panel T's
     const int3 it = items[blockIdx.x];
     const TTask& t = tasks[it.x];
     const int side = it.y;
@@ -161,16 +246,35 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
         if (nr <= 0) return;
         double* base = seg_area(t, ws, side, s);
         const long long nsub = ts_nsub(t.seg[side]);
+        // column pointers and scales resolved once (the group walk reads device ranks)
+        __shared__ const double* sCol[KIN_MAX];
+        __shared__ double sScl[KIN_MAX];
+        if (threadIdx.x < k) {
+            double sc; int ld;
+            sCol[threadIdx.x] = col_ptr(t, side, threadIdx.x, sc, ld) + r0;
+            sScl[threadIdx.x] = sc;
+        }
+        __syncthreads();
         auto load = [&](int sub0, double* B) {
-            for (int c = threadIdx.x >> 7; c < k; c += blockDim.x >> 7) {
-                double sc; int ld;
-                const double* cp = col_ptr(t, side, c, sc, ld);
-                const int i = threadIdx.x & 127;
-                const int gi = sub0 + i;
-                B[(long long)c * SB + i] = (gi < nr) ? sc * cp[r0 + gi] : 0.0;
+            const int i = threadIdx.x & 127;
+            const int gi = sub0 + i;
+            const bool in = gi < nr;
+            constexpr int CPT = TS_THREADS / SB;   // column groups per pass
+            for (int c0 = threadIdx.x >> 7; c0 < k; c0 += 4 * CPT) {   // 4 independent loads in flight
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = c0 + u * CPT;
+                    v[u] = (in && c < k) ? sCol[c][gi] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = c0 + u * CPT;
+                    if (c < k) B[(long long)c * SB + i] = sScl[c] * v[u];
+                }
             }
         };
-        stream_qr(k, nr, base, base + nsub * SB * KIN_MAX, base + nsub * SB * KIN_MAX + nsub * KIN_MAX, sR, sB,
+        stream_qr(k, nr, base, base + nsub * SB * KIN_MAX, base + nsub * SB * KIN_MAX + nsub * TS_TAUT, sR, sB,
                   sTau, load);
     } else {
         const int ns = t.nseg[side];
@@ -186,13 +290,13 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
                 double v = 0.0;
                 if (gi < mrows) {
                     const int s = gi / k, lr = gi % k;
-                    const double* Rs = seg_area(t, ws, side, s) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + KIN_MAX);
+                    const double* Rs = seg_area(t, ws, side, s) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + TS_TAUT);
                     v = Rs[lr + (long long)c * KIN_MAX];
                 }
                 B[(long long)c * SB + i] = v;
             }
         };
-        stream_qr(k, mrows, mb, mb + nsubm * SB * KIN_MAX, mb + nsubm * SB * KIN_MAX + nsubm * KIN_MAX, sR, sB,
+        stream_qr(k, mrows, mb, mb + nsubm * SB * KIN_MAX, mb + nsubm * SB * KIN_MAX + nsubm * TS_TAUT, sR, sB,
                   sTau, load);
     }
 }
@@ -201,9 +305,9 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
 __device__ __forceinline__ const double* final_R(const TTask& t, double* ws, int side) {
     if (t.nseg[side] > 1) {
         const long long nsubm = ts_nsub(t.nseg[side] * KIN_MAX);
-        return merge_area(t, ws, side) + nsubm * (SB * KIN_MAX + KIN_MAX);
+        return merge_area(t, ws, side) + nsubm * (SB * KIN_MAX + TS_TAUT);
     }
-    return seg_area(t, ws, side, 0) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + KIN_MAX);
+    return seg_area(t, ws, side, 0) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + TS_TAUT);
 }
 
 // one CTA per task: C = R_u R_v^T, parallel one-sided Jacobi, sort, threshold
@@ -353,46 +457,78 @@ __global__ void __launch_bounds__(TS_THREADS) k_core(const TTask* __restrict__ t
 }
 
 // ------------------------------------------------------------------ Q application
-// Applies Q (stored as per-sub-block reflectors, see stream_qr) to [Z; 0]:
-// the R-part starts as Z (k x r), every sub-block's output rows start at 0;
-// sub-blocks are visited in reverse, reflectors within a block in reverse.
+// Applies Q (per sub-block compact-WY panels, see stream_qr) to [Z; 0]: the R-part
+// starts as Z (k x r), every sub-block's output rows start at 0; sub-blocks are
+// visited in reverse, panels within a block in reverse (x -= Y (T (Y^T x))).
+// Each warp owns whole output columns, so a sub-block needs no barrier between
+// its panels; the finished rows go straight from registers to the writer.
 template <class Writer>
-__device__ void stream_apply(int k, int r, int nrows, const double* refl, const double* taus, const double* Z0,
-                             int ldz, double* sZ, double* sO, double* sV, const Writer& write) {
+__device__ void stream_apply(int k, int r, int nrows, const double* refl, const double* taut, const double* Z0,
+                             int ldz, double* sZ, double* sV, double* sTT, const Writer& write) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     for (int idx = tid; idx < k * r; idx += blockDim.x) {
         const int i = idx % k, c = idx / k;
         sZ[i + c * KIN_MAX] = Z0[i + (long long)c * ldz];
     }
     const int nsub = (nrows + SB - 1) / SB;
+    const int npan = (k + TS_NB - 1) / TS_NB;
     for (int b = nsub - 1; b >= 0; --b) {
         __syncthreads();
         const double* vb = refl + (long long)b * SB * KIN_MAX;
         for (int i = tid; i < SB * k; i += blockDim.x) sV[i] = vb[i];
-        for (int i = tid; i < SB * r; i += blockDim.x) sO[i] = 0.0;
+        for (int i = tid; i < TS_TAUT; i += blockDim.x) sTT[i] = taut[(long long)b * TS_TAUT + i];
         __syncthreads();
-        for (int j = k - 1; j >= 0; --j) {
-            const double tau = taus[(long long)b * KIN_MAX + j];
-            if (tau != 0.0) {
-                const double* v = sV + (long long)j * SB;
-                double vr[SB / 32];
+        for (int c = warp; c < r; c += nwarps) {
+            double o[SB / 32];
 #pragma unroll
-                for (int t = 0; t < SB / 32; ++t) vr[t] = v[lane + 32 * t];
-                for (int c = warp; c < r; c += nwarps) {
-                    double* o = sO + (long long)c * SB;
-                    double d = 0.0;
+            for (int t = 0; t < SB / 32; ++t) o[t] = 0.0;
+            double* zc = sZ + c * KIN_MAX;
+            for (int pn = npan - 1; pn >= 0; --pn) {
+                const int j0 = pn * TS_NB, nb = min(TS_NB, k - j0);
+                const double* Tp = sTT + KIN_MAX + pn * TS_NB * TS_NB;
+                double w[TS_NB];
 #pragma unroll
-                    for (int t = 0; t < SB / 32; ++t) d += vr[t] * o[lane + 32 * t];
-                    d = warp_sum(d) + sZ[j + c * KIN_MAX];
-                    const double w = tau * d;
+                for (int a = 0; a < TS_NB; ++a) {
+                    double s = 0.0;
+                    if (a < nb)
 #pragma unroll
-                    for (int t = 0; t < SB / 32; ++t) o[lane + 32 * t] -= w * vr[t];
-                    if (lane == 0) sZ[j + c * KIN_MAX] -= w;
+                        for (int t = 0; t < SB / 32; ++t) s += sV[(lane + 32 * t) + (j0 + a) * SB] * o[t];
+                    w[a] = s;
                 }
+#pragma unroll
+                for (int of = 16; of > 0; of >>= 1)
+#pragma unroll
+                    for (int a = 0; a < TS_NB; ++a) w[a] += __shfl_xor_sync(0xffffffffu, w[a], of);
+                double za[TS_NB];
+#pragma unroll
+                for (int a = 0; a < TS_NB; ++a) {
+                    za[a] = a < nb ? zc[j0 + a] : 0.0;
+                    w[a] += za[a];
+                }
+                double wt[TS_NB];
+#pragma unroll
+                for (int a = 0; a < TS_NB; ++a) {   // (T w)_a = sum_{i >= a} T(a, i) w_i
+                    double s = 0.0;
+#pragma unroll
+                    for (int i = a; i < TS_NB; ++i) s += Tp[a + i * TS_NB] * w[i];
+                    wt[a] = s;
+                }
+#pragma unroll
+                for (int t = 0; t < SB / 32; ++t) {
+                    double s = o[t];
+#pragma unroll
+                    for (int a = 0; a < TS_NB; ++a)
+                        if (a < nb) s -= sV[(lane + 32 * t) + (j0 + a) * SB] * wt[a];
+                    o[t] = s;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int a = 0; a < TS_NB; ++a)
+                    if (lane == a && a < nb) zc[j0 + a] = za[a] - wt[a];
+                __syncwarp();
             }
-            __syncthreads();
+            write(b * SB, c, o);
         }
-        write(b * SB, sO);
     }
 }
 
@@ -400,8 +536,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
                                                      double* __restrict__ ws, int merge) {
     extern __shared__ double smem[];
     double* sZ = smem;                         // KIN_MAX x KCAP
-    double* sO = sZ + KIN_MAX * KCAP;          // SB x KCAP
-    double* sV = sO + SB * KCAP;               // SB x KIN_MAX
+    double* sV = sZ + KIN_MAX * KCAP;          // SB x KIN_MAX
+    double* sTT = sV + SB * KIN_MAX;           // TS_TAUT
     const int3 it = items[blockIdx.x];
     const TTask& t = tasks[it.x];
     const int side = it.y;
@@ -409,21 +545,23 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
     const int k = (int)hdr[0], r = (int)hdr[1];
     if (k == 0 || r == 0) return;
     const int rows = side == 0 ? t.p : t.s;
+    const int lane = threadIdx.x & 31;
     if (merge) {
         const int ns = t.nseg[side];
         if (ns <= 1) return;
         double* mb = merge_area(t, ws, side);
         const long long nsubm = ts_nsub(ns * KIN_MAX);
-        double* Zst = mb + nsubm * (SB * KIN_MAX + KIN_MAX) + (long long)KIN_MAX * KIN_MAX;
+        double* Zst = mb + nsubm * (SB * KIN_MAX + TS_TAUT) + (long long)KIN_MAX * KIN_MAX;
         const int mrows = ns * k;
         const int ldst = ns * KIN_MAX;
-        auto write = [&](int r0, const double* O) {
-            for (int idx = threadIdx.x; idx < SB * r; idx += blockDim.x) {
-                const int i = idx % SB, c = idx / SB;
-                if (r0 + i < mrows) Zst[r0 + i + (long long)c * ldst] = O[i + (long long)c * SB];
+        auto write = [&](int r0, int c, const double* o) {
+#pragma unroll
+            for (int tt = 0; tt < SB / 32; ++tt) {
+                const int i = r0 + lane + 32 * tt;
+                if (i < mrows) Zst[i + (long long)c * ldst] = o[tt];
             }
         };
-        stream_apply(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, sZ, sO, sV, write);
+        stream_apply(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, sZ, sV, sTT, write);
     } else {
         const int s = it.z;
         const int r0 = s * t.seg[side];
@@ -435,7 +573,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
         int ldz;
         if (t.nseg[side] > 1) {
             const long long nsubm = ts_nsub(t.nseg[side] * KIN_MAX);
-            const double* Zst = merge_area(t, ws, side) + nsubm * (SB * KIN_MAX + KIN_MAX) + (long long)KIN_MAX * KIN_MAX;
+            const double* Zst = merge_area(t, ws, side) + nsubm * (SB * KIN_MAX + TS_TAUT) + (long long)KIN_MAX * KIN_MAX;
             Z0 = Zst + (long long)s * k;
             ldz = t.nseg[side] * KIN_MAX;
         } else {
@@ -444,20 +582,21 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
         }
         double* out = side == 0 ? t.ou : t.ov;
         const int ldo = side == 0 ? t.ldou : t.ldov;
-        auto write = [&](int sub0, const double* O) {
-            for (int idx = threadIdx.x; idx < SB * r; idx += blockDim.x) {
-                const int i = idx % SB, c = idx / SB;
-                if (sub0 + i < nr) out[r0 + sub0 + i + (long long)c * ldo] = O[i + (long long)c * SB];
+        auto write = [&](int sub0, int c, const double* o) {
+#pragma unroll
+            for (int tt = 0; tt < SB / 32; ++tt) {
+                const int i = sub0 + lane + 32 * tt;
+                if (i < nr) out[r0 + i + (long long)c * ldo] = o[tt];
             }
         };
-        stream_apply(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, sZ, sO, sV, write);
+        stream_apply(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, sZ, sV, sTT, write);
     }
 }
 
 // ------------------------------------------------------------------ host side
-size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + SB * KIN_MAX + KIN_MAX); }
+size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + SB * KIN_MAX + TS_TAUT); }
 size_t trunc_smem_core() { return sizeof(double) * (2 * KIN_MAX * KIN_MAX); }
-size_t trunc_smem_apply() { return sizeof(double) * (KIN_MAX * KCAP + SB * KCAP + SB * KIN_MAX); }
+size_t trunc_smem_apply() { return sizeof(double) * (KIN_MAX * KCAP + SB * KIN_MAX + TS_TAUT); }
 
 void trunc_init_attributes() {
     SPG_CUDA(cudaFuncSetAttribute(k_tsqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_tsqr()));
