@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -98,7 +99,8 @@ ABI_SYMBOLS = (
     "spg_result_apply", "spg_result_free", "spg_last_error", "spg_tree", "spg_qdwh_params", "spg_l_update",
     "spg_make_dimer_chain", "spg_make_random_banded", "spg_kcap", "spg_ctx_create", "spg_ctx_free",
     "spg_ctx_upload", "spg_ctx_flat_size", "spg_ctx_download", "spg_ctx_op", "spg_ctx_from_banded",
-    "spg_truncate", "spg_set_profile", "spg_measure_dmma_tflops", "spg_micro_kernel",
+    "spg_truncate", "spg_set_profile", "spg_measure_dmma_tflops", "spg_micro_kernel", "spg_host_alloc",
+    "spg_host_free",
 )
 
 
@@ -139,6 +141,8 @@ def load_library(path: str | None = None):
         "spg_set_profile": ([C.c_int], None),
         "spg_measure_dmma_tflops": ([_dp], C.c_int),
         "spg_micro_kernel": ([C.c_int, C.c_int, C.c_int, _dp, C.c_int], C.c_int),
+        "spg_host_alloc": ([C.c_longlong, C.POINTER(vp)], C.c_int),
+        "spg_host_free": ([vp], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -258,6 +262,39 @@ def make_tree(n, n_min):
     return PartitionTree(n, n_min)
 
 
+class _HostSlot:
+    """A page-locked host buffer of the export pool (reused across results)."""
+
+    def __init__(self, n):
+        L = load_library()
+        self.ptr = C.c_void_p()
+        self.n = max(int(n), 1)
+        _raise(L.spg_host_alloc(8 * self.n, C.byref(self.ptr)))
+        self.busy = True
+
+    def release(self):
+        self.busy = False
+
+    def __del__(self):
+        try:
+            load_library().spg_host_free(self.ptr)
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
+
+
+_HOST_POOL: list = []
+
+
+def _host_buffer(n: int) -> _HostSlot:
+    for slot in _HOST_POOL:
+        if not slot.busy and slot.n >= n:
+            slot.busy = True
+            return slot
+    slot = _HostSlot(n)
+    _HOST_POOL.append(slot)
+    return slot
+
+
 class HodlrMatrix:
     """Host copy of a device HODLR matrix (hodlr.hpp:20-48).  Nodes in preorder;
     ``dense[id]`` for leaves, ``upper[id] = (U, V)`` / ``lower[id]`` otherwise."""
@@ -271,9 +308,9 @@ class HodlrMatrix:
         H = cls(tree)
         off = 0
 
-        def take(r, c):
+        def take(r, c):   # views into the flat buffer (no copies)
             nonlocal off
-            m = np.array(data[off:off + r * c]).reshape(r, c)
+            m = data[off:off + r * c].reshape(r, c)
             off += r * c
             return m
 
@@ -390,7 +427,12 @@ class ProjectorResult:
         nd = C.c_longlong(0)
         _raise(L.spg_result_flat_size(self._handle, which, C.byref(nd)))
         ranks = np.zeros(2 * len(self._tree), dtype=np.int32)
-        data = np.zeros(nd.value)
+        slot = _host_buffer(nd.value)
+        # a fresh ctypes view per lease: every block array of the result keeps it alive,
+        # and the pool gets the buffer back only when the last of them is gone
+        lease = (C.c_double * max(nd.value, 1)).from_address(slot.ptr.value)
+        weakref.finalize(lease, slot.release)
+        data = np.ctypeslib.as_array(lease)[:nd.value]
         _raise(L.spg_result_export(self._handle, which, _i(ranks), _d(data)))
         return HodlrMatrix.from_flat(self._tree, ranks, data)
 

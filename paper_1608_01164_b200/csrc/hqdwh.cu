@@ -202,12 +202,15 @@ void export_flat(Engine& E, const DHodlr& H, int* ranks, double* data, long long
     SPG_CUDA(cudaStreamSynchronize(st));
     if (nd) *nd = total;
     if (data) {
-        double* buf;
-        SPG_CUDA(cudaMalloc(&buf, sizeof(double) * std::max<long long>(total, 1)));
+        // staging in the engine workspace when it is large enough (free once the projector is done)
+        double* buf = nullptr;
+        const bool own = (size_t)std::max<long long>(total, 1) > E.ws().capacity();
+        if (own) SPG_CUDA(cudaMalloc(&buf, sizeof(double) * std::max<long long>(total, 1)));
+        else buf = E.ws().base();
         k_flat_pack<<<nn, 256, 0, st>>>(E.dtree(), H.view(), doff, buf);
         SPG_CUDA(cudaMemcpyAsync(data, buf, sizeof(double) * total, cudaMemcpyDeviceToHost, st));
         SPG_CUDA(cudaStreamSynchronize(st));
-        cudaFree(buf);
+        if (own) cudaFree(buf);
     }
     if (ranks) {
         SPG_CUDA(cudaMemcpyAsync(ranks, H.rank, sizeof(int) * 2 * nn, cudaMemcpyDeviceToHost, st));
@@ -608,6 +611,18 @@ int spg_measure_dmma_tflops(double* out) {
     });
 }
 int spg_kcap(void) { return KCAP; }
+
+int spg_host_alloc(long long bytes, void** out) {
+    *out = nullptr;
+    return guarded([&]() {
+        ensure_device();
+        SPG_CUDA(cudaHostAlloc(out, (size_t)std::max<long long>(bytes, 8), cudaHostAllocDefault));
+    });
+}
+
+void spg_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
 
 int spg_micro_kernel(int which, int n, int reps, double* out, int nout) {
     return guarded([&]() {
