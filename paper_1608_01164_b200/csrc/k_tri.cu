@@ -25,6 +25,25 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// reciprocal / square root from the MUFU seeds plus Newton steps (no slow-path
+// calls on the dependent chain; results within an ulp of the IEEE operations)
+__device__ __forceinline__ double rcp_t(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double sqrt_t(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
+    y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
+    const double r = x * y;
+    return fma(0.5 * y, fma(-r, r, x), r);
+}
+
 // NA input streams read in step order kk = 0, 1, ...: stream a at step kk is
 // p[a][(rev ? hi - kk : kk) + off[a]], 0 outside [0, len[a]).
 template <int NA>
@@ -182,7 +201,7 @@ __global__ void __launch_bounds__(32) k_est_l0_tri(int n, const double* __restri
             double p0 = a0, p1 = a1, p2 = 0.0, q0 = e, q1 = d1, q2 = e1;
             if (swp) { p0 = e; p1 = d1; p2 = e1; q0 = a0; q1 = a1; q2 = 0.0; }
             if (p0 == 0.0) singular = true;
-            const double inv = 1.0 / p0;
+            const double inv = p0 == 0.0 ? 0.0 : rcp_t(p0);
             const double mm = q0 * inv;
             if (mm != 0.0) { q1 -= mm * p1; q2 -= mm * p2; }
             if (lane == 0) {
@@ -246,11 +265,13 @@ __device__ __forceinline__ void givens_cs_t(double f, double g, double& c, doubl
     if (f == 0.0) { c = 0.0; s = 1.0; return; }
     const double af = fabs(f), ag = fabs(g);
     const double scale = af + ag;
-    const double fs = f / scale, gs = g / scale;
-    double r = scale * sqrt(fs * fs + gs * gs);
+    const double is = rcp_t(scale);
+    const double fs = f * is, gs = g * is;
+    double r = scale * sqrt_t(fs * fs + gs * gs);
     if (f < 0.0) r = -r;
-    c = f / r;
-    s = g / r;
+    const double ir = rcp_t(r);
+    c = f * ir;
+    s = g * ir;
 }
 
 // reduce_tridiag: per row t the rotations alpha_{t,t} (rowN_t against aux_t = 1),
