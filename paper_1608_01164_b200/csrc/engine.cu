@@ -136,6 +136,23 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     arena_ = std::make_unique<Arena>(size_t(512) << 20);
     if (!ws_doubles) ws_doubles = std::max<size_t>(size_t(64) << 20, (size_t)90 * n * KIN_MAX);
     ws_ = std::make_unique<Workspace>(ws_doubles);
+    // side streams of the deferred Cholesky cascades: one per tree depth (a block's
+    // updates stay ordered on its depth's stream) plus one for the leaf updates
+    const int nside = std::max(1, tree_.depth) + 1;
+    for (int i = 0; i < nside; ++i) {
+        cudaStream_t s;
+        SPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        sides_.push_back(s);
+        ws_side_.push_back(std::make_unique<Workspace>(
+            i + 1 == nside ? size_t(1) << 20 : std::max<size_t>((size_t)3 * n * KIN_MAX, size_t(8) << 20)));
+    }
+    events_.resize((size_t)tree_.nnodes() * (nside + 2) + 4 * nside + 4);
+    for (auto& e : events_) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int t = 0; t < std::max(1, tree_.depth); ++t) {
+        double* p;
+        SPG_CUDA(cudaMalloc(&p, sizeof(double) * (size_t)n * KCAP));
+        chol_panels_.push_back(p);
+    }
     // device tree
     std::vector<int> tb = tree_.begin, ts = tree_.size, tl = tree_.left, tr = tree_.right, tv = tree_.level,
                      to = tree_.leaf_ord;
@@ -164,15 +181,37 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     arena_->commit(st_);
 }
 
+// every launch of a plan goes through here: in side mode it is bound to the side
+// stream (deferred work that overlaps the critical path, see op_cholesky)
+void Engine::push(Plan& p, Launch l) {
+    if (side_sel_ >= 0) {
+        cudaStream_t side = sides_[side_sel_];
+        p.launches.push_back([l = std::move(l), side](cudaStream_t) { l(side); });
+    } else {
+        p.launches.push_back(std::move(l));
+    }
+}
+
 void Engine::push_timed(Plan& p, int cls, Launch l) {
-    if (!profile_) { p.launches.push_back(std::move(l)); return; }
+    if (!profile_) { push(p, std::move(l)); return; }
     cudaEvent_t a, b;
     SPG_CUDA(cudaEventCreate(&a));
     SPG_CUDA(cudaEventCreate(&b));
     prof_.push_back({cls, cur_op_, a, b});
-    p.launches.push_back([a](cudaStream_t s) { SPG_CUDA(cudaEventRecord(a, s)); });
-    p.launches.push_back(std::move(l));
-    p.launches.push_back([b](cudaStream_t s) { SPG_CUDA(cudaEventRecord(b, s)); });
+    push(p, [a](cudaStream_t s) { SPG_CUDA(cudaEventRecord(a, s)); });
+    push(p, std::move(l));
+    push(p, [b](cudaStream_t s) { SPG_CUDA(cudaEventRecord(b, s)); });
+}
+
+// cross-stream ordering: record event `e` on the stream of the current mode ...
+void Engine::record(Plan& p, int e) {
+    cudaEvent_t ev = events_[e];
+    push(p, [ev](cudaStream_t s) { SPG_CUDA(cudaEventRecord(ev, s)); });
+}
+// ... and make the stream of the current mode wait for it
+void Engine::wait(Plan& p, int e) {
+    cudaEvent_t ev = events_[e];
+    push(p, [ev](cudaStream_t s) { SPG_CUDA(cudaStreamWaitEvent(s, ev, 0)); });
 }
 
 void Engine::prof_sum(double* ms, long long* nb) const {
@@ -211,8 +250,12 @@ Engine::~Engine() {
     if (coef_) cudaFree(coef_);
     if (iranks_) cudaFree(iranks_);
     if (scalar_mem_) cudaFree(scalar_mem_);
+    for (double* p : chol_panels_) cudaFree(p);
+    for (auto& e : events_) cudaEventDestroy(e);
     arena_.reset();
     ws_.reset();
+    ws_side_.clear();
+    for (auto sd : sides_) cudaStreamDestroy(sd);
     if (st_) cudaStreamDestroy(st_);
 }
 
@@ -227,7 +270,8 @@ std::unique_ptr<DHodlr> Engine::new_hodlr() {
 // ---------------------------------------------------------------- truncation batch
 void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     if (tasks.empty()) return;
-    const long long mark = ws_->mark();
+    Workspace& wsp = side_sel_ >= 0 ? *ws_side_[side_sel_] : *ws_;   // each stream has its own stack
+    const long long mark = wsp.mark();
     std::vector<int3> it0, itm;
     for (size_t i = 0; i < tasks.size(); ++i) {
         TTask& t = tasks[i];
@@ -245,7 +289,7 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
         t.wsz[0] = 0;
         t.wsz[1] = ts_side_doubles(t.p, t.seg[0], t.nseg[0]);
         t.wcore = TS_HEADER + t.wsz[1] + ts_side_doubles(t.s, t.seg[1], t.nseg[1]);
-        t.ws = ws_->alloc(t.wcore + (long long)KIN_MAX * KIN_MAX);
+        t.ws = wsp.alloc(t.wcore + (long long)KIN_MAX * KIN_MAX);
         for (int side = 0; side < 2; ++side) {
             for (int s = 0; s < t.nseg[side]; ++s) it0.push_back(make_int3((int)i, side, s));
             if (t.nseg[side] > 1) itm.push_back(make_int3((int)i, side, -1));
@@ -258,11 +302,11 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     b.ntasks = (int)tasks.size();
     b.n_items0 = (int)it0.size();
     b.n_itemsm = (int)itm.size();
-    double* ws = ws_->base();
+    double* ws = wsp.base();
     const double eps = eps_;
     unsigned* status = sc_.status;
     push_timed(p, PC_TRUNC, [b, ws, eps, status](cudaStream_t st) { launch_truncate(b, ws, eps, status, st); });
-    ws_->release(mark);
+    wsp.release(mark);
 }
 
 // ---------------------------------------------------------------- GEMM batch
@@ -430,14 +474,14 @@ void Engine::copy(Plan& p, std::vector<CopyItem> items, int maxm, int maxk) {
     if (items.empty()) return;
     const CopyItem* d = arena_->push(items);
     const int ni = (int)items.size();
-    p.launches.push_back([d, ni, maxm, maxk](cudaStream_t st) { launch_copy_cols(d, ni, maxm, maxk, st); });
+    push(p, [d, ni, maxm, maxk](cudaStream_t st) { launch_copy_cols(d, ni, maxm, maxk, st); });
 }
 
 static void push_rankops(Plan& p, Arena& a, const std::vector<RankOp>& ops) {
     if (ops.empty()) return;
     const RankOp* d = a.push(ops);
     const int n = (int)ops.size();
-    p.launches.push_back([d, n](cudaStream_t st) {
+    p.launches.push_back([d, n](cudaStream_t st) {   // main stream only
         k_rank_op<<<(n + 127) / 128, 128, 0, st>>>(d, n);
         SPG_LAUNCH_CHECK();
     });
@@ -456,7 +500,7 @@ void Engine::op_axpby(Plan& p, double a, const double* ap, const DHodlr& A, doub
     }
     const LeafItem* d = arena_->push(li);
     const int ni = (int)li.size();
-    p.launches.push_back([=](cudaStream_t st) { launch_leaf_axpby(d, ni, maxn, a, ap, b, bp, st); });
+    push(p, [=](cudaStream_t st) { launch_leaf_axpby(d, ni, maxn, a, ap, b, bp, st); });
     std::vector<TTask> tasks;
     const int n = tree_.n;
     for (int x = 0; x < tree_.nnodes(); ++x) {
@@ -489,7 +533,7 @@ void Engine::op_symmetrize(Plan& p, DHodlr& H) {
     }
     const LeafItem* d = arena_->push(li);
     const int ni = (int)li.size();
-    p.launches.push_back([=](cudaStream_t st) { launch_leaf_symmetrize(d, ni, maxn, st); });
+    push(p, [=](cudaStream_t st) { launch_leaf_symmetrize(d, ni, maxn, st); });
     std::vector<TTask> tasks;
     std::vector<CopyItem> cp;
     const int n = tree_.n;
@@ -523,7 +567,7 @@ void Engine::op_scale_shift(Plan& p, DHodlr& H, double s, const double* sp, doub
     }
     const LeafItem* d = arena_->push(li);
     const int ni = (int)li.size();
-    p.launches.push_back([=](cudaStream_t st) { launch_leaf_scale_shift(d, ni, maxn, s, sp, mu, st); });
+    push(p, [=](cudaStream_t st) { launch_leaf_scale_shift(d, ni, maxn, s, sp, mu, st); });
     // scale the U factors (upper.U and lower.U) in place
     std::vector<LeafItem> fi;
     const int n = tree_.n;
@@ -539,7 +583,7 @@ void Engine::op_scale_shift(Plan& p, DHodlr& H, double s, const double* sp, doub
         const LeafItem* df = arena_->push(fi);
         const int nf = (int)fi.size();
         // columns beyond the rank are scaled too (harmless: never read)
-        p.launches.push_back([=](cudaStream_t st) { launch_leaf_axpby(df, nf, std::max(maxm, KCAP), s, sp, 0.0, nullptr, st); });
+        push(p, [=](cudaStream_t st) { launch_leaf_axpby(df, nf, std::max(maxm, KCAP), s, sp, 0.0, nullptr, st); });
     }
 }
 
@@ -550,7 +594,7 @@ void Engine::op_copy(Plan& p, const DHodlr& src, DHodlr& dst) {
     const int* sr = src.rank;
     int* dr = dst.rank;
     const size_t rb = sizeof(int) * 2 * tree_.nnodes();
-    p.launches.push_back([=](cudaStream_t st) {
+    push(p, [=](cudaStream_t st) {
         SPG_CUDA(cudaMemcpyAsync(dd, s, bytes, cudaMemcpyDeviceToDevice, st));
         SPG_CUDA(cudaMemcpyAsync(dr, sr, rb, cudaMemcpyDeviceToDevice, st));
     });
@@ -685,17 +729,102 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
 }
 
 // hodlr_cholesky (hodlr.hpp:540-574)
+//
+// The recursion is kept, but the Schur cascade of every node x (M22 -= V (U^T U) V^T
+// over the whole subtree r(x), hodlr.hpp:566-569) runs on a side stream: a block of
+// M is first needed only when the recursion reaches it, so the main stream waits on
+// the side stream's event for that block (or leaf) right before using it.  Each
+// block still receives its updates in the reference's order (the side stream is
+// FIFO), so the factor is unchanged; the cascades just leave the critical path.
+// Only M's upper blocks and leaves are updated: cholesky_rec never reads M.lower.
+// SPG_CHOL_SERIAL=1 restores the single-stream schedule (A/B checks).
+static const bool g_chol_serial = std::getenv("SPG_CHOL_SERIAL") != nullptr;
+
 void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work) {
     cur_op_ = 6;
     op_copy(p, M, work);
     const DHodlr* Wp = &W;
-    p.launches.push_back([Wp](cudaStream_t st) { Wp->zero(st); });
+    push(p, [Wp](cudaStream_t st) { Wp->zero(st); });
+    if (g_chol_serial) {
+        chol_deferred_ = false;
+        chol_rec(p, 0, work, W);
+        return;
+    }
+    const int nn = tree_.nnodes(), nside = (int)sides_.size();
+    last_leaf_ev_.assign(nn, -1);
+    last_block_ev_.assign(nn, -1);
+    const int ev_fork = nn * (nside + 2), ev_join = ev_fork + 1;
+    record(p, ev_fork);
+    for (int i = 0; i < nside; ++i) {
+        side_sel_ = i;
+        wait(p, ev_fork);
+    }
+    side_sel_ = -1;
+    chol_deferred_ = true;
     chol_rec(p, 0, work, W);
+    chol_deferred_ = false;
+    for (int i = 0; i < nside; ++i) {
+        side_sel_ = i;
+        record(p, ev_join + i);
+        side_sel_ = -1;
+        wait(p, ev_join + i);
+    }
+}
+
+// deferred Schur cascade of node x into the subtree `root` = r(x): the leaf updates
+// on the leaf stream, the upper-block truncations of each depth on that depth's
+// stream, every piece with its own completion event (event slots: ready(x) = x,
+// leaves(x) = nn + x, blocks(x, depth d) = nn * (2 + d) + x)
+void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU, const double* QV, const int* qrank) {
+    const int nn = tree_.nnodes(), nside = (int)sides_.size();
+    std::vector<int> in, lv;
+    tree_.subtree(root, in, lv);
+    std::vector<LowRankUpd> upd;
+    int maxm = 0;
+    for (int f : lv) {
+        const int b = tree_.begin[f], s = tree_.size[f];
+        upd.push_back(LowRankUpd{M.leaf(f), QU + b, QV + b, s, s, tree_.n, tree_.n, qrank, 1.0});
+        maxm = std::max(maxm, s);
+    }
+    side_sel_ = nside - 1;
+    wait(p, x);
+    if (!upd.empty()) {
+        const LowRankUpd* d = arena_->push(upd);
+        const int ni = (int)upd.size();
+        push_timed(p, PC_LEAF, [d, ni, maxm](cudaStream_t st) { launch_lowrank_update(d, ni, maxm, st); });
+    }
+    record(p, nn + x);
+    for (int f : lv) last_leaf_ev_[f] = nn + x;
+    std::vector<std::vector<int>> nodes(tree_.depth + 1);
+    std::vector<std::vector<TTask>> bylev(tree_.depth + 1);
+    for (int y : in) {
+        const int l = tree_.left[y], r = tree_.right[y];
+        const int bl = tree_.begin[l], br = tree_.begin[r];
+        TTask up{};
+        up.p = tree_.size[l]; up.s = tree_.size[r]; up.ng = 2;
+        up.g[0] = TGroup{M.upU(y), M.upV(y), tree_.n, tree_.n, M.rup(y), 0, 1.0, nullptr};
+        up.g[1] = TGroup{QU + bl, QV + br, tree_.n, tree_.n, qrank, 0, 1.0, nullptr};
+        up.ou = M.upU(y); up.ov = M.upV(y); up.ldou = up.ldov = tree_.n; up.orank = M.rup(y); up.skipg = 1;
+        up.tag = cur_op_ * 100000 + 50000 + y;
+        bylev[tree_.level[y]].push_back(up);
+        nodes[tree_.level[y]].push_back(y);
+    }
+    for (int d = tree_.depth; d >= 0; --d) {   // deepest first: the recursion needs those soonest
+        if (bylev[d].empty()) continue;
+        side_sel_ = std::min(d, nside - 2);
+        wait(p, x);
+        trunc(p, bylev[d]);
+        const int ev = nn * (2 + d) + x;
+        record(p, ev);
+        for (int y : nodes[d]) last_block_ev_[y] = ev;
+    }
+    side_sel_ = -1;
 }
 
 void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     const int n = tree_.n;
     if (tree_.leaf(x)) {
+        if (chol_deferred_ && last_leaf_ev_[x] >= 0) wait(p, last_leaf_ev_[x]);
         const int s = tree_.size[x];
         std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s, W.leaf_dinv(x)}};
         const CholItem* d = arena_->push(ci);
@@ -711,6 +840,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     const int t = tree_.level[x];
     const int bl = tree_.begin[l], br = tree_.begin[r], s1 = tree_.size[l], s2 = tree_.size[r];
     chol_rec(p, l, M, W);
+    if (chol_deferred_ && last_block_ev_[x] >= 0) wait(p, last_block_ev_[x]);   // m12 complete
     // b12 = trunc({W11^{-T} m12.U, m12.V})
     double* P0 = panel(0);
     copy(p, {CopyItem{M.upU(x), P0 + bl, s1, n, n, M.rup(x), 0, 1.0, nullptr}}, s1, KCAP);
@@ -725,12 +855,17 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     // Schur: M22 -= V (U^T U) V^T
     {
         double* G = coef_ + (size_t)(4 * x + 2) * KCAP * KCAP;
-        double* P1 = panel(1);
+        double* P1 = chol_deferred_ ? chol_panels_[t] : panel(1);
         gemm(p, {gitem(W.upU(x), n, 1, W.upU(x), n, 0, G, KCAP, 0, W.rup(x), 0, W.rup(x), s1, nullptr, -1.0, 0.0)},
              {make_int3(KCAP, KCAP, s1)});
         gemm(p, {gitem(W.upV(x), n, 0, G, KCAP, 0, P1 + br, n, s2, nullptr, 0, W.rup(x), 0, W.rup(x), 1.0, 0.0)},
              {make_int3(s2, KCAP, KCAP)});
-        cascade(p, M, {Cascade{r, P1, W.slabV(t), W.rup(x), 1.0}});
+        if (chol_deferred_) {
+            record(p, x);
+            cascade_chol(p, M, x, r, P1, W.slabV(t), W.rup(x));
+        } else {
+            cascade(p, M, {Cascade{r, P1, W.slabV(t), W.rup(x), 1.0}});
+        }
     }
     chol_rec(p, r, M, W);
 }
@@ -814,7 +949,7 @@ void Engine::sur_levels(Plan& p, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         const double* src = B.leaves;
         double* dst = Y.leaves;
         const size_t lb = sizeof(double) * B.leaf_doubles;
-        p.launches.push_back([=](cudaStream_t st) {
+        push(p, [=](cudaStream_t st) {
             SPG_CUDA(cudaMemcpyAsync(dst, src, lb, cudaMemcpyDeviceToDevice, st));
         });
         const TrsmItem* d = arena_->push(ti);
@@ -852,7 +987,7 @@ void Engine::sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         const int s = tree_.size[x];
         const double* src = B.leaf(x);
         double* dst = Y.leaf(x);
-        p.launches.push_back([=](cudaStream_t st) {
+        push(p, [=](cudaStream_t st) {
             SPG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, st));
         });
         std::vector<TrsmItem> ti{TrsmItem{W.leaf(x), Y.leaf(x), s, s, s, nullptr, s, 0, 1, W.leaf_dinv(x)}};
@@ -977,7 +1112,7 @@ void Engine::surt_levels(Plan& p, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         const double* src = B.leaves;
         double* dst = Y.leaves;
         const size_t lb = sizeof(double) * B.leaf_doubles;
-        p.launches.push_back([=](cudaStream_t st) {
+        push(p, [=](cudaStream_t st) {
             SPG_CUDA(cudaMemcpyAsync(dst, src, lb, cudaMemcpyDeviceToDevice, st));
         });
         const TrsmItem* d = arena_->push(ti);
@@ -1015,7 +1150,7 @@ void Engine::surt_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         const int s = tree_.size[x];
         const double* src = B.leaf(x);
         double* dst = Y.leaf(x);
-        p.launches.push_back([=](cudaStream_t st) {
+        push(p, [=](cudaStream_t st) {
             SPG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, st));
         });
         std::vector<TrsmItem> ti{TrsmItem{W.leaf(x), Y.leaf(x), s, s, s, nullptr, s, 1, 1, W.leaf_dinv(x)}};

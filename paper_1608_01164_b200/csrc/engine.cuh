@@ -179,6 +179,9 @@ public:
     void prof_sum(double* ms_per_class, long long* batches_per_class) const;
     void prof_clear();
     void push_timed(Plan& p, int cls, Launch l);
+    void push(Plan& p, Launch l);
+    void record(Plan& p, int e);   // event slot e
+    void wait(Plan& p, int e);
 
 private:
     void chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W);
@@ -191,6 +194,14 @@ private:
     HTree tree_;
     double eps_;
     cudaStream_t st_ = nullptr;
+    std::vector<cudaStream_t> sides_;   // deferred Schur cascades of the Cholesky (per depth + leaves)
+    int side_sel_ = -1;                 // stream of the launches being built (-1 = main)
+    std::vector<cudaEvent_t> events_;
+    std::vector<std::unique_ptr<Workspace>> ws_side_;   // one stack per side stream
+    std::vector<double*> chol_panels_;  // per-depth Schur panels (a deferred cascade reads its own)
+    bool chol_deferred_ = false;
+    std::vector<int> last_leaf_ev_, last_block_ev_;   // latest side-stream event touching a leaf / block
+    void cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU, const double* QV, const int* qrank);
     std::unique_ptr<Arena> arena_;
     std::unique_ptr<Workspace> ws_;
     DevTree dtree_{};
