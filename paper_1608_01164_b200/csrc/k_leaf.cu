@@ -460,93 +460,121 @@ __device__ __forceinline__ double rsqrt_nr(double d, double& root) {
     return y;
 }
 
+// W_bb^{-1} = (L11^{-1})^T of one panel by warp 0 (lane i: row i of L11^{-1}, i.e.
+// column i of D), from the panel's L11 / 1/diag left in shared memory
+__device__ __forceinline__ void chol3_dinv(const double* sL11, const double* sInv, int nb, double* D, unsigned* status) {
+    const int lane = threadIdx.x & 31;
+    double tv[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) tv[c] = c == lane ? 1.0 : 0.0;
+    bool sing = false;
+#pragma unroll
+    for (int j = 31; j >= 0; --j) {
+        if (sL11[j * 33 + j] == 0.0) sing = true;
+        tv[j] = tv[j] * sInv[j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) tv[k] -= tv[j] * sL11[j * 33 + k];
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) D[c + 32 * lane] = (lane < nb && c < nb) ? tv[c] : 0.0;
+    if (sing) atomicOr(status, ST_SINGULAR);
+}
+
 __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __restrict__ it, unsigned* status) {
     extern __shared__ double sm[];
     const CholItem C = it[blockIdx.x];
     const int n = C.n;
     const int ldp = chol_ldp(n);
     double* sP = sm;                     // panel (n - J) x 32, col-major ld ldp
-    double* sPart = sm + ldp * CH_NB;    // C3_TASKS partial 8 x 32 tiles (row-major)
+    double* sPart = sm + ldp * CH_NB;    // partial S: per (K segment, column) a row vector, ld LDR
     __shared__ double sL11[32 * 33];
     __shared__ double sInv[32];
-    __shared__ double sCol[32];
+    __shared__ double sCol[2][32];
     __shared__ int sFail;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gi = lane >> 2, gk = lane & 3;
+    constexpr int NW = CH_THREADS / 32;
     const long long ldw = C.ldw;
     if (tid == 0) sFail = 0;
     for (long long idx = tid; idx < (long long)n * n; idx += CH_THREADS) {
         const int i = idx % n, j = idx / n;
         if (i > j) C.W[i + (long long)j * ldw] = 0.0;
     }
+    __syncthreads();
     long long* tr = C.trace;
 #define C3_TRACE(k) if (tr && tid == 0) tr[(J / CH_NB) * 8 + (k)] = clock64()
     for (int J = 0; J < n; J += CH_NB) {
         const int nb = min(CH_NB, n - J), mr = n - J;
         const int nrt = (mr + 7) / 8;
         C3_TRACE(0);
-        for (int idx = tid; idx < mr * nb; idx += CH_THREADS) {
-            const int i = idx % mr, jj = idx / mr;
-            cp_async8_l(sP + i + jj * ldp, C.M + (J + i) + (long long)(J + jj) * C.ldm);
-        }
-        cp_commit_l();
-        // (1) partial S tiles
         const int nks = J / 4;
-        int nseg = nks > 0 ? max(1, min(nks / 8, C3_TASKS / nrt)) : 0;
+        const int nseg = nks > 0 ? max(1, min(nks / 8, C3_TASKS / nrt)) : 0;
         const int ntask = nrt * nseg;
-        for (int task = warp; task < ntask; task += CH_THREADS / 32) {
-            const int rt = task / nseg, seg = task % nseg;
-            const int ks0 = seg * nks / nseg, ks1 = (seg + 1) * nks / nseg;
-            const int row = J + rt * 8 + gi;
-            const double* pa = C.W + (long long)min(row, n - 1) * ldw + gk;   // L(row, k) = W(k, row)
-            const double* pb[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) pb[c] = C.W + (long long)(J + min(c * 8 + gi, nb - 1)) * ldw + gk;
-            double acc[4][2];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
-            int ks = ks0;
-            for (; ks + 8 <= ks1; ks += 8) {
-                double a[8], b[8][4];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    a[u] = pa[4 * (ks + u)];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) b[u][c] = pb[c][4 * (ks + u)];
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) dmma_leaf(acc[c][0], acc[c][1], a[u], b[u][c]);
-            }
-            for (; ks < ks1; ++ks) {
-                const double a = pa[4 * ks];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) dmma_leaf(acc[c][0], acc[c][1], a, pb[c][4 * ks]);
-            }
-            double* pt = sPart + task * 256 + gi * 32;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                pt[c * 8 + 2 * gk] = acc[c][0];
-                pt[c * 8 + 2 * gk + 1] = acc[c][1];
-            }
-        }
-        cp_wait_l<0>();
-        __syncthreads();
-        C3_TRACE(1);
-        if (nseg > 0)
-            for (int idx = tid; idx < mr * nb; idx += CH_THREADS) {
+        const int LDR = ((nrt * 8 + 15) / 16) * 16 + 4;   // = 4 mod 16: conflict-free fragment stores
+        if (warp == 0) {
+            // W_bb^{-1} of the previous panel, overlapped with this panel's update
+            if (J > 0 && C.D) chol3_dinv(sL11, sInv, CH_NB, C.D + (long long)(J / 32 - 1) * 1024, status);
+        } else {
+            for (int idx = tid - 32; idx < mr * nb; idx += CH_THREADS - 32) {
                 const int i = idx % mr, jj = idx / mr;
-                if (i < jj) continue;
-                const int rt = i >> 3;
-                const double* pt = sPart + (rt * nseg) * 256 + (i & 7) * 32 + jj;
-                double s = 0.0;
-                for (int sg = 0; sg < nseg; ++sg) s += pt[sg * 256];
-                sP[i + jj * ldp] -= s;
+                cp_async8_l(sP + i + jj * ldp, C.M + (J + i) + (long long)(J + jj) * C.ldm);
             }
+            cp_commit_l();
+            // (1) partial S tiles over (8-row tile, K segment) tasks, warps 1..15
+            for (int task = warp - 1; task < ntask; task += NW - 1) {
+                const int rt = task / nseg, seg = task % nseg;
+                const int ks0 = seg * nks / nseg, ks1 = (seg + 1) * nks / nseg;
+                const int row = J + rt * 8 + gi;
+                const double* pa = C.W + (long long)min(row, n - 1) * ldw + gk;   // L(row, k) = W(k, row)
+                const double* pb[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) pb[c] = C.W + (long long)(J + min(c * 8 + gi, nb - 1)) * ldw + gk;
+                double acc[4][2];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+                int ks = ks0;
+                for (; ks + 8 <= ks1; ks += 8) {
+                    double a[8], bq[8][4];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        a[u] = pa[4 * (ks + u)];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) bq[u][c] = pb[c][4 * (ks + u)];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) dmma_leaf(acc[c][0], acc[c][1], a[u], bq[u][c]);
+                }
+                for (; ks < ks1; ++ks) {
+                    const double a = pa[4 * ks];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) dmma_leaf(acc[c][0], acc[c][1], a, pb[c][4 * ks]);
+                }
+                double* pt = sPart + (long long)(seg * 32) * LDR + rt * 8 + gi;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    pt[(c * 8 + 2 * gk) * LDR] = acc[c][0];
+                    pt[(c * 8 + 2 * gk + 1) * LDR] = acc[c][1];
+                }
+            }
+            cp_wait_l<0>();
+        }
+        C3_TRACE(1);
         __syncthreads();
         C3_TRACE(2);
-        // (2a) diagonal block, warp 0
+        if (nseg > 0)   // P = M - S, fixed-order reduction over the K segments
+            for (int jj = warp; jj < nb; jj += NW)
+                for (int i = jj + lane; i < mr; i += 32) {
+                    const double* pt = sPart + (long long)jj * LDR + i;
+                    double s = 0.0;
+                    for (int sg = 0; sg < nseg; ++sg) s += pt[(long long)sg * 32 * LDR];
+                    sP[i + jj * ldp] -= s;
+                }
+        __syncthreads();
+        C3_TRACE(3);
+        // (2a) diagonal block, warp 0: rows in registers, column j broadcast through
+        //      a double-buffered shared vector (one warp barrier per column)
         if (warp == 0) {
             double r[32];
 #pragma unroll
@@ -561,12 +589,12 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
                     const double y = rsqrt_nr(d, ljj);
                     const double lij = lane == j ? ljj : r[j] * y;
                     r[j] = lij;
-                    sCol[lane] = lij;
+                    sCol[j & 1][lane] = lij;
                     if (lane == 0) sInv[j] = y;
                     __syncwarp();
+                    // entries right of a lane's diagonal are never read: no predicate needed
 #pragma unroll
-                    for (int k = j + 1; k < 32; ++k) r[k] -= lij * sCol[k];
-                    __syncwarp();
+                    for (int k = j + 1; k < 32; ++k) r[k] -= lij * sCol[j & 1][k];
                 }
             }
             if (fail && lane == 0) sFail = 1;
@@ -575,36 +603,17 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
                 const bool in = lane < nb && c < nb;
                 sL11[lane * 33 + c] = in ? (c <= lane ? r[c] : 0.0) : (c == lane ? 1.0 : 0.0);
             }
-            if (lane < nb) {
-                double* wcol = C.W + J + (long long)(J + lane) * ldw;   // W(J.., J+lane) = L(J+lane, J..)
-#pragma unroll
-                for (int c = 0; c < 32; ++c)
-                    if (c <= lane) wcol[c] = r[c];
-            }
             if (lane >= nb) sInv[lane] = 1.0;
         }
         __syncthreads();
-        C3_TRACE(3);
-        if (warp == 0) {
-            if (C.D) {   // (2c) D = W_bb^{-1} = (L11^{-1})^T, lane i -> row i of L11^{-1} = column i of D
-                double tv[32];
-#pragma unroll
-                for (int c = 0; c < 32; ++c) tv[c] = c == lane ? 1.0 : 0.0;
-                bool sing = false;
-#pragma unroll
-                for (int j = 31; j >= 0; --j) {
-                    if (sL11[j * 33 + j] == 0.0) sing = true;
-                    tv[j] = tv[j] * sInv[j];
-#pragma unroll
-                    for (int k = 0; k < j; ++k) tv[k] -= tv[j] * sL11[j * 33 + k];
-                }
-                double* D = C.D + (long long)(J / 32) * 1024;
-#pragma unroll
-                for (int c = 0; c < 32; ++c) D[c + 32 * lane] = (lane < nb && c < nb) ? tv[c] : 0.0;
-                if (sing) atomicOr(status, ST_SINGULAR);
-            }
-        } else {
+        C3_TRACE(4);
+        if (warp > 0) {
+            // diagonal block of L -> W(J.., J+col) (coalesced), then
             // (2b) L21 = P21 L11^{-T}, one row per thread, written straight to W
+            for (int idx = tid - 32; idx < 32 * nb; idx += CH_THREADS - 32) {
+                const int c = idx & 31, col = idx >> 5;   // W(J + c, J + col) = L(J + col, J + c)
+                if (c <= col && c < nb) C.W[(J + c) + (long long)(J + col) * ldw] = sL11[col * 33 + c];
+            }
             const volatile double* vL11 = sL11;
             const volatile double* vInv = sInv;
 #pragma unroll 1
@@ -627,14 +636,17 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
             }
         }
         __syncthreads();
-        C3_TRACE(4);
         C3_TRACE(5);
     }
 #undef C3_TRACE
+    if (warp == 0 && C.D) {   // W_bb^{-1} of the last panel
+        const int Jl = ((n - 1) / 32) * 32;
+        chol3_dinv(sL11, sInv, min(CH_NB, n - Jl), C.D + (long long)(Jl / 32) * 1024, status);
+    }
     if (tid == 0 && sFail) atomicOr(status, ST_NPD);
 }
 
-static size_t chol3_smem(int n) { return sizeof(double) * ((size_t)chol_ldp(n) * CH_NB + (size_t)C3_TASKS * 256); }
+static size_t chol3_smem(int n) { return sizeof(double) * ((size_t)chol_ldp(n) * CH_NB + (size_t)32 * 480); }
 
 static size_t chol2_smem(int kc, int n) {
     const int kcp = kc == 16 ? 20 : kc;
