@@ -40,6 +40,21 @@ struct CudaError : std::runtime_error {
                                    " at " + __FILE__ + ":" + std::to_string(__LINE__));   \
     } while (0)
 
+// Asynchronous global -> shared copies (cp.async, 8 bytes each).  Staging loops
+// written as "for (i = tid; i < n; i += blockDim.x) s[i] = g[i]" wait for every
+// load before the next iteration; issuing cp.async instead keeps all of a thread's
+// copies in flight at once (one memory latency per staging pass, not one per element).
+#ifdef __CUDACC__
+__device__ __forceinline__ void cpa8(double* dst, const double* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+#endif
+
 extern std::atomic<long long> g_launches;   // kernel launches issued (host-side count)
 #define SPG_LAUNCH_CHECK()            \
     do {                              \

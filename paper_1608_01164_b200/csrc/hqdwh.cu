@@ -522,8 +522,10 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     }
     I.launches = g_launches.load() - launches0;
     {
-        double ctr[3];
+        double ctr[4];
         SPG_CUDA(cudaMemcpy(ctr, S.counters, sizeof(ctr), cudaMemcpyDeviceToHost));
+        if (std::getenv("SPG_CORE_STATS"))
+            std::fprintf(stderr, "core tasks %.0f, with k_in > 64: %.0f\n", ctr[2], ctr[3]);
         I.trunc_bytes = ctr[0];
         I.gemm_flops = ctr[1];
         I.trunc_tasks = (long long)ctr[2];

@@ -398,10 +398,15 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     const double* Rv = core_final_R(t, ws, 1);
     for (int idx = tid; idx < K3 * K3; idx += TS_THREADS) {
         const int i = idx & 63, j = idx >> 6;
-        const bool in = i < k && j < k && i <= j;
-        sZ[i + j * L3] = in ? Ru[i + (long long)j * KIN_MAX] : 0.0;
-        sJ[i + j * L3] = in ? Rv[i + (long long)j * KIN_MAX] : 0.0;
+        if (i < k && j < k && i <= j) {
+            cpa8(sZ + i + j * L3, Ru + i + (long long)j * KIN_MAX);
+            cpa8(sJ + i + j * L3, Rv + i + (long long)j * KIN_MAX);
+        } else {
+            sZ[i + j * L3] = 0.0;
+            sJ[i + j * L3] = 0.0;
+        }
     }
+    cpa_wait_all();
     if (tid < K3) { sAct[tid] = 1; sCn2[0][tid] = -1.0; sCn2[1][tid] = -1.0; }
     __syncthreads();
     // C[i][j] = sum_l Ru[i][l] Rv[j][l]
@@ -710,6 +715,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_core_any(const TTask* __restrict
             core3_body(t, k, ws, eps, status, smem);
             return;
         }
+        if (k > K3 && threadIdx.x == 0) atomicAdd(reinterpret_cast<double*>(status + 16) + 3, 1.0);
     }
     core2_body(tasks, ws, eps, status, smem);
 }

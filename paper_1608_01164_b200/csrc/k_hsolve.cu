@@ -282,8 +282,10 @@ __global__ void __launch_bounds__(H2_THREADS) k_hsolve2(DevTree t, DevHodlrView 
             const int s32 = ((s + 31) / 32) * 32;
             for (int idx = tid; idx < s32 * HS_TC; idx += H2_THREADS) {
                 const int i = idx % s32, c = idx / s32;
-                sX[i + c * LD] = (i < s && c < ncols) ? Xb[(lb + i) + c * ldx] : 0.0;
+                if (i < s && c < ncols) cpa8(sX + i + c * LD, Xb + (lb + i) + c * ldx);
+                else sX[i + c * LD] = 0.0;
             }
+            cpa_wait_all();
             __syncthreads();
             const double* Wl = W.leaves + W.leaf_off[lo];
             const double* D = W.dinv + W.dinv_off[lo];

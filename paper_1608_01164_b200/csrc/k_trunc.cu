@@ -260,19 +260,13 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
             const int gi = sub0 + i;
             const bool in = gi < nr;
             constexpr int CPT = TS_THREADS / SB;   // column groups per pass
-            for (int c0 = threadIdx.x >> 7; c0 < k; c0 += 4 * CPT) {   // 4 independent loads in flight
-                double v[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int c = c0 + u * CPT;
-                    v[u] = (in && c < k) ? sCol[c][gi] : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int c = c0 + u * CPT;
-                    if (c < k) B[(long long)c * SB + i] = sScl[c] * v[u];
-                }
+            for (int c = threadIdx.x >> 7; c < k; c += CPT) {
+                if (in) cpa8(B + (long long)c * SB + i, sCol[c] + gi);
+                else B[(long long)c * SB + i] = 0.0;
             }
+            cpa_wait_all();   // own copies landed: scale them in place
+            for (int c = threadIdx.x >> 7; c < k; c += CPT)
+                if (in) B[(long long)c * SB + i] *= sScl[c];
         };
         stream_qr(k, nr, base, base + nsub * SB * KIN_MAX, base + nsub * SB * KIN_MAX + nsub * TS_TAUT, sR, sB,
                   sTau, load);
@@ -284,17 +278,21 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
         double* mb = merge_area(t, ws, side);
         const long long nsubm = ts_nsub(ns * KIN_MAX);
         auto load = [&](int sub0, double* B) {
-            for (int idx = threadIdx.x; idx < SB * k; idx += blockDim.x) {
-                const int i = idx % SB, c = idx / SB;
-                const int gi = sub0 + i;
-                double v = 0.0;
-                if (gi < mrows) {
-                    const int s = gi / k, lr = gi % k;
-                    const double* Rs = seg_area(t, ws, side, s) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + TS_TAUT);
-                    v = Rs[lr + (long long)c * KIN_MAX];
-                }
-                B[(long long)c * SB + i] = v;
+            const int i = threadIdx.x & 127;
+            const int gi = sub0 + i;
+            constexpr int CPT = TS_THREADS / SB;
+            const double* Rs = nullptr;
+            int lr = 0;
+            if (gi < mrows) {
+                const int s = gi / k;
+                lr = gi % k;
+                Rs = seg_area(t, ws, side, s) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + TS_TAUT);
             }
+            for (int c = threadIdx.x >> 7; c < k; c += CPT) {
+                if (Rs) cpa8(B + (long long)c * SB + i, Rs + lr + (long long)c * KIN_MAX);
+                else B[(long long)c * SB + i] = 0.0;
+            }
+            cpa_wait_all();
         };
         stream_qr(k, mrows, mb, mb + nsubm * SB * KIN_MAX, mb + nsubm * SB * KIN_MAX + nsubm * TS_TAUT, sR, sB,
                   sTau, load);
@@ -468,15 +466,17 @@ __device__ void stream_apply(int k, int r, int nrows, const double* refl, const 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     for (int idx = tid; idx < k * r; idx += blockDim.x) {
         const int i = idx % k, c = idx / k;
-        sZ[i + c * KIN_MAX] = Z0[i + (long long)c * ldz];
+        cpa8(sZ + i + c * KIN_MAX, Z0 + i + (long long)c * ldz);
     }
+    cpa_wait_all();
     const int nsub = (nrows + SB - 1) / SB;
     const int npan = (k + TS_NB - 1) / TS_NB;
     for (int b = nsub - 1; b >= 0; --b) {
         __syncthreads();
         const double* vb = refl + (long long)b * SB * KIN_MAX;
-        for (int i = tid; i < SB * k; i += blockDim.x) sV[i] = vb[i];
-        for (int i = tid; i < TS_TAUT; i += blockDim.x) sTT[i] = taut[(long long)b * TS_TAUT + i];
+        for (int i = tid; i < SB * k; i += blockDim.x) cpa8(sV + i, vb + i);
+        for (int i = tid; i < TS_TAUT; i += blockDim.x) cpa8(sTT + i, taut + (long long)b * TS_TAUT + i);
+        cpa_wait_all();
         __syncthreads();
         for (int c = warp; c < r; c += nwarps) {
             double o[SB / 32];

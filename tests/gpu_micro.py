@@ -9,8 +9,8 @@ sizes = [int(a) for a in sys.argv[2:]] or [256]
 for n in sizes:
     if mode == "chol":
         o = S.micro_kernel(0, n, 20)
-        print(f"leaf_chol n={n}: {o[0]:.1f} us/launch; cycles/panel: update {o[1]:.0f} P {o[2]:.0f} diag {o[3]:.0f} "
-              f"solve {o[4]:.0f} write {o[5]:.0f} gap {o[6]:.0f}; status {int(o[7])}", flush=True)
+        print(f"leaf_chol n={n}: {o[0]:.1f} us/launch; cycles/panel: tasks {o[1]:.0f} wait {o[2]:.0f} reduce {o[3]:.0f} "
+              f"diag {o[4]:.0f} solve {o[5]:.0f} gap {o[6]:.0f}; status {int(o[7])}", flush=True)
     else:
         for g in (1, 2):
             o = S.micro_kernel(g, n, 20)
