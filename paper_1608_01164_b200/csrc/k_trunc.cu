@@ -8,6 +8,7 @@
 //
 // Five launches per batch: tsqr(level 0) -> tsqr(merge) -> core -> apply(merge) -> apply(level 0).
 // Ranks are read from / written to device memory, so a batch never syncs the host.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -532,6 +533,132 @@ __device__ void stream_apply(int k, int r, int nrows, const double* refl, const 
     }
 }
 
+// ------------------------------------------------------------------ Q application, k <= 64 (DMMA)
+// Every sub-block's output rows start at zero, so Q_b [Z; 0] = [Z - W'; -V_b W']
+// with W' = T_b Z, T_b the compact-WY factor of ALL k reflectors of the block
+// (I - Y T_b Y^T, Y = [E; V_b]).  T_b is assembled from the stored panel T's and
+// the Gram blocks V_p^T V_q (panel merge T_{AB} = -T_A (V_A^T V_B) T_B), after
+// which the block costs two small GEMMs on the FP64 tensor path instead of k
+// dependent reflector steps.
+constexpr int AD_K = 64, AD_LV = SB + 4, AD_LG = AD_K + 4;
+__constant__ int g_apply_v1_dev = 0;   // SPG_APPLY_V1=1: reflector-by-panel path for every k (A/B checks)
+__device__ __forceinline__ void dmma_a(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+size_t apply_dmma_smem() { return sizeof(double) * ((size_t)AD_LV * AD_K + 3 * (size_t)AD_LG * AD_K + 64 * 8 + TS_TAUT); }
+
+template <class Writer>
+__device__ void stream_apply_dmma(int k, int r, int nrows, const double* refl, const double* taut, const double* Z0,
+                                  int ldz, double* smem, const Writer& write) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int gi = lane >> 2, gk = lane & 3;
+    double* sV = smem;                          // SB x k, ld AD_LV
+    double* sTG = sV + AD_LV * AD_K;            // T_b (upper, built over the Gram blocks), ld AD_LG
+    double* sZ = sTG + AD_LG * AD_K;            // Z (k x r), ld AD_LG
+    double* sW = sZ + AD_LG * AD_K;             // W' = T_b Z, ld AD_LG
+    double* sX = sW + AD_LG * AD_K;             // merge scratch (<= 64 x 8)
+    double* sTT = sX + 64 * 8;                  // taus + panel T's of the block
+    const int npan = (k + TS_NB - 1) / TS_NB;
+    const int kp = npan * TS_NB;                // k padded to the panel width
+    const int ntr = (r + 7) / 8;
+    for (int idx = tid; idx < kp * r; idx += blockDim.x) {
+        const int i = idx % kp, c = idx / kp;
+        if (i < k) cpa8(sZ + i + c * AD_LG, Z0 + i + (long long)c * ldz);
+        else sZ[i + c * AD_LG] = 0.0;
+    }
+    for (int idx = tid; idx < kp * 8; idx += blockDim.x) {   // zero padding columns of W' (r..ntr*8)
+        const int i = idx % kp, c = r + idx / kp;
+        if (c < ntr * 8) sZ[i + c * AD_LG] = 0.0;
+    }
+    cpa_wait_all();
+    const int nsub = (nrows + SB - 1) / SB;
+    for (int b = nsub - 1; b >= 0; --b) {
+        __syncthreads();
+        const double* vb = refl + (long long)b * SB * KIN_MAX;
+        for (int idx = tid; idx < SB * kp; idx += blockDim.x) {
+            const int i = idx % SB, c = idx / SB;
+            if (c < k) cpa8(sV + i + c * AD_LV, vb + i + (long long)c * SB);
+            else sV[i + c * AD_LV] = 0.0;
+        }
+        for (int i = tid; i < TS_TAUT; i += blockDim.x) cpa8(sTT + i, taut + (long long)b * TS_TAUT + i);
+        cpa_wait_all();
+        __syncthreads();
+        // diagonal blocks of T_b = the panel T's; strictly-upper blocks = Gram V_p^T V_q (p < q)
+        for (int idx = tid; idx < npan * 64; idx += blockDim.x) {
+            const int p = idx >> 6, a = (idx >> 3) & 7, c = idx & 7;
+            sTG[(8 * p + a) + (8 * p + c) * AD_LG] = a <= c ? sTT[KIN_MAX + p * 64 + a + c * 8] : 0.0;
+        }
+        const int npairs = npan * (npan - 1) / 2;
+        for (int task = warp; task < npairs; task += nwarps) {
+            int p = 0, q = task;   // task -> (p, q), p < q
+            while (q >= npan - 1 - p) { q -= npan - 1 - p; ++p; }
+            q += p + 1;
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll 8
+            for (int ks = 0; ks < SB / 4; ++ks)
+                dmma_a(c0, c1, sV[(4 * ks + gk) + (8 * p + gi) * AD_LV], sV[(4 * ks + gk) + (8 * q + gi) * AD_LV]);
+            sTG[(8 * p + gi) + (8 * q + 2 * gk) * AD_LG] = c0;
+            sTG[(8 * p + gi) + (8 * q + 2 * gk + 1) * AD_LG] = c1;
+        }
+        // lower blocks of T_b are zero
+        for (int idx = tid; idx < kp * kp; idx += blockDim.x) {
+            const int i = idx % kp, c = idx / kp;
+            if ((i >> 3) > (c >> 3)) sTG[i + c * AD_LG] = 0.0;
+        }
+        __syncthreads();
+        // merge: T(0:8q, q-block) = -T(0:8q, 0:8q) G(0:8q, q-block) T_q, q = 1 .. npan-1
+        for (int q = 1; q < npan; ++q) {
+            const int m = 8 * q;
+            if (warp < q) {   // X1 = G(0:m, q) T_q : 8-row tile `warp`
+                double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks)
+                    dmma_a(c0, c1, sTG[(8 * warp + gi) + (m + 4 * ks + gk) * AD_LG],
+                           sTG[(m + 4 * ks + gk) + (m + gi) * AD_LG]);
+                sX[(8 * warp + gi) + (2 * gk) * 64] = c0;
+                sX[(8 * warp + gi) + (2 * gk + 1) * 64] = c1;
+            }
+            __syncthreads();
+            if (warp < q) {   // T(0:m, q) = -T(0:m, 0:m) X1 (T upper: k-steps from this tile's rows)
+                double c0 = 0.0, c1 = 0.0;
+                for (int ks = 2 * warp; ks < 2 * q; ++ks)
+                    dmma_a(c0, c1, sTG[(8 * warp + gi) + (4 * ks + gk) * AD_LG], sX[(4 * ks + gk) + gi * 64]);
+                sTG[(8 * warp + gi) + (m + 2 * gk) * AD_LG] = -c0;
+                sTG[(8 * warp + gi) + (m + 2 * gk + 1) * AD_LG] = -c1;
+            }
+            __syncthreads();
+        }
+        // W' = T_b Z  (kp x ntr*8)
+        for (int task = warp; task < npan * ntr; task += nwarps) {
+            const int mt = task % npan, nt = task / npan;
+            double c0 = 0.0, c1 = 0.0;
+            for (int ks = 2 * mt; ks < 2 * npan; ++ks)
+                dmma_a(c0, c1, sTG[(8 * mt + gi) + (4 * ks + gk) * AD_LG], sZ[(4 * ks + gk) + (8 * nt + gi) * AD_LG]);
+            sW[(8 * mt + gi) + (8 * nt + 2 * gk) * AD_LG] = c0;
+            sW[(8 * mt + gi) + (8 * nt + 2 * gk + 1) * AD_LG] = c1;
+        }
+        __syncthreads();
+        // Z -= W'; block rows O_b = -V_b W'
+        for (int idx = tid; idx < kp * r; idx += blockDim.x) {
+            const int i = idx % kp, c = idx / kp;
+            sZ[i + c * AD_LG] -= sW[i + c * AD_LG];
+        }
+        for (int task = warp; task < (SB / 8) * ntr; task += nwarps) {
+            const int mt = task % (SB / 8), nt = task / (SB / 8);
+            double c0 = 0.0, c1 = 0.0;
+            for (int ks = 0; ks < 2 * npan; ++ks)
+                dmma_a(c0, c1, sV[(8 * mt + gi) + (4 * ks + gk) * AD_LV], sW[(4 * ks + gk) + (8 * nt + gi) * AD_LG]);
+            const int row = b * SB + 8 * mt + gi, col = 8 * nt + 2 * gk;
+            if (row < nrows) {
+                if (col < r) write(row, col, -c0);
+                if (col + 1 < r) write(row, col + 1, -c1);
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ tasks, const int3* __restrict__ items,
                                                      double* __restrict__ ws, int merge) {
     extern __shared__ double smem[];
@@ -561,7 +688,12 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
                 if (i < mrows) Zst[i + (long long)c * ldst] = o[tt];
             }
         };
-        stream_apply(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, sZ, sV, sTT, write);
+        if (k <= AD_K && !g_apply_v1_dev) {
+            auto wr1 = [&](int row, int c, double v) { Zst[row + (long long)c * ldst] = v; };
+            stream_apply_dmma(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, smem, wr1);
+        } else {
+            stream_apply(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, sZ, sV, sTT, write);
+        }
     } else {
         const int s = it.z;
         const int r0 = s * t.seg[side];
@@ -589,16 +721,27 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
                 if (i < nr) out[r0 + i + (long long)c * ldo] = o[tt];
             }
         };
-        stream_apply(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, sZ, sV, sTT, write);
+        if (k <= AD_K && !g_apply_v1_dev) {
+            auto wr1 = [&](int row, int c, double v) { out[r0 + row + (long long)c * ldo] = v; };
+            stream_apply_dmma(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, smem, wr1);
+        } else {
+            stream_apply(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, sZ, sV, sTT, write);
+        }
     }
 }
 
 // ------------------------------------------------------------------ host side
 size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + SB * KIN_MAX + TS_TAUT); }
 size_t trunc_smem_core() { return sizeof(double) * (2 * KIN_MAX * KIN_MAX); }
-size_t trunc_smem_apply() { return sizeof(double) * (KIN_MAX * KCAP + SB * KIN_MAX + TS_TAUT); }
+size_t trunc_smem_apply() {
+    return std::max(sizeof(double) * (KIN_MAX * KCAP + SB * KIN_MAX + TS_TAUT), apply_dmma_smem());
+}
 
 void trunc_init_attributes() {
+    if (std::getenv("SPG_APPLY_V1")) {
+        const int one = 1;
+        SPG_CUDA(cudaMemcpyToSymbol(g_apply_v1_dev, &one, sizeof(int)));
+    }
     SPG_CUDA(cudaFuncSetAttribute(k_tsqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_tsqr()));
     SPG_CUDA(cudaFuncSetAttribute(k_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_core()));
     SPG_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_apply()));
