@@ -277,9 +277,12 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
         TTask& t = tasks[i];
         for (int side = 0; side < 2; ++side) {
             const int rows = side == 0 ? t.p : t.s;
+            // two-level TSQR: segments of `seg` rows stream their sub-blocks in parallel CTAs,
+            // then one CTA folds the nseg stacked R's.  Both levels are chains of 128-row
+            // sub-block QRs, so seg ~ sqrt(rows * k) balances them (k ~ 48 typical).
             int seg = rows, nseg = 1;
-            if (rows > 1024) {
-                seg = (int)std::ceil(std::sqrt((double)rows * KIN_MAX) / SB) * SB;
+            if (rows > 2 * SB) {
+                seg = std::max(2 * SB, (int)std::ceil(std::sqrt((double)rows * 48.0) / SB) * SB);
                 nseg = (rows + seg - 1) / seg;
                 if (nseg == 1) seg = rows;
             }
