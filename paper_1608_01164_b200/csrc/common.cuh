@@ -56,10 +56,12 @@ __device__ __forceinline__ void cpa_wait_all() {
 #endif
 
 extern std::atomic<long long> g_launches;   // kernel launches issued (host-side count)
-#define SPG_LAUNCH_CHECK()            \
-    do {                              \
-        SPG_CUDA(cudaGetLastError()); \
-        ++::spg::g_launches;          \
+extern const bool g_sync_launch;            // SPG_SYNC_LAUNCH=1 (debug, with SPG_NO_GRAPH=1): sync after every launch
+#define SPG_LAUNCH_CHECK()                                                      \
+    do {                                                                        \
+        SPG_CUDA(cudaGetLastError());                                           \
+        if (::spg::g_sync_launch) SPG_CUDA(cudaDeviceSynchronize());            \
+        ++::spg::g_launches;                                                    \
     } while (0)
 
 // ---------------------------------------------------------------- truncation

@@ -24,6 +24,7 @@
 namespace spg {
 double measure_dmma_tflops();
 std::atomic<long long> g_launches{0};
+const bool g_sync_launch = std::getenv("SPG_SYNC_LAUNCH") != nullptr;
 std::atomic<int> g_profile{0};
 }
 

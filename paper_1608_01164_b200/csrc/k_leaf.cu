@@ -14,6 +14,11 @@ __device__ __forceinline__ double warp_sum_l(double v) {
 }
 
 // ---------------------------------------------------------------- elementwise
+// grid-stride CTAs per item for an m x m elementwise pass (64-bit: m reaches n/2 = 65536)
+static unsigned leaf_grid_x(int maxn) {
+    const long long ctas = ((long long)maxn * maxn + 255) / 256;
+    return (unsigned)(ctas < 1 ? 1 : ctas < 64 ? ctas : 64);
+}
 // hodlr_axpby leaves (hodlr.hpp:326-330): X = a A + b B
 __global__ void k_leaf_axpby(const LeafItem* __restrict__ it, double a, const double* ap, double b, const double* bp) {
     const LeafItem L = it[blockIdx.y];
@@ -29,7 +34,7 @@ __global__ void k_leaf_axpby(const LeafItem* __restrict__ it, double a, const do
 void launch_leaf_axpby(const LeafItem* d, int nitems, int maxn, double a, const double* ap, double b,
                        const double* bp, cudaStream_t st) {
     if (!nitems) return;
-    dim3 g((maxn * maxn + 255) / 256 < 64 ? (maxn * maxn + 255) / 256 : 64, nitems);
+    dim3 g(leaf_grid_x(maxn), nitems);
     k_leaf_axpby<<<g, 256, 0, st>>>(d, a, ap, b, bp);
     SPG_LAUNCH_CHECK();
 }
@@ -49,7 +54,7 @@ __global__ void k_leaf_sym(const LeafItem* __restrict__ it) {
 }
 void launch_leaf_symmetrize(const LeafItem* d, int nitems, int maxn, cudaStream_t st) {
     if (!nitems) return;
-    dim3 g((maxn * maxn + 255) / 256 < 64 ? (maxn * maxn + 255) / 256 : 64, nitems);
+    dim3 g(leaf_grid_x(maxn), nitems);
     k_leaf_sym<<<g, 256, 0, st>>>(d);
     SPG_LAUNCH_CHECK();
 }
@@ -68,7 +73,7 @@ __global__ void k_leaf_scale_shift(const LeafItem* __restrict__ it, double s, co
 void launch_leaf_scale_shift(const LeafItem* d, int nitems, int maxn, double s, const double* sp, double mu,
                              cudaStream_t st) {
     if (!nitems) return;
-    dim3 g((maxn * maxn + 255) / 256 < 64 ? (maxn * maxn + 255) / 256 : 64, nitems);
+    dim3 g(leaf_grid_x(maxn), nitems);
     k_leaf_scale_shift<<<g, 256, 0, st>>>(d, s, sp, mu);
     SPG_LAUNCH_CHECK();
 }
