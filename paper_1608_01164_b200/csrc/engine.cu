@@ -873,6 +873,27 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     chol_rec(p, r, M, W);
 }
 
+// all-leaves TRSM of the level-batched solves: the DMMA row-strip kernel when every
+// leaf is a multiple of 32 (diagonal-block inverses present), else the generic one
+void Engine::leaf_trsm_batch(Plan& p, const std::vector<TrsmItem>& ti, const std::vector<int2>& ct) {
+    bool rows = !std::getenv("SPG_TRSM_V1");
+    int maxn = 0;
+    for (const auto& t : ti) {
+        rows = rows && t.D && t.rhs_t && t.n % 32 == 0 && t.n <= TRM_NMAX && !t.ncp && t.nc == t.n;
+        maxn = std::max(maxn, t.n);
+    }
+    const TrsmItem* d = arena_->push(ti);
+    const int ni = (int)ti.size();
+    unsigned* status = sc_.status;
+    if (rows) {
+        push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm_rows(d, ni, maxn, st); });
+        return;
+    }
+    const int2* dc = arena_->push(ct);
+    const int nc = (int)ct.size();
+    push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
+}
+
 // solve_upper_right (hodlr.hpp:579-604, 641-647): Y W = B
 // SPG_SOLVE_RECURSIVE=1 runs the solves in the reference's recursion order (one node per step)
 static const bool g_solve_recursive = std::getenv("SPG_SOLVE_RECURSIVE") != nullptr;
@@ -955,11 +976,7 @@ void Engine::sur_levels(Plan& p, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         push(p, [=](cudaStream_t st) {
             SPG_CUDA(cudaMemcpyAsync(dst, src, lb, cudaMemcpyDeviceToDevice, st));
         });
-        const TrsmItem* d = arena_->push(ti);
-        const int2* dc = arena_->push(ct);
-        const int nc = (int)ct.size();
-        unsigned* status = sc_.status;
-        push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
+        leaf_trsm_batch(p, ti, ct);
     }
     for (int t = tree_.depth - 1; t >= 0; --t) {   // ---- phase B: internal levels, bottom-up
         const auto& xs = tree_.internal_at[t];
@@ -1118,11 +1135,7 @@ void Engine::surt_levels(Plan& p, DHodlr& B, const DHodlr& W, DHodlr& Y) {
         push(p, [=](cudaStream_t st) {
             SPG_CUDA(cudaMemcpyAsync(dst, src, lb, cudaMemcpyDeviceToDevice, st));
         });
-        const TrsmItem* d = arena_->push(ti);
-        const int2* dc = arena_->push(ct);
-        const int nc = (int)ct.size();
-        unsigned* status = sc_.status;
-        push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
+        leaf_trsm_batch(p, ti, ct);
     }
     for (int t = tree_.depth - 1; t >= 0; --t) {   // ---- phase B: internal levels, bottom-up
         const auto& xs = tree_.internal_at[t];

@@ -157,6 +157,7 @@ public:
     void cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs);
     void hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items);
     void copy(Plan& p, std::vector<CopyItem> items, int maxm, int maxk);
+    void leaf_trsm_batch(Plan& p, const std::vector<TrsmItem>& ti, const std::vector<int2>& ct);
 
     // ---- HODLR operations (hodlr.hpp) ------------------------------------------
     void op_axpby(Plan& p, double a, const double* ap, const DHodlr& A, double b, const double* bp, const DHodlr& B,

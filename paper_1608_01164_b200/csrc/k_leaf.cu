@@ -710,7 +710,103 @@ void launch_leaf_trsm(const TrsmItem* d, const int2* d_ctas, int nctas, unsigned
     SPG_LAUNCH_CHECK();
 }
 
+// Leaf TRSM on the FP64 tensor path for the level-batched solves:
+//   mode 0: X <- X W^{-1}    (Y W = X, solve_right_upper, dense_factor.hpp:226-244)
+//   mode 1: X <- X W^{-T}    (Y W^T = X, solve_right_upperT, dense_factor.hpp:247-264)
+// W upper triangular (n x n, ld ldw) with its 32x32 diagonal-block inverses D.  Rows
+// of X are independent right-hand sides, so one CTA owns a 32-row strip of X and
+// walks the 32-column blocks in dependency order:
+//   Y_b = (X_b - sum_a Y_a W_ab) D_b         (mode 0, a < b)
+//   Y_b = (X_b - sum_a Y_a W_ba^T) D_b^T     (mode 1, a > b)
+// Both products are m8n8k4 DMMA; the solved strip stays in shared memory (it is the
+// A operand of every later block), W fragments stream from L2 one 32-deep block at a
+// time with all 16 loads of a block in flight.  Requires n % 32 == 0 (the BASELINE
+// leaves are 128 / 256 / 512); other sizes use k_leaf_trsm.
+constexpr int TRM_RS = 32, TRM_LD = TRM_RS + 4, TRM_THREADS = 256;
+__global__ void __launch_bounds__(TRM_THREADS) k_leaf_trsm_rows(const TrsmItem* __restrict__ it) {
+    extern __shared__ double smem_trm[];
+    const TrsmItem T = it[blockIdx.y];
+    const int n = T.n;
+    const int r0 = blockIdx.x * TRM_RS;
+    if (r0 >= n) return;
+    double* sY = smem_trm;                       // n x RS: sY[col * LD + row]
+    double* sT = smem_trm + (size_t)n * TRM_LD;  // 32 x 32 staging of X_b - sum
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gi = lane >> 2, gk = lane & 3;
+    const int rt = warp & 3, ct0 = (warp >> 2) * 2;
+    const int row = rt * 8 + gi;                 // A-fragment / output row within the strip
+    const int nblk = n / 32;
+    const long long ldw = T.ldw, ldx = T.ldx;
+    double* X = T.X;
+    for (int bi = 0; bi < nblk; ++bi) {
+        const int b = T.mode == 0 ? bi : nblk - 1 - bi;
+        const int c0 = b * 32;
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+        const int a_lo = T.mode == 0 ? 0 : b + 1, a_hi = T.mode == 0 ? b : nblk;
+#pragma unroll 1
+        for (int a = a_lo; a < a_hi; ++a) {
+            const int k0 = a * 32;
+            double bf[8][2], af[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = k0 + 4 * u + gk;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int col = c0 + (ct0 + c) * 8 + gi;
+                    bf[u][c] = T.mode == 0 ? T.W[k + (long long)col * ldw] : T.W[col + (long long)k * ldw];
+                }
+                af[u] = sY[(size_t)k * TRM_LD + row];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) dmma_leaf(acc[c][0], acc[c][1], af[u], bf[u][c]);
+        }
+        // T = X_b - acc
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int col = (ct0 + c) * 8 + 2 * gk + v;
+                sT[col * TRM_LD + row] = X[(r0 + row) + (long long)(c0 + col) * ldx] - acc[c][v];
+            }
+        __syncthreads();
+        // Y_b = T D_b (mode 0) or T D_b^T (mode 1)
+        const double* D = T.D + (long long)b * 1024;
+        double y[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = 4 * u + gk;
+            const double a = sT[k * TRM_LD + row];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int col = (ct0 + c) * 8 + gi;
+                const double d = T.mode == 0 ? D[k + 32 * col] : D[col + 32 * k];
+                dmma_leaf(y[c][0], y[c][1], a, d);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int col = (ct0 + c) * 8 + 2 * gk + v;
+                sY[(size_t)(c0 + col) * TRM_LD + row] = y[c][v];
+                X[(r0 + row) + (long long)(c0 + col) * ldx] = y[c][v];
+            }
+        __syncthreads();
+    }
+}
+static size_t trm_smem(int n) { return sizeof(double) * ((size_t)n * TRM_LD + 32 * TRM_LD); }
+void launch_leaf_trsm_rows(const TrsmItem* d, int nitems, int maxn, cudaStream_t st) {
+    if (!nitems) return;
+    dim3 g((maxn + TRM_RS - 1) / TRM_RS, nitems);
+    k_leaf_trsm_rows<<<g, TRM_THREADS, trm_smem(maxn), st>>>(d);
+    SPG_LAUNCH_CHECK();
+}
+
 void leaf_init_attributes() {
+    SPG_CUDA(cudaFuncSetAttribute(k_leaf_trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)trm_smem(TRM_NMAX)));
     SPG_CUDA(cudaFuncSetAttribute(k_leaf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(double) * TR_NMAX * TR_TC)));
     SPG_CUDA(cudaFuncSetAttribute(k_leaf_chol2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
