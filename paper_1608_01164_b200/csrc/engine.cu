@@ -829,7 +829,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     if (tree_.leaf(x)) {
         if (chol_deferred_ && last_leaf_ev_[x] >= 0) wait(p, last_leaf_ev_[x]);
         const int s = tree_.size[x];
-        std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s, W.leaf_dinv(x)}};
+        std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s, W.leaf_dinv(x), nullptr, 1}};   // W memset above
         const CholItem* d = arena_->push(ci);
         unsigned* status = sc_.status;
         push_timed(p, PC_LEAF, [d, status, s](cudaStream_t st) { launch_leaf_cholesky(d, 1, status, st, s); });

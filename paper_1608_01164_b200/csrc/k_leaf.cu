@@ -651,6 +651,342 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
     if (tid == 0 && sFail) atomicOr(status, ST_NPD);
 }
 
+// Leaf Cholesky v4 (n % 32 == 0, n <= C4_NMAX): left-looking 32-column panels with a
+// one-panel lookahead, arranged so that only the 32-step diagonal sweep and two
+// 32-row DMMA products stay on the critical path.  Iteration J (three rotating panel
+// buffers, prv = J-32, cur = J, nxt = J+32; a panel holds rows J.. of its columns):
+//   (a) warps 0-3: cur[0:32] -= L[J:J+32, J-32:J] L[J:J+32, J-32:J]^T
+//   (b) warp 0: factors the diagonal block, rows in registers, in two 16-column halves
+//               (the half-to-half update is a 16x16x16 DMMA product); the next pivot
+//               is formed from the pivot row's own update before each column broadcast;
+//       warp 1: L11^{-1} column by column (lane k owns column k) from the columns warp 0
+//               publishes (one mbarrier per column) -> D = W_bb^{-1} = L11^{-T};
+//       warps 2..: (h1) prv[64:] <- prv[64:] D_{J-32}  (rest of the previous L21)
+//                  (h2) cur[32:] -= L[J+32:, J-32:J] L[J:J+32, J-32:J]^T
+//                  (h3) panel J-32 -> W (transposed)
+//                  (h4) nxt = M[J+32:, J+32:J+64] - L[J+32:, :J] L[J+32:J+64, :J]^T
+//                       (K < J-32 from W in L2, K in [J-32, J) from prv)
+//   (c) warps 0-3: cur[32:64] <- cur[32:64] D_J  (the rows the next (a) needs)
+// Same arithmetic contract as cholesky_upper (dense_factor.hpp:201-223): W = L^T.
+constexpr int C4_NMAX = 256, C4_THREADS = 384, C4_NW = C4_THREADS / 32, C4_HELP = C4_NW - 2;
+constexpr int C4_DP = 36;   // pitch of the D tiles (conflict-free m8n8k4 B-fragment reads)
+__host__ __device__ inline int c4_ldp(int n) { return ((n + 15) / 16) * 16 + 4; }
+static size_t chol4_smem(int n) {
+    return sizeof(double) * ((size_t)3 * c4_ldp(n) * 32 + 2 * 32 * C4_DP + 32 * 33 + 32 + 16 * 17);
+}
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void c4_helper_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(C4_HELP * 32) : "memory"); }
+
+// rows [r0, r1) of a panel (column block J0, relative rows) -> W(J0 + c, J0 + row)
+__device__ __forceinline__ void c4_copy_to_w(const double* pnl, int ldp, double* W, long long ldw, int J0, int r0,
+                                             int r1, int w0, int nw, int lane) {
+    for (int row = r0 + w0; row < r1; row += nw) {
+        const double v = pnl[row + lane * ldp];
+        if (row >= 32 || lane <= row) W[(J0 + lane) + (long long)(J0 + row) * ldw] = v;
+    }
+}
+
+// rows [8 rt0, 8 rt1) of X (32 columns, ld ldp): X <- X D  (in place), tiles strided by `step`
+__device__ __forceinline__ void c4_times_d(double* X, int ldp, const double* sD, int rt0, int rt1, int step, int gi,
+                                           int gk) {
+    for (int rt = rt0; rt < rt1; rt += step) {
+        double acc[4][2] = {};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = 4 * u + gk;
+            const double a = X[(rt * 8 + gi) + k * ldp];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dmma_leaf(acc[c][0], acc[c][1], a, sD[k * C4_DP + c * 8 + gi]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) X[(rt * 8 + gi) + (c * 8 + 2 * gk + v) * ldp] = acc[c][v];
+    }
+}
+
+// rows [8 rt0, 8 rt1) of Y -= A B^T with A rows at `pa` (same row index), B rows at `pb` (32 x 32), K = 32
+__device__ __forceinline__ void c4_sub_abt(double* Y, const double* pa, const double* pb, int ldp, int rt0, int rt1,
+                                           int step, int gi, int gk) {
+    for (int rt = rt0; rt < rt1; rt += step) {
+        double acc[4][2] = {};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = 4 * u + gk;
+            const double a = pa[(rt * 8 + gi) + k * ldp];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dmma_leaf(acc[c][0], acc[c][1], a, pb[(c * 8 + gi) + k * ldp]);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) Y[(rt * 8 + gi) + (c * 8 + 2 * gk + v) * ldp] -= acc[c][v];
+    }
+}
+
+__device__ int g_c4_flags = 0;   // diagnostics only (SPG_C4_FLAGS): 1 skip W copy, 2 skip lookahead, 4 skip h1/h2
+__global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __restrict__ it, unsigned* status) {
+    const int dflags = g_c4_flags;
+    extern __shared__ double sm4[];
+    const CholItem C = it[blockIdx.x];
+    const int n = C.n;
+    const int ldp = c4_ldp(n);
+    const int pstride = ldp * 32;   // panel buffers at sm4 + {0,1,2} * pstride (kept as shared-space arithmetic)
+    double* sDb = sm4 + (size_t)3 * ldp * 32;   // two D tiles: sD[k * C4_DP + c] = (L11^{-T})(k, c)
+    double* sLc = sDb + 2 * 32 * C4_DP;         // sLc[j * 33 + i] = L11(i, j), published by warp 0
+    double* sInvd = sLc + 32 * 33;              // 1 / L11(j, j)
+    double* sS = sInvd + 32;                    // 16 x 17 half-block update
+    __shared__ unsigned long long sBar[32];
+    __shared__ int sFail;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gi = lane >> 2, gk = lane & 3;
+    const long long ldw = C.ldw, ldm = C.ldm;
+    if (tid == 0) {
+        sFail = 0;
+        for (int j = 0; j < 32; ++j) mbar_init(&sBar[j], 32);   // all 32 lanes of warp 0 arrive
+    }
+    if (!C.w_zeroed)
+        for (int j = warp; j < n; j += C4_NW)   // W strictly lower = 0 (column j, rows > j)
+            for (int i = j + 1 + lane; i < n; i += 32) C.W[i + (long long)j * ldw] = 0.0;
+    for (int jj = warp; jj < 32; jj += C4_NW)   // panel 0 = M[:, 0:32]
+        for (int i = lane; i < n; i += 32) sm4[i + jj * ldp] = C.M[i + (long long)jj * ldm];
+    __syncthreads();
+    long long* tr = C.trace;
+#define C4_TRACE(k) if (tr && tid == 0) tr[(J / 32) * 8 + (k)] = clock64()
+    for (int J = 0; J < n; J += 32) {
+        const int pi = J / 32;
+        double* cur = sm4 + (pi % 3) * pstride;
+        double* prv = sm4 + ((pi + 2) % 3) * pstride;
+        double* nxt = sm4 + ((pi + 1) % 3) * pstride;
+        double* sD = sDb + (pi & 1) * 32 * C4_DP;
+        const double* sDp = sDb + ((pi + 1) & 1) * 32 * C4_DP;   // D of panel J-32
+        const int mr = n - J;
+        C4_TRACE(0);
+        if (J > 0) {   // (a) diagonal block rows
+            if (warp < 4) c4_sub_abt(cur, prv + 32, prv + 32, ldp, warp, warp + 1, 1, gi, gk);
+            __syncthreads();
+        }
+        C4_TRACE(1);
+        if (warp == 0) {
+            // (b0) diagonal block factor in two 16-column halves
+            double r[16], q[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                r[c] = c <= lane ? cur[lane + c * ldp] : 0.0;
+                q[c] = c + 16 <= lane ? cur[lane + (c + 16) * ldp] : 0.0;
+            }
+            bool fail = false;
+            double dnext = __shfl_sync(0xffffffffu, r[0], 0);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                double d = dnext;
+                if (!(d > 0.0)) { fail = true; d = 1.0; }
+                double ljj;
+                const double y = rsqrt_nr(d, ljj);
+                const double lij = lane == j ? ljj : r[j] * y;   // L(lane, j) for lane >= j
+                if (j < 15) dnext = __shfl_sync(0xffffffffu, r[j + 1] - lij * lij, j + 1);
+                r[j] = lij;
+                sLc[j * 33 + lane] = lij;
+                if (lane == 0) sInvd[j] = y;
+                __syncwarp();
+                mbar_arrive(&sBar[j]);
+#pragma unroll
+                for (int k = j + 1; k < 16; ++k) r[k] -= lij * sLc[j * 33 + k];
+            }
+            {   // rows/cols 16..31 -= L[16:32, 0:16] L[16:32, 0:16]^T  (DMMA, K = 16)
+                double acc[2][2][2] = {};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = 4 * u + gk;
+                    const double x0 = sLc[k * 33 + 16 + gi], x1 = sLc[k * 33 + 24 + gi];
+                    dmma_leaf(acc[0][0][0], acc[0][0][1], x0, x0);
+                    dmma_leaf(acc[0][1][0], acc[0][1][1], x0, x1);
+                    dmma_leaf(acc[1][0][0], acc[1][0][1], x1, x0);
+                    dmma_leaf(acc[1][1][0], acc[1][1][1], x1, x1);
+                }
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int v = 0; v < 2; ++v) sS[(a * 8 + gi) * 17 + c * 8 + 2 * gk + v] = acc[a][c][v];
+                __syncwarp();
+                if (lane >= 16)
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) q[c] -= sS[(lane - 16) * 17 + c];
+            }
+            dnext = __shfl_sync(0xffffffffu, q[0], 16);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+                const int j = jj + 16;
+                double d = dnext;
+                if (!(d > 0.0)) { fail = true; d = 1.0; }
+                double ljj;
+                const double y = rsqrt_nr(d, ljj);
+                const double lij = lane == j ? ljj : q[jj] * y;
+                if (jj < 15) dnext = __shfl_sync(0xffffffffu, q[jj + 1] - lij * lij, j + 1);
+                q[jj] = lij;
+                sLc[j * 33 + lane] = lij;
+                if (lane == 0) sInvd[j] = y;
+                __syncwarp();
+                mbar_arrive(&sBar[j]);
+#pragma unroll
+                for (int k = jj + 1; k < 16; ++k) q[k] -= lij * sLc[j * 33 + 16 + k];
+            }
+            if (fail) sFail = 1;
+            C4_TRACE(2);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                cur[lane + c * ldp] = c <= lane ? r[c] : 0.0;
+                cur[lane + (c + 16) * ldp] = c + 16 <= lane ? q[c] : 0.0;
+            }
+        } else if (warp == 1) {
+            // (b1) T = L11^{-1}: lane owns column `lane`, forward column sweep
+            double t[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) t[c] = c == lane ? 1.0 : 0.0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                mbar_wait(&sBar[j], pi & 1);
+                t[j] *= sInvd[j];
+#pragma unroll
+                for (int k = j + 1; k < 32; ++k) t[k] -= sLc[j * 33 + k] * t[j];
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) sD[lane * C4_DP + c] = t[c];   // D(lane, c) = T(c, lane)
+            if (C.D) {
+                double* D = C.D + (long long)pi * 1024;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) D[lane + 32 * c] = t[c];
+            }
+        } else {
+            const int hw = warp - 2;
+            if (J + 32 < n && !(dflags & 16)) {   // M[J+32:, J+32:J+64] -> nxt (cp.async, 16 B, coalesced)
+                const int J2 = J + 32, m2 = n - J2;
+                for (int idx = tid - 64; idx < m2 * 16; idx += C4_HELP * 32) {
+                    const int col = idx / (m2 / 2), i2 = idx % (m2 / 2);
+                    const unsigned dst = smem_addr(nxt + 2 * i2 + col * ldp);
+                    const double* src = C.M + (J2 + 2 * i2) + (long long)(J2 + col) * ldm;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+                }
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+            }
+            if (J > 0) {
+                // (h1) rest of the previous panel's L21: rows 64.. (relative to J-32)
+                if (!(dflags & 4)) c4_times_d(prv, ldp, sDp, 8 + hw, (mr + 32) / 8, C4_HELP, gi, gk);
+                c4_helper_sync();
+                // (h2) cur[32:] -= prv[64:] prv[32:64]^T
+                if (!(dflags & 4)) c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw, mr / 8, C4_HELP, gi, gk);
+                // (h3) panel J-32 -> W
+                if (!(dflags & 1)) c4_copy_to_w(prv, ldp, C.W, ldw, J - 32, 0, mr + 32, hw, C4_HELP, lane);
+            }
+            if (J + 32 < n && !(dflags & 16)) {   // the M copies into nxt have landed (all helpers)
+                asm volatile("cp.async.wait_all;\n" ::: "memory");
+                c4_helper_sync();
+            }
+            if (J + 32 < n && !(dflags & 2)) {   // (h4) lookahead of panel J+32
+                // each helper owns row tiles hw, hw + H, hw + 2H (<= 3; n <= 256) and loads every
+                // B fragment once for all of them (B = L[J+32:J+64, :J] is shared by all tiles)
+                const int J2 = J + 32, nrt2 = (n - J2) / 8;
+                const int nt = nrt2 > hw ? (nrt2 - hw + C4_HELP - 1) / C4_HELP : 0;
+                if (nt > 0) {
+                    double acc[3][4][2] = {};
+                    // K < J-32 from W: L(row, k) = W(k, row); lane gk takes k = k0 + 8u + 2gk + {0,1}
+                    // as one 16-byte L2 load (a fixed permutation of the k order)
+                    const double* pb = C.W + (long long)(J2 + gi) * ldw + 2 * gk;
+                    const double* pa = C.W + (long long)(J2 + hw * 8 + gi) * ldw + 2 * gk;
+                    const long long tstep = (long long)C4_HELP * 8 * ldw;
+                    for (int k0 = 0; k0 + 16 <= J - 32; k0 += 16) {
+                        double2 a[3][2], b[2][4];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) b[u][c] = __ldcg(reinterpret_cast<const double2*>(pb + (long long)c * 8 * ldw + k0 + 8 * u));
+#pragma unroll
+                            for (int t = 0; t < 3; ++t)
+                                a[t][u] = t < nt ? __ldcg(reinterpret_cast<const double2*>(pa + t * tstep + k0 + 8 * u)) : make_double2(0.0, 0.0);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+#pragma unroll
+                            for (int t = 0; t < 3; ++t)
+                                if (t < nt) {
+#pragma unroll
+                                    for (int c = 0; c < 4; ++c) dmma_leaf(acc[t][c][0], acc[t][c][1], a[t][u].x, b[u][c].x);
+#pragma unroll
+                                    for (int c = 0; c < 4; ++c) dmma_leaf(acc[t][c][0], acc[t][c][1], a[t][u].y, b[u][c].y);
+                                }
+                    }
+                    if (J > 0) {   // K in [J-32, J): panel J-32 (rows relative to J-32)
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int k = 4 * u + gk;
+                            double b[4];
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) b[c] = prv[(64 + c * 8 + gi) + k * ldp];
+#pragma unroll
+                            for (int t = 0; t < 3; ++t)
+                                if (t < nt) {
+                                    const double a = prv[(64 + (hw + t * C4_HELP) * 8 + gi) + k * ldp];
+#pragma unroll
+                                    for (int c = 0; c < 4; ++c) dmma_leaf(acc[t][c][0], acc[t][c][1], a, b[c]);
+                                }
+                        }
+                    }
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+                        if (t < nt)
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                                for (int v = 0; v < 2; ++v) {
+                                    const int row = (hw + t * C4_HELP) * 8 + gi, col = c * 8 + 2 * gk + v;
+                                    if (dflags & 16) nxt[row + col * ldp] = 1.0 - acc[t][c][v];
+                                    else nxt[row + col * ldp] -= acc[t][c][v];
+                                }
+                }
+            }
+        }
+        __syncthreads();
+        C4_TRACE(3);
+        // (c) the first 32 rows of L21 (what the next (a) reads)
+        if (tr && (dflags & 32) && warp == 0) {   // diagnostics: split phase (c) of warp 0
+            const double a0 = cur[32 + gi];
+            const long long t0 = clock64();
+            const double a1 = cur[32 + gi + ldp] + a0;
+            const long long t1 = clock64();
+            double x = 0.0, y = 0.0;
+            dmma_leaf(x, y, a1, a1);
+            dmma_leaf(x, y, a1, x);
+            const long long t2 = clock64() + (long long)(x != 12345.0);
+            if (lane == 0) { tr[pi * 8 + 6] = t1 - t0; tr[pi * 8 + 7] = t2 - t1; }
+            if (x == 1.2345) cur[0] = y;
+        }
+        if (warp < 4 && mr > 32) c4_times_d(cur, ldp, sD, 4 + warp, 5 + warp, 1, gi, gk);
+        C4_TRACE(4);
+        __syncthreads();
+        C4_TRACE(5);
+    }
+#undef C4_TRACE
+    c4_copy_to_w(sm4 + ((n / 32 - 1) % 3) * pstride, ldp, C.W, ldw, n - 32, 0, 32, warp, C4_NW, lane);   // last panel
+    if (tid == 0 && sFail) atomicOr(status, ST_NPD);
+}
+
 static size_t chol3_smem(int n) { return sizeof(double) * ((size_t)chol_ldp(n) * CH_NB + (size_t)32 * 480); }
 
 static size_t chol2_smem(int kc, int n) {
@@ -660,7 +996,12 @@ static size_t chol2_smem(int kc, int n) {
 
 void launch_leaf_cholesky(const CholItem* d, int nitems, unsigned* status, cudaStream_t st, int maxn) {
     if (!nitems) return;
-    if (maxn <= C3_NMAX && !std::getenv("SPG_CHOL_V2")) {
+    if (maxn <= C4_NMAX && maxn % 32 == 0 && !std::getenv("SPG_CHOL_V3") && !std::getenv("SPG_CHOL_V2")) {
+        static const int fl = std::getenv("SPG_C4_FLAGS") ? std::atoi(std::getenv("SPG_C4_FLAGS")) : -1;
+        static bool set = false;
+        if (fl >= 0 && !set) { SPG_CUDA(cudaMemcpyToSymbol(g_c4_flags, &fl, sizeof(int))); set = true; }
+        k_leaf_chol4<<<nitems, C4_THREADS, chol4_smem(maxn), st>>>(d, status);
+    } else if (maxn <= C3_NMAX && !std::getenv("SPG_CHOL_V2")) {
         k_leaf_chol3<<<nitems, CH_THREADS, chol3_smem(maxn), st>>>(d, status);
     } else if (maxn <= 256) {
         k_leaf_chol2<16><<<nitems, CH_THREADS, chol2_smem(16, maxn), st>>>(d, status);
@@ -805,6 +1146,7 @@ void launch_leaf_trsm_rows(const TrsmItem* d, int nitems, int maxn, cudaStream_t
 }
 
 void leaf_init_attributes() {
+    SPG_CUDA(cudaFuncSetAttribute(k_leaf_chol4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol4_smem(C4_NMAX)));
     SPG_CUDA(cudaFuncSetAttribute(k_leaf_trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)trm_smem(TRM_NMAX)));
     SPG_CUDA(cudaFuncSetAttribute(k_leaf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,6 +1,8 @@
 // Micro-benchmarks of single kernels on synthetic inputs (diagnostics only; used
 // by tests/gpu_micro.py to tune the latency-bound kernels of the critical path).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -106,7 +108,8 @@ int micro_kernel(int which, int n, int reps, double* out, int nout) {
     SPG_CUDA(cudaMalloc(&dI, sizeof(CholItem)));
     SPG_CUDA(cudaMemset(st, 0, sizeof(unsigned) * 16));
     k_micro_spd<<<64, 256>>>(M, n);
-    CholItem h{M, W, n, n, n, D, nullptr};
+    SPG_CUDA(cudaMemset(W, 0, sizeof(double) * n * n));
+    CholItem h{M, W, n, n, n, D, nullptr, 1};
     SPG_CUDA(cudaMemcpy(dI, &h, sizeof(h), cudaMemcpyHostToDevice));
     leaf_init_attributes();
     for (int r = 0; r < 3; ++r) launch_leaf_cholesky(dI, 1, st, 0, n);
@@ -129,6 +132,8 @@ int micro_kernel(int which, int n, int reps, double* out, int nout) {
     for (int p = 0; p < np; ++p) {
         for (int k = 1; k <= 5 && k < nout; ++k) out[k] += (double)(t[p * 8 + k] - t[p * 8 + k - 1]) / np;
         if (p + 1 < np && 6 < nout) out[6] += (double)(t[(p + 1) * 8] - t[p * 8 + 5]) / np;
+        if (std::getenv("SPG_C4_FLAGS") && (std::atoi(std::getenv("SPG_C4_FLAGS")) & 32))
+            std::printf("panel %d: lds %lld dmma2 %lld\n", p, t[p * 8 + 6], t[p * 8 + 7]);
     }
     unsigned hs = 0;
     SPG_CUDA(cudaMemcpy(&hs, st, sizeof(unsigned), cudaMemcpyDeviceToHost));

@@ -93,6 +93,7 @@ struct CholItem {
     int n, ldm, ldw;
     double* D;         // optional: inverses of W's 32x32 diagonal blocks (for trsm_tile_dinv)
     long long* trace;  // optional (micro-benchmarks): clock64 per panel phase, 8 per panel
+    int w_zeroed;      // 1: W's strictly lower triangle is already zero (the engine memsets W)
 };
 // inverses of the 32x32 diagonal blocks of upper-triangular leaves (W or R)
 struct DinvItem {
