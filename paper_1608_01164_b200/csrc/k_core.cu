@@ -19,6 +19,27 @@
 
 namespace spg {
 
+__device__ int g_core_hist_on = 0;            // diagnostics: histograms of k_in, r', sweeps, rank
+__device__ unsigned g_core_hist[4][128];
+__device__ __forceinline__ void core_hist(int k, int rp, int sweeps, int r) {
+    if (!g_core_hist_on) return;
+    atomicAdd(&g_core_hist[0][min(k, 127)], 1u);
+    atomicAdd(&g_core_hist[1][min(rp, 127)], 1u);
+    atomicAdd(&g_core_hist[2][min(sweeps, 127)], 1u);
+    atomicAdd(&g_core_hist[3][min(r, 127)], 1u);
+}
+void core_hist_ctl(int enable, double* out, int nout) {
+    if (enable >= 0) {
+        SPG_CUDA(cudaMemcpyToSymbol(g_core_hist_on, &enable, sizeof(int)));
+        static unsigned z[4][128] = {};
+        SPG_CUDA(cudaMemcpyToSymbol(g_core_hist, z, sizeof(z)));
+    }
+    if (out) {
+        unsigned h[4][128];
+        SPG_CUDA(cudaMemcpyFromSymbol(h, g_core_hist, sizeof(h)));
+        for (int i = 0; i < nout && i < 512; ++i) out[i] = h[i / 128][i % 128];
+    }
+}
 __device__ long long* g_core_trace = nullptr;   // micro-benchmarks: clock64 per phase of task 0
 void set_core_trace(long long* p) { SPG_CUDA(cudaMemcpyToSymbol(g_core_trace, &p, sizeof(p))); }
 #define CORE_TRACE(k) do { if (g_core_trace && blockIdx.x == 0 && threadIdx.x == 0) g_core_trace[k] = clock64(); } while (0)
@@ -374,6 +395,28 @@ __device__ __forceinline__ double sqrt_nr(double x) {
     const double r = x * y;
     return fma(0.5 * y, fma(-r, r, x), r);
 }
+// one-Newton-step variants: ~1e-13 relative, enough for Jacobi angle parameters
+// (the rotation itself is c = rsqrt(1 + t^2) to full accuracy, s = c t, so it stays
+// orthogonal whatever t is)
+__device__ __forceinline__ double rcp_nr1(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return fma(y, fma(-x, y, 1.0), y);
+}
+__device__ __forceinline__ double sqrt_nr1(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
+    const double r = x * y;
+    return fma(0.5 * y, fma(-r, r, x), r);
+}
+// reduction vote over the first `cnt` threads (named barrier 1)
+__device__ __forceinline__ int bar_or_1(int v, int cnt) {
+    int res;
+    asm volatile("{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.or.pred q, 1, %2, p;\n selp.u32 %0, 1, 0, q;\n}\n"
+                 : "=r"(res) : "r"(v), "r"(cnt) : "memory");
+    return res;
+}
 __device__ __forceinline__ void dmma_c(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
@@ -434,14 +477,17 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     for (int c = warp; c < k; c += 16) {
         const double a0 = sC[lane + c * L3], a1 = sC[lane + 32 + c * L3];
         const double s = csum(a0 * a0 + a1 * a1);
-        if (lane == 0) sCn2[0][c] = sqrt(s);
+        if (lane == 0) sCn2[0][c] = s;   // squared column norms (-1 = pivoted or absent)
     }
     __syncthreads();
     const double delta = sDelta3;
+    const double delta2 = delta * delta;
     CORE_TRACE(1);
     // ---- QRCP
-    // column norms double-buffered (read cur, write nxt; -1 = pivoted or absent) so
-    // that the redundant per-warp pivot search never races with the updates
+    // squared column norms double-buffered (read cur, write nxt) so that the redundant
+    // per-warp pivot search never races with the updates; after each reflector they
+    // are downdated (|a(j+1:)|^2 = |a(j:)|^2 - a_j^2, the reflector preserves the
+    // norm of rows j..) and recomputed exactly once cancellation has cost 8 digits
     int rp = 0, pprev = -1;
     for (int j = 0; j < k; ++j) {
         const double* cur = sCn2[j & 1];
@@ -460,36 +506,40 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
             const int op = __shfl_xor_sync(0xffffffffu, p, o);
             if (ob > best || (ob == best && op < p)) { best = ob; p = op; }
         }
-        if (best <= delta) break;
+        if (best <= delta2) break;
         const double* xp = sC + p * L3;
         const double x0 = (lane > j && lane < k) ? xp[lane] : 0.0;
         const double x1 = (lane + 32 > j && lane + 32 < k) ? xp[lane + 32] : 0.0;
-        const double s2 = csum(x0 * x0 + x1 * x1);
         const double alpha = xp[j];
-        double tau = 0.0, scal = 0.0, beta = alpha;
-        if (s2 > 0.0) {
-            const double nrm = sqrt(alpha * alpha + s2);
-            beta = alpha > 0.0 ? -nrm : nrm;
-            tau = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
-        }
-        const double v0 = x0 * scal, v1 = x1 * scal;
-        double a0[4], a1[4], aj[4], d[4];
+        double a0[4], a1[4], aj[4], cn[4];
         bool act[4];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < 4; ++m) {   // owned columns, loaded while the reflector is formed
             const int c = warp + 16 * m;
-            act[m] = c < k && c != p && cur[c] >= 0.0;
+            cn[m] = c < k ? cur[c] : -1.0;
+            act[m] = c < k && c != p && cn[m] >= 0.0;
             const double* col = sC + c * L3;
             a0[m] = (act[m] && lane > j && lane < k) ? col[lane] : 0.0;
             a1[m] = (act[m] && lane + 32 > j && lane + 32 < k) ? col[lane + 32] : 0.0;
             aj[m] = act[m] ? col[j] : 0.0;
-            d[m] = v0 * a0[m] + v1 * a1[m];
         }
+        const double s2 = csum(x0 * x0 + x1 * x1);
+        double tau = 0.0, scal = 0.0, beta = alpha;
+        if (s2 > 0.0) {
+            const double nrm = sqrt_nr(fma(alpha, alpha, s2));
+            beta = alpha > 0.0 ? -nrm : nrm;
+            tau = (beta - alpha) * rcp_nr(beta);
+            scal = rcp_nr(alpha - beta);
+        }
+        const double v0 = x0 * scal, v1 = x1 * scal;
+        double d[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) d[m] = v0 * a0[m] + v1 * a1[m];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
             for (int m = 0; m < 4; ++m) d[m] += __shfl_xor_sync(0xffffffffu, d[m], o);
+        bool redo = false;
         double ns[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
@@ -497,19 +547,24 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
             aj[m] -= w;
             a0[m] -= w * v0;
             a1[m] -= w * v1;
-            ns[m] = a0[m] * a0[m] + a1[m] * a1[m];
+            ns[m] = cn[m] - aj[m] * aj[m];
+            if (act[m] && !(ns[m] > 1e-8 * cn[m])) redo = true;   // warp-uniform
         }
+        if (redo) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+            for (int m = 0; m < 4; ++m) ns[m] = a0[m] * a0[m] + a1[m] * a1[m];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) ns[m] += __shfl_xor_sync(0xffffffffu, ns[m], o);
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) ns[m] += __shfl_xor_sync(0xffffffffu, ns[m], o);
+        }
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
             if (!act[m]) continue;
             double* col = sC + (warp + 16 * m) * L3;
             if (lane > j && lane < k) col[lane] = a0[m];
             if (lane + 32 > j && lane + 32 < k) col[lane + 32] = a1[m];
-            if (lane == 0) { col[j] = aj[m]; nxt[warp + 16 * m] = sqrt(ns[m]); }
+            if (lane == 0) { col[j] = aj[m]; nxt[warp + 16 * m] = ns[m]; }
         }
         if (tid == 0) {
             sPerm3[j] = p; sBeta[j] = beta; sTau[j] = tau; sScal[j] = scal;
@@ -553,10 +608,11 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     __syncthreads();
     CORE_TRACE(3);
     int nsweeps = 0;
-    if (rp > 1) {
+    const int nact = (npairs + 1) / 2;   // warps holding a pair (a half-warp per pair)
+    if (rp > 1 && warp < nact) {
         const int h = tid >> 4, hl = tid & 15;
         const unsigned hmask = 0xFFFFu << (lane & 16);
-        const double tol = 1e-15;
+        const double tol2 = 1e-30;   // |a_pq| > 1e-15 sqrt(a_pp a_qq), squared
         for (int sweep = 0; sweep < 60; ++sweep) {
             int any = 0;
             for (int r = 0; r < mrr; ++r) {
@@ -565,13 +621,15 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
                     const unsigned pq = sPairs[r * 32 + h];
                     const int p = pq & 255, q = pq >> 8;
                     if (q < rp) {
-                        double zp[4], zq[4];
+                        double zp[4], zq[4], jp[4], jq[4];
                         double app = 0.0, aqq = 0.0, apq = 0.0;
 #pragma unroll
                         for (int m = 0; m < 4; ++m) {
                             const int i = hl + 16 * m;
                             zp[m] = i < k ? sZ[i + p * L3] : 0.0;
                             zq[m] = i < k ? sZ[i + q * L3] : 0.0;
+                            jp[m] = i < rp ? sJ[i + p * L3] : 0.0;
+                            jq[m] = i < rp ? sJ[i + q * L3] : 0.0;
                             app += zp[m] * zp[m];
                             aqq += zq[m] * zq[m];
                             apq += zp[m] * zq[m];
@@ -582,13 +640,13 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
                             aqq += __shfl_xor_sync(hmask, aqq, o);
                             apq += __shfl_xor_sync(hmask, apq, o);
                         }
-                        if (app > 0.0 && aqq > 0.0 && fabs(apq) > tol * sqrt_nr(app * aqq)) {
+                        if (app > 0.0 && aqq > 0.0 && apq * apq > tol2 * (app * aqq)) {
                             rot = 1;
-                            const double zeta = (aqq - app) * rcp_nr(2.0 * apq);
+                            const double zeta = (aqq - app) * rcp_nr1(2.0 * apq);
                             const double az = fabs(zeta);
                             double tt;
-                            if (az > 1e100) tt = 0.5 * rcp_nr(zeta);
-                            else tt = copysign(1.0, zeta) * rcp_nr(az + sqrt_nr(fma(zeta, zeta, 1.0)));
+                            if (az > 1e100) tt = 0.5 * rcp_nr1(zeta);
+                            else tt = copysign(1.0, zeta) * rcp_nr1(az + sqrt_nr1(fma(zeta, zeta, 1.0)));
                             const double c = rsqrt_nr3(fma(tt, tt, 1.0));
                             const double s = c * tt;
 #pragma unroll
@@ -599,20 +657,20 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
                                     sZ[i + q * L3] = s * zp[m] + c * zq[m];
                                 }
                                 if (i < rp) {
-                                    const double x = sJ[i + p * L3], y = sJ[i + q * L3];
-                                    sJ[i + p * L3] = c * x - s * y;
-                                    sJ[i + q * L3] = s * x + c * y;
+                                    sJ[i + p * L3] = c * jp[m] - s * jq[m];
+                                    sJ[i + q * L3] = s * jp[m] + c * jq[m];
                                 }
                             }
                         }
                     }
                 }
-                any |= __syncthreads_or(rot);
+                any |= bar_or_1(rot, nact * 32);
             }
             ++nsweeps;
             if (!any) break;
         }
     }
+    __syncthreads();
     CORE_TRACE(4);
     if (g_core_trace && blockIdx.x == 0 && tid == 0) { g_core_trace[8] = nsweeps; g_core_trace[9] = rp; g_core_trace[10] = k; }
     // ---- singular values, order, rank
@@ -647,6 +705,7 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         }
         sR3 = r;
         hdr[0] = k; hdr[1] = r;
+        core_hist(k, rp, nsweeps, r);
         if (rp > 0 && !(sSig[sOrd3[0]] == sSig[sOrd3[0]])) atomicOr(status, ST_NONFINITE);
         double* ctr = reinterpret_cast<double*>(status + 16);
         atomicAdd(ctr, 8.0 * (double)(t.p + t.s) * (double)(k + r));
@@ -705,7 +764,7 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     CORE_TRACE(5);
 }
 
-__global__ void __launch_bounds__(TS_THREADS) k_core_any(const TTask* __restrict__ tasks, double* __restrict__ ws,
+__global__ void __launch_bounds__(TS_THREADS, 1) k_core_any(const TTask* __restrict__ tasks, double* __restrict__ ws,
                                                         double eps, unsigned* status, int use3) {
     extern __shared__ double smem[];
     const TTask& t = tasks[blockIdx.x];

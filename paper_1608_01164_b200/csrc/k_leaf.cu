@@ -763,8 +763,13 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
     if (!C.w_zeroed)
         for (int j = warp; j < n; j += C4_NW)   // W strictly lower = 0 (column j, rows > j)
             for (int i = j + 1 + lane; i < n; i += 32) C.W[i + (long long)j * ldw] = 0.0;
-    for (int jj = warp; jj < 32; jj += C4_NW)   // panel 0 = M[:, 0:32]
-        for (int i = lane; i < n; i += 32) sm4[i + jj * ldp] = C.M[i + (long long)jj * ldm];
+    for (int idx = tid; idx < n * 16; idx += C4_THREADS) {   // panel 0 = M[:, 0:32] (cp.async, 16 B)
+        const int col = idx / (n / 2), i2 = idx % (n / 2);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(sm4 + 2 * i2 + col * ldp)),
+                     "l"(C.M + 2 * i2 + (long long)col * ldm)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
     __syncthreads();
     long long* tr = C.trace;
 #define C4_TRACE(k) if (tr && tid == 0) tr[(J / 32) * 8 + (k)] = clock64()

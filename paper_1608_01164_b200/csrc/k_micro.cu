@@ -92,7 +92,68 @@ static int micro_trunc(int ngroups, int p, int reps, double* out, int nout) {
     return 0;
 }
 
+
+// latency calibration (cycles per dependent op, single warp unless noted):
+// out = [dfma, dmul, shfl f64, lds f64, rcp.approx f64, rsqrt.approx f64, rcp_nr (2 Newton),
+//        bar.sync 384 threads, syncwarp, dmma m8n8k4, IEEE div, IEEE sqrt]
+__global__ void k_lat(double* out, double seed) {
+    __shared__ double sh[64];
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 64) sh[threadIdx.x] = seed + threadIdx.x;
+    __syncthreads();
+    double x = seed + lane * 1e-3, y = 1.0 + 1e-9 * lane;
+    long long t0, t1;
+    const int N = 256;
+#define LAT(slot, body)                                                      \
+    t0 = clock64();                                                          \
+    for (int i = 0; i < N; ++i) { body; }                                    \
+    t1 = clock64();                                                          \
+    if (threadIdx.x == 0) out[slot] = (double)(t1 - t0) / N;
+    if (threadIdx.x < 32) {
+        LAT(0, x = fma(x, y, 1e-300))
+        LAT(1, x = x * y)
+        LAT(2, x = __shfl_xor_sync(0xffffffffu, x, 1) + 0.0)
+        int idx = lane;
+        LAT(3, { x = sh[idx]; idx = ((int)x) & 31; })
+        LAT(4, { double z; asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(x)); x = z; })
+        LAT(5, { double z; asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(x)); x = fabs(z) + 1.0; })
+        LAT(6, { double z; asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(z) : "d"(x)); double e = fma(-x, z, 1.0); z = fma(z, e, z); e = fma(-x, z, 1.0); x = fma(z, e, z) + 1.0; })
+    }
+    LAT(7, { __syncthreads(); x += 1.0; })
+    if (threadIdx.x < 32) {
+        LAT(8, { __syncwarp(); x += 1.0; })
+        double c0 = 0.0, c1 = 0.0;
+        LAT(9, { asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n" : "+d"(c0), "+d"(c1) : "d"(x), "d"(y)); })
+        x += c0 + c1;
+        LAT(10, x = 1.0 / (x + 2.0))
+        LAT(11, x = sqrt(x + 2.0))
+        int iv = lane;
+        LAT(12, { __syncwarp(); iv += 1; })
+        LAT(13, { asm volatile("bar.warp.sync 0xffffffff;" ::: "memory"); iv += 1; })
+        LAT(14, { sh[lane] = x; __syncwarp(); x = sh[(lane + 1) & 31] + 1.0; })
+        if (iv == 12345) out[15] = iv;
+    }
+#undef LAT
+    if (x == 12345.678) out[15] = x;
+}
+static int micro_lat(double* out, int nout) {
+    double* d;
+    SPG_CUDA(cudaMalloc(&d, sizeof(double) * 16));
+    SPG_CUDA(cudaMemset(d, 0, sizeof(double) * 16));
+    k_lat<<<1, 384>>>(d, 1.5);
+    SPG_CUDA(cudaGetLastError());
+    std::vector<double> h(16);
+    SPG_CUDA(cudaMemcpy(h.data(), d, sizeof(double) * 16, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < nout && i < 16; ++i) out[i] = h[i];
+    cudaFree(d);
+    return 0;
+}
+
+void core_hist_ctl(int enable, double* out, int nout);
 int micro_kernel(int which, int n, int reps, double* out, int nout) {
+    if (which == 2) { core_hist_ctl(n, nullptr, 0); return 0; }        // enable (n=1) / disable (n=0) + clear
+    if (which == 3) { core_hist_ctl(-1, out, nout); return 0; }       // read 4 x 128 bins
+    if (which == 4) return micro_lat(out, nout);                      // latency calibration
     if (which == 1 || which == 2) return micro_trunc(which, n, reps, out, nout);
     if (which != 0) return -1;
     double *M, *W, *D;
