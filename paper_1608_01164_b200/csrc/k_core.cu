@@ -377,6 +377,7 @@ __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double*
 constexpr int K3 = 64, L3 = 65;
 
 __device__ __forceinline__ double rcp_nr(double x) {
+    if (!(fabs(x) > 1e-290 && fabs(x) < 1e290)) return 1.0 / x;
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
     double e = fma(-x, y, 1.0);
@@ -391,6 +392,7 @@ __device__ __forceinline__ double rsqrt_nr3(double x) {
     return fma(0.5 * y, fma(-x * y, y, 1.0), y);
 }
 __device__ __forceinline__ double sqrt_nr(double x) {
+    if (!(x > 1e-290 && x < 1e290)) return sqrt(x);
     const double y = rsqrt_nr3(x);
     const double r = x * y;
     return fma(0.5 * y, fma(-r, r, x), r);

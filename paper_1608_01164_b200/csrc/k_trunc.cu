@@ -108,10 +108,10 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                     const double alpha = sR[j + j * KIN_MAX];
                     double tau = 0.0, scal = 0.0;
                     if (s2 > 0.0) {
-                        const double nrm = sqrt(alpha * alpha + s2);
+                        const double nrm = nr_sqrt(fma(alpha, alpha, s2));
                         const double beta = alpha > 0.0 ? -nrm : nrm;
-                        tau = (beta - alpha) / beta;
-                        scal = 1.0 / (alpha - beta);
+                        tau = (beta - alpha) * nr_rcp(beta);
+                        scal = nr_rcp(alpha - beta);
                         __syncwarp();
                         if (lane == 0) sR[j + j * KIN_MAX] = beta;
                     }
