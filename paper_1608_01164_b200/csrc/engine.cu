@@ -105,6 +105,8 @@ void DHodlr::alloc(const HTree& tree, Arena& arena) {
 }
 
 void DHodlr::release() {
+    if (tU) cudaFree(tU);
+    tU = tV = nullptr;
     if (dinv) cudaFree(dinv);
     dinv = nullptr;
     if (leaves) cudaFree(leaves);
@@ -163,6 +165,7 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     const size_t nsc = 32 + 32 + 256 + 32;
     SPG_CUDA(cudaMalloc(&scalar_mem_, nsc * sizeof(double)));
     SPG_CUDA(cudaMemset(scalar_mem_, 0, nsc * sizeof(double)));
+    SPG_CUDA(cudaMallocHost(&host_pinned_, 64 * sizeof(double)));
     sc_.scal = scalar_mem_;
     sc_.slots = scalar_mem_ + 32;
     sc_.sched = scalar_mem_ + 64;
@@ -177,6 +180,7 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
         panels_.push_back(p);
     }
     SPG_CUDA(cudaMalloc(&coef_, sizeof(double) * (size_t)KCAP * KCAP * 4 * tree_.nnodes()));
+    SPG_CUDA(cudaMalloc(&pcoef_, sizeof(double) * (size_t)KCAP * KCAP * tree_.nnodes()));
     SPG_CUDA(cudaMalloc(&iranks_, sizeof(int) * 4 * tree_.nnodes()));
     arena_->commit(st_);
 }
@@ -248,8 +252,10 @@ Engine::~Engine() {
     owned_.clear();
     for (double* p : panels_) cudaFree(p);
     if (coef_) cudaFree(coef_);
+    if (pcoef_) cudaFree(pcoef_);
     if (iranks_) cudaFree(iranks_);
     if (scalar_mem_) cudaFree(scalar_mem_);
+    if (host_pinned_) cudaFreeHost(host_pinned_);
     for (double* p : chol_panels_) cudaFree(p);
     for (auto& e : events_) cudaEventDestroy(e);
     arena_.reset();
@@ -459,8 +465,20 @@ void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs) {
     }
 }
 
+static const bool g_psolve_off = std::getenv("SPG_PSOLVE_OFF") != nullptr;
+
 void Engine::hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items) {
     if (items.empty()) return;
+    if (W.tready && !g_psolve_off) {   // subtrees of >= 4 leaves: the subtree-parallel form
+        std::vector<HSolveItem> big, small;
+        for (const auto& it : items) {
+            const int dep = tree_.depth - tree_.level[it.root];   // levels below the root
+            (dep >= 2 ? big : small).push_back(it);
+        }
+        if (!big.empty()) psolve(p, W, big);
+        if (small.empty()) return;
+        items.swap(small);
+    }
     std::vector<int2> ctas;
     for (size_t i = 0; i < items.size(); ++i)
         for (int t = 0; t < (KCAP + hsolve_tile_cols() - 1) / hsolve_tile_cols(); ++t) ctas.push_back(make_int2((int)i, t));
@@ -471,6 +489,90 @@ void Engine::hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items) {
     const DevHodlrView wv = W.view();
     unsigned* status = sc_.status;
     push_timed(p, PC_HSOLVE, [dt, wv, d, dc, nc, status](cudaStream_t st) { launch_hsolve(dt, wv, d, dc, nc, status, st); });
+}
+
+// Subtree-parallel triangular solve (solve_WT_rec / solve_W_rec, hodlr.hpp:456-521).
+// For W_sub = [W11, U V^T; 0, W22]:
+//   forward  (W^T x = b): x1 = W11^{-T} b1,  x2 = W22^{-T} b2 - tV (U^T x1),  tV = W22^{-T} V
+//   backward (W x = b):   x2 = W22^{-1} b2,  x1 = W11^{-1} b1 - tU (V^T x2),  tU = W11^{-1} U
+// so every leaf is solved at once and the couplings are applied bottom-up, one batched
+// pair of GEMMs per level (G = P_in^T X_in, X_out -= tP G), instead of walking the
+// leaves in order.  Same result as the sequential recursion up to rounding.
+void Engine::psolve(Plan& p, const DHodlr& W, const std::vector<HSolveItem>& items) {
+    const int n = tree_.n;
+    std::vector<TrsmItem> ti;
+    std::vector<std::vector<GemmItem>> g1(tree_.depth + 1), g2(tree_.depth + 1);
+    std::vector<std::vector<int3>> c1(tree_.depth + 1), c2(tree_.depth + 1);
+    for (const auto& it : items) {
+        std::vector<int> in, lv;
+        tree_.subtree(it.root, in, lv);
+        const int base = tree_.begin[it.root];
+        for (int f : lv) {
+            const int s = tree_.size[f];
+            ti.push_back(TrsmItem{W.leaf(f), it.X + (tree_.begin[f] - base), s, s, it.ldx, it.ncp, it.nc,
+                                  it.backward ? 1 : 0, 0, W.leaf_dinv(f)});
+        }
+        for (int y : in) {
+            const int l = tree_.left[y], r = tree_.right[y], t = tree_.level[y];
+            const int s1 = tree_.size[l], s2 = tree_.size[r];
+            double* G = pcoef_ + (size_t)y * KCAP * KCAP;
+            double* Xl = it.X + (tree_.begin[l] - base);
+            double* Xr = it.X + (tree_.begin[r] - base);
+            const int* ky = W.rup(y);
+            if (!it.backward) {   // G = U^T X_l ; X_r -= tV G
+                g1[t].push_back(gitem(W.upU(y), n, 1, Xl, it.ldx, 0, G, KCAP, 0, ky, it.nc, it.ncp, s1, nullptr, 1.0, 0.0));
+                c1[t].push_back(make_int3(KCAP, KCAP, s1));
+                g2[t].push_back(gitem(W.tslabV(t) + tree_.begin[r], n, 0, G, KCAP, 0, Xr, it.ldx, s2, nullptr, it.nc,
+                                      it.ncp, 0, ky, -1.0, 1.0));
+                c2[t].push_back(make_int3(s2, KCAP, KCAP));
+            } else {              // G = V^T X_r ; X_l -= tU G
+                g1[t].push_back(gitem(W.upV(y), n, 1, Xr, it.ldx, 0, G, KCAP, 0, ky, it.nc, it.ncp, s2, nullptr, 1.0, 0.0));
+                c1[t].push_back(make_int3(KCAP, KCAP, s2));
+                g2[t].push_back(gitem(W.tslabU(t) + tree_.begin[l], n, 0, G, KCAP, 0, Xl, it.ldx, s1, nullptr, it.nc,
+                                      it.ncp, 0, ky, -1.0, 1.0));
+                c2[t].push_back(make_int3(s1, KCAP, KCAP));
+            }
+        }
+    }
+    leaf_trsm_batch(p, ti, {});
+    for (int t = tree_.depth; t >= 0; --t) {   // deepest couplings first
+        if (g1[t].empty()) continue;
+        gemm(p, g1[t], c1[t]);
+        gemm(p, g2[t], c2[t]);
+    }
+}
+
+// tV_t[rows r(y)] = W_{r(y)}^{-T} V_y and tU_t[rows l(y)] = W_{l(y)}^{-1} U_y for every
+// internal node y, bottom-up (a level's solves use the bases of the levels below).
+void Engine::op_solve_prep(Plan& p, DHodlr& W) {
+    if (g_psolve_off) return;
+    const int n = tree_.n;
+    if (!W.tU) {
+        SPG_CUDA(cudaMalloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
+        W.tV = W.tU + W.slab_doubles;
+    }
+    W.tready = false;
+    for (int t = tree_.depth - 1; t >= 0; --t) {
+        const auto& ys = tree_.internal_at[t];
+        std::vector<CopyItem> cp;
+        std::vector<HSolveItem> hs;
+        int maxm = 0;
+        for (int y : ys) {
+            const int l = tree_.left[y], r = tree_.right[y];
+            const int s1 = tree_.size[l], s2 = tree_.size[r];
+            maxm = std::max(maxm, std::max(s1, s2));
+            double* tv = W.tslabV(t) + tree_.begin[r];
+            double* tu = W.tslabU(t) + tree_.begin[l];
+            cp.push_back(CopyItem{W.upV(y), tv, s2, n, n, W.rup(y), 0, 1.0, nullptr});
+            cp.push_back(CopyItem{W.upU(y), tu, s1, n, n, W.rup(y), 0, 1.0, nullptr});
+            hs.push_back(HSolveItem{r, tv, n, W.rup(y), 0, 0});
+            hs.push_back(HSolveItem{l, tu, n, W.rup(y), 0, 1});
+        }
+        copy(p, cp, maxm, KCAP);
+        W.tready = true;    // the solves below only touch levels > t, already prepared
+        hsolve(p, W, hs);
+    }
+    W.tready = true;
 }
 
 void Engine::copy(Plan& p, std::vector<CopyItem> items, int maxm, int maxk) {
@@ -745,6 +847,7 @@ static const bool g_chol_serial = std::getenv("SPG_CHOL_SERIAL") != nullptr;
 
 void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work) {
     cur_op_ = 6;
+    W.tready = false;
     op_copy(p, M, work);
     const DHodlr* Wp = &W;
     push(p, [Wp](cudaStream_t st) { Wp->zero(st); });
@@ -877,20 +980,27 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
 // leaf is a multiple of 32 (diagonal-block inverses present), else the generic one
 void Engine::leaf_trsm_batch(Plan& p, const std::vector<TrsmItem>& ti, const std::vector<int2>& ct) {
     bool rows = !std::getenv("SPG_TRSM_V1");
-    int maxn = 0;
+    int maxn = 0, maxrhs = 0;
     for (const auto& t : ti) {
-        rows = rows && t.D && t.rhs_t && t.n % 32 == 0 && t.n <= TRM_NMAX && !t.ncp && t.nc == t.n;
+        maxrhs = std::max(maxrhs, t.ncp ? KCAP : t.nc);
+        rows = rows && t.D && t.n % 32 == 0 && t.n <= TRM_NMAX;
         maxn = std::max(maxn, t.n);
     }
     const TrsmItem* d = arena_->push(ti);
     const int ni = (int)ti.size();
     unsigned* status = sc_.status;
     if (rows) {
-        push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm_rows(d, ni, maxn, st); });
+        push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm_rows(d, ni, maxn, maxrhs, st); });
         return;
     }
-    const int2* dc = arena_->push(ct);
-    const int nc = (int)ct.size();
+    std::vector<int2> ctl = ct;
+    if (ctl.empty())
+        for (size_t i = 0; i < ti.size(); ++i) {
+            const int nr = ti[i].ncp ? KCAP : ti[i].nc;
+            for (int c = 0; c < (nr + 15) / 16; ++c) ctl.push_back(make_int2((int)i, c));
+        }
+    const int2* dc = arena_->push(ctl);
+    const int nc = (int)ctl.size();
     push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_trsm(d, dc, nc, status, st); });
 }
 

@@ -85,6 +85,13 @@ struct DHodlr {
     double* V = nullptr;
     int* rank = nullptr;
     double* dinv = nullptr;                 // diagonal-block inverses (used when this is a triangular factor)
+    // triangular factors only: per node y the solved coupling bases (see Engine::op_solve_prep)
+    //   tV_t[rows r(y)] = W_{r(y)}^{-T} V_y   and   tU_t[rows l(y)] = W_{l(y)}^{-1} U_y
+    double* tU = nullptr;
+    double* tV = nullptr;
+    bool tready = false;                    // plan-build-time flag: tU / tV are current
+    double* tslabU(int lev) const { return tU + (size_t)lev * KCAP * t->n; }
+    double* tslabV(int lev) const { return tV + (size_t)lev * KCAP * t->n; }
     long long* d_dinv_off = nullptr;
     std::vector<long long> dinv_off;
     size_t leaf_doubles = 0, slab_doubles = 0;
@@ -156,6 +163,9 @@ public:
     struct Cascade { int root; const double* QU; const double* QV; const int* qrank; double s; };
     void cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs);
     void hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items);
+    // the same solves, subtree-parallel: all leaves at once, then one batched low-rank
+    // correction per tree level with the solved coupling bases (needs op_solve_prep(W))
+    void psolve(Plan& p, const DHodlr& W, const std::vector<HSolveItem>& items);
     void copy(Plan& p, std::vector<CopyItem> items, int maxm, int maxk);
     void leaf_trsm_batch(Plan& p, const std::vector<TrsmItem>& ti, const std::vector<int2>& ct);
 
@@ -167,6 +177,8 @@ public:
     void op_copy(Plan& p, const DHodlr& src, DHodlr& dst);
     // inverses of the 32x32 diagonal blocks of every leaf of an upper-triangular factor
     void op_leaf_dinv(Plan& p, DHodlr& W);
+    // solved coupling bases tU / tV of a finished upper-triangular factor (bottom-up)
+    void op_solve_prep(Plan& p, DHodlr& W);
     void op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C);
     void op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work);
     void op_solve_upper_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work);
@@ -208,8 +220,13 @@ private:
     DevTree dtree_{};
     Scalars sc_{};
     double* scalar_mem_ = nullptr;
+    double* host_pinned_ = nullptr;   // page-locked 64 doubles for asynchronous scalar read-back
+public:
+    double* host_pinned() const { return host_pinned_; }
+private:
     std::vector<double*> panels_;
     double* coef_ = nullptr;    // per-node coefficient blocks (KCAP x KCAP)
+    double* pcoef_ = nullptr;   // per-node psolve coupling products (KCAP x KCAP)
     int* iranks_ = nullptr;     // scratch ranks (4 * nnodes)
     std::vector<std::unique_ptr<DHodlr>> owned_;
     int cur_op_ = 0;

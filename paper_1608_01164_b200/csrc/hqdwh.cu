@@ -12,6 +12,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <random>
@@ -341,18 +342,29 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
             });
         });
         commit_run(p);
-        double sc[2];
-        SPG_CUDA(cudaMemcpyAsync(&count, S.count, sizeof(int), cudaMemcpyDeviceToHost, st));
-        SPG_CUDA(cudaMemcpyAsync(&status, S.status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        SPG_CUDA(cudaMemcpyAsync(sc, S.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
-        SPG_CUDA(cudaStreamSynchronize(st));
-        alpha = sc[0];
-        l0 = sc[1];
+    }
+    // The setup results (iteration count, alpha, l0, status) are read back only after
+    // the first iterate has been queued and the iteration graph has been built and
+    // instantiated, so that host work overlaps the device's setup and first iterate.
+    // (pinned destinations: a pageable D2H copy would block the host until the setup ends)
+    double* hp = E.host_pinned();
+    SPG_CUDA(cudaMemcpyAsync(hp, S.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+    SPG_CUDA(cudaMemcpyAsync(hp + 2, S.count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SPG_CUDA(cudaMemcpyAsync(hp + 3, S.status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    cudaEvent_t ev_setup = mkev();
+    SPG_CUDA(cudaEventRecord(ev_setup, st));
+    auto finish_setup = [&]() {
+        SPG_CUDA(cudaEventSynchronize(ev_setup));
+        alpha = hp[0];
+        l0 = hp[1];
+        std::memcpy(&count, hp + 2, sizeof(int));
+        std::memcpy(&status, hp + 3, sizeof(unsigned));
+        if (alpha == 0.0 || (status & ST_SINGULAR) || count < 0) SPG_CUDA(cudaStreamSynchronize(st));
         if (alpha == 0.0) throw StatusError(SPG_SINGULAR, "hqdwh: zero matrix");
         if (status & ST_SINGULAR) throw StatusError(SPG_SINGULAR, "BandedLu: zero pivot");
         if (count == -1) throw StatusError(SPG_INVALID_ARGUMENT, "qdwh: nonpositive lower bound l0");
         if (count < 0) throw StatusError(SPG_DOMAIN, "qdwh_params: l must lie in (0, 1]");
-    }
+    };
 
     // ---------------- X0 = from_banded(A / alpha)
     {
@@ -378,8 +390,9 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     };
     std::vector<cudaEvent_t> it_ev;
 
-    // ---------------- k = 0: QR-based first iterate
-    if (count >= 1) {
+    // ---------------- k = 0: QR-based first iterate (queued before the count is known;
+    // undone below when the schedule has no iteration at all)
+    {
         Plan p;
         cudaEvent_t e0 = mkev();
         it_ev.push_back(e0);
@@ -397,6 +410,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
                 launch_from_band(dt, Zp->view(), 0, b, d_bands, S.slots + 5, 1.0, s);   // sqrt(c0) A / alpha
             });
             E.op_leaf_dinv(p, *W);                         // diagonal-block inverses of R's leaves
+            E.op_solve_prep(p, *W);                        // solved coupling bases of HODLR(R)
             E.op_solve_upper_right(p, *Z, *W, *Y, *WK);    // Q1 = B R^{-1}
             E.op_solve_upperT_right(p, *Y, *W, *V, *WK);   // M  = Q1 R^{-T} = Q1 Q2^T
             E.op_symmetrize(p, *V);                        // q1q2t symmetrizes M (fast_qr.hpp:513)
@@ -408,7 +422,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     }
 
     // ---------------- k >= 1: Cholesky-based iterates (one plan, replayed; rebuilt per run in profile mode)
-    if (count >= 2) {
+    {
         auto build_iter = [&](Plan& p) {
             timed(p, PH_MUL, [&]() {
                 p.launches.push_back([=](cudaStream_t s) { launch_iter_params(S.sched, S.counter, S.slots, S.scal, s); });
@@ -416,7 +430,10 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
                 E.op_scale_shift(p, *Z, 1.0, S.slots + 0, 1.0);
             });
             timed(p, PH_CHOL, [&]() { E.op_cholesky(p, *Z, *W, *WK); });
-            timed(p, PH_SOLVE, [&]() { E.op_solve_upper_right(p, *X, *W, *Y, *WK); });
+            timed(p, PH_SOLVE, [&]() {
+                E.op_solve_prep(p, *W);
+                E.op_solve_upper_right(p, *X, *W, *Y, *WK);
+            });
             timed(p, PH_SOLVET, [&]() { E.op_solve_upperT_right(p, *Y, *W, *V, *WK); });
             timed(p, PH_AXPBY, [&]() {
                 E.op_axpby(p, 1.0, S.slots + 1, *X, 1.0, S.slots + 2, *V, *X);
@@ -432,25 +449,45 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         const bool use_graph = !E.profile() && !std::getenv("SPG_NO_GRAPH");
         Plan p;
         cudaGraphExec_t gexec = nullptr;
+        long long per_iter_launches = 0;
         if (use_graph) {
+            auto hclock = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+            const double h0 = hclock();
             phase_events = false;
             build_iter(p);
             phase_events = true;
+            const double h1 = hclock();
             cudaGraph_t g;
             const long long l0c = g_launches.load();
             SPG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
             p.run(st);
             SPG_CUDA(cudaStreamEndCapture(st, &g));
+            const double h2 = hclock();
             SPG_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+            const double h3 = hclock();
+            if (std::getenv("SPG_HOST_TIMING"))
+                std::fprintf(stderr, "host: build %.1f ms, capture %.1f ms, instantiate %.1f ms\n", h1 - h0, h2 - h1, h3 - h2);
             size_t nn = 0;
             SPG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
             SPG_CUDA(cudaGraphDestroy(g));
-            const long long per_iter = g_launches.load() - l0c;   // kernels captured once ...
-            g_launches += per_iter * (count - 2);                 // ... and replayed count-1 times
+            per_iter_launches = g_launches.load() - l0c;   // kernels captured once (replayed count-1 times)
             R->info.graph_nodes = (long long)nn;
             R->info.graph_used = 1;
         } else if (!E.profile()) {
             build_iter(p);
+        }
+        finish_setup();
+        if (gexec) g_launches += per_iter_launches * ((long long)count - 2);
+        if (count == 0) {   // no iteration: X = X0 = A / alpha (the queued first iterate is discarded)
+            Plan p0;
+            const DevTree dt = E.dtree();
+            const DHodlr* Xp = X.get();
+            p0.launches.push_back([=](cudaStream_t s) {
+                Xp->zero(s);
+                launch_from_band(dt, Xp->view(), 0, b, d_bands, S.scal + 2, 1.0, s);
+            });
+            commit_run(p0);
+            it_ev.clear();
         }
         for (int k = 1; k < count; ++k) {
             cur_run = k;

@@ -1069,21 +1069,27 @@ void launch_leaf_trsm(const TrsmItem* d, const int2* d_ctas, int nctas, unsigned
 // time with all 16 loads of a block in flight.  Requires n % 32 == 0 (the BASELINE
 // leaves are 128 / 256 / 512); other sizes use k_leaf_trsm.
 constexpr int TRM_RS = 32, TRM_LD = TRM_RS + 4, TRM_THREADS = 256;
+// X(rhs, w) addressing: rhs_t = 1 -> X[rhs + w ldx] (a leaf, rows are right-hand sides);
+// rhs_t = 0 -> X[w + rhs ldx] (a panel, columns are right-hand sides).  The number of
+// right-hand sides is *ncp (device) when given, else nc.
 __global__ void __launch_bounds__(TRM_THREADS) k_leaf_trsm_rows(const TrsmItem* __restrict__ it) {
     extern __shared__ double smem_trm[];
     const TrsmItem T = it[blockIdx.y];
     const int n = T.n;
+    const int nrhs = T.ncp ? *T.ncp : T.nc;
     const int r0 = blockIdx.x * TRM_RS;
-    if (r0 >= n) return;
+    if (r0 >= nrhs) return;
     double* sY = smem_trm;                       // n x RS: sY[col * LD + row]
     double* sT = smem_trm + (size_t)n * TRM_LD;  // 32 x 32 staging of X_b - sum
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gi = lane >> 2, gk = lane & 3;
     const int rt = warp & 3, ct0 = (warp >> 2) * 2;
     const int row = rt * 8 + gi;                 // A-fragment / output row within the strip
+    const bool rv = r0 + row < nrhs;
     const int nblk = n / 32;
-    const long long ldw = T.ldw, ldx = T.ldx;
-    double* X = T.X;
+    const long long ldw = T.ldw;
+    const long long rs = T.rhs_t ? 1 : T.ldx, ws = T.rhs_t ? T.ldx : 1;   // strides of (rhs, w)
+    double* X = T.X + (long long)(r0 + row) * rs;
     for (int bi = 0; bi < nblk; ++bi) {
         const int b = T.mode == 0 ? bi : nblk - 1 - bi;
         const int c0 = b * 32;
@@ -1114,7 +1120,7 @@ __global__ void __launch_bounds__(TRM_THREADS) k_leaf_trsm_rows(const TrsmItem* 
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
                 const int col = (ct0 + c) * 8 + 2 * gk + v;
-                sT[col * TRM_LD + row] = X[(r0 + row) + (long long)(c0 + col) * ldx] - acc[c][v];
+                sT[col * TRM_LD + row] = (rv ? X[(long long)(c0 + col) * ws] : 0.0) - acc[c][v];
             }
         __syncthreads();
         // Y_b = T D_b (mode 0) or T D_b^T (mode 1)
@@ -1137,15 +1143,15 @@ __global__ void __launch_bounds__(TRM_THREADS) k_leaf_trsm_rows(const TrsmItem* 
             for (int v = 0; v < 2; ++v) {
                 const int col = (ct0 + c) * 8 + 2 * gk + v;
                 sY[(size_t)(c0 + col) * TRM_LD + row] = y[c][v];
-                X[(r0 + row) + (long long)(c0 + col) * ldx] = y[c][v];
+                if (rv) X[(long long)(c0 + col) * ws] = y[c][v];
             }
         __syncthreads();
     }
 }
 static size_t trm_smem(int n) { return sizeof(double) * ((size_t)n * TRM_LD + 32 * TRM_LD); }
-void launch_leaf_trsm_rows(const TrsmItem* d, int nitems, int maxn, cudaStream_t st) {
+void launch_leaf_trsm_rows(const TrsmItem* d, int nitems, int maxn, int maxrhs, cudaStream_t st) {
     if (!nitems) return;
-    dim3 g((maxn + TRM_RS - 1) / TRM_RS, nitems);
+    dim3 g((maxrhs + TRM_RS - 1) / TRM_RS, nitems);
     k_leaf_trsm_rows<<<g, TRM_THREADS, trm_smem(maxn), st>>>(d);
     SPG_LAUNCH_CHECK();
 }

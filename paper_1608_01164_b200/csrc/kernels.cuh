@@ -127,7 +127,7 @@ void launch_leaf_trsm(const TrsmItem* d, const int2* d_ctas, int nctas, unsigned
 // leaves with n % 32 == 0, n <= TRM_NMAX, D present, X row-major RHS (rhs_t = 1) viewed as
 // X <- X W^{-1} (mode 0) / X W^{-T} (mode 1) on a column-major leaf; DMMA, one CTA per 32 rows
 constexpr int TRM_NMAX = 576;
-void launch_leaf_trsm_rows(const TrsmItem* d, int nitems, int maxn, cudaStream_t st);
+void launch_leaf_trsm_rows(const TrsmItem* d, int nitems, int maxn, int maxrhs, cudaStream_t st);
 
 // ------------------------------------------------------------ HODLR subtree solves
 struct DevTree {
