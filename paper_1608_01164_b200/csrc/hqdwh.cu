@@ -138,19 +138,44 @@ __global__ void k_flat_unpack(DevTree t, DevHodlrView H, const long long* off, c
     }
 }
 
-__global__ void k_trace(DevTree t, DevHodlrView H, double* out) {
-    // hodlr_trace (hodlr.hpp:658-663), fixed order: leaves in preorder, one thread
-    if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(256) k_trace(DevTree t, DevHodlrView H, double* out) {
+    // hodlr_trace (hodlr.hpp:658-663) in a fixed order: per leaf a fixed-shape warp sum
+    // of its diagonal, then the leaf sums in preorder by one thread (deterministic);
+    // leaves are taken in preorder chunks of 1024
+    __shared__ double sLeaf[1024];
+    __shared__ int sIds[1024];
+    __shared__ int sNl, sNext;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double tr = 0.0;
-    for (int id = 0; id < t.nnodes; ++id) {
-        if (t.left[id] >= 0) continue;
-        const int s = t.size[id];
-        const double* L = H.leaves + H.leaf_off[t.leaf_ord[id]];
-        double ts = 0.0;
-        for (int i = 0; i < s; ++i) ts += L[i + (long long)i * s];
-        tr += ts;
+    int next = 0;
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int c = 0, id = next;
+            for (; id < t.nnodes && c < 1024; ++id)
+                if (t.left[id] < 0) sIds[c++] = id;
+            sNl = c;
+            sNext = id;
+        }
+        __syncthreads();
+        const int nl = sNl;
+        next = sNext;
+        if (nl == 0) break;
+        for (int q = warp; q < nl; q += 8) {
+            const int id = sIds[q];
+            const int s = t.size[id];
+            const double* L = H.leaves + H.leaf_off[t.leaf_ord[id]];
+            double ts = 0.0;
+            for (int i = lane; i < s; i += 32) ts += L[i + (long long)i * s];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
+            if (lane == 0) sLeaf[q] = ts;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int q = 0; q < nl; ++q) tr += sLeaf[q];
     }
-    *out = tr;
+    if (threadIdx.x == 0) *out = tr;
 }
 
 int check_status(const unsigned* blk) {
@@ -261,6 +286,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     const long long blen = band_len(n, b);
     for (long long i = 0; i < blen; ++i)
         if (!std::isfinite(bands_host[i])) throw StatusError(SPG_INVALID_ARGUMENT, "hqdwh: nonfinite input");
+    const auto hc0 = std::chrono::steady_clock::now();
     auto R = std::make_unique<spg_result>();
     R->eng = std::make_unique<Engine>(n, n_min, eps);
     Engine& E = *R->eng;
@@ -271,6 +297,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     Scalars& S = E.sc();
 
     auto X = E.new_hodlr();
+    auto hms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hc0).count(); };
     auto Z = E.new_hodlr();
     auto W = E.new_hodlr();
     auto Y = E.new_hodlr();
@@ -289,6 +316,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     SPG_CUDA(cudaMalloc(&d_diag, sizeof(double) * 2 * 64));
     SPG_CUDA(cudaMalloc(&d_piv, sizeof(int) * n));
 
+    const double h_alloc = hms();
     // ---- timing instrumentation: per-run event tables, no host sync inside the loop
     std::vector<cudaEvent_t> evs;
     auto mkev = [&]() { cudaEvent_t e; SPG_CUDA(cudaEventCreate(&e)); evs.push_back(e); return e; };
@@ -518,6 +546,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     }
     SPG_CUDA(cudaStreamSynchronize(st));
     SPG_CUDA(cudaGetLastError());
+    if (std::getenv("SPG_HOST_TIMING")) std::fprintf(stderr, "host: engine+alloc %.1f ms, run_hqdwh to sync %.1f ms\n", h_alloc, hms());
     check_status_dev(S.status);
 
     // ---------------- report
@@ -593,12 +622,12 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         }
         I.max_rank = mx;
         I.memory_bytes = 8 * ent;
-        double* dtr;
-        SPG_CUDA(cudaMalloc(&dtr, sizeof(double)));
-        k_trace<<<1, 32, 0, st>>>(E.dtree(), P->view(), dtr);
-        SPG_CUDA(cudaMemcpyAsync(&I.trace, dtr, sizeof(double), cudaMemcpyDeviceToHost, st));
+        double* dtr = d_tmp;   // setup scratch, free by now
+        k_trace<<<1, 256, 0, st>>>(E.dtree(), P->view(), dtr);
+        SPG_LAUNCH_CHECK();
+        SPG_CUDA(cudaMemcpyAsync(hp + 8, dtr, sizeof(double), cudaMemcpyDeviceToHost, st));
         SPG_CUDA(cudaStreamSynchronize(st));
-        cudaFree(dtr);
+        I.trace = hp[8];
     }
     for (auto e : evs) cudaEventDestroy(e);
     cudaFree(d_bands); cudaFree(d_tmp); cudaFree(d_rdiag); cudaFree(d_diag); cudaFree(d_piv);
