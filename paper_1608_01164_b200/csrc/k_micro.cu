@@ -28,8 +28,8 @@ __global__ void k_micro_spd(double* M, int n) {
 // truncation of a synthetic p x k pair (k = 48 single group, or 2 x 28 groups),
 // singular values 10^(-14 j / k): out = [us/trunc, tsqr us, core us, apply us,
 // core cycles: C, QRCP, spill, Jacobi, finalize, sweeps, r', k, rank]
-static int micro_trunc(int ngroups, int p, int reps, double* out, int nout) {
-    const int k = ngroups == 1 ? 48 : 28;
+static int micro_trunc(int ngroups, int p, int reps, double* out, int nout, int kgrp = 0) {
+    const int k = kgrp > 0 ? kgrp : (ngroups == 1 ? 48 : 28);
     const int ktot = k * ngroups;
     std::vector<double> hu((size_t)p * ktot), hv((size_t)p * ktot);
     unsigned long long x = 88172645463325252ull;
@@ -154,7 +154,9 @@ int micro_kernel(int which, int n, int reps, double* out, int nout) {
     if (which == 2) { core_hist_ctl(n, nullptr, 0); return 0; }        // enable (n=1) / disable (n=0) + clear
     if (which == 3) { core_hist_ctl(-1, out, nout); return 0; }       // read 4 x 128 bins
     if (which == 4) return micro_lat(out, nout);                      // latency calibration
-    if (which == 1 || which == 2) return micro_trunc(which, n, reps, out, nout);
+    if (which == 1) return micro_trunc(1, n, reps, out, nout);
+    if (which == 6) return micro_trunc(2, n, reps, out, nout);
+    if (which >= 100) return micro_trunc(1, n, reps, out, nout, which - 100);   // one group of k = which - 100
     if (which != 0) return -1;
     double *M, *W, *D;
     long long* tr;

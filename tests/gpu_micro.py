@@ -12,11 +12,18 @@ for n in sizes:
         print(f"leaf_chol n={n}: {o[0]:.1f} us/launch; cycles/panel: tasks {o[1]:.0f} wait {o[2]:.0f} reduce {o[3]:.0f} "
               f"diag {o[4]:.0f} solve {o[5]:.0f} gap {o[6]:.0f}; status {int(o[7])}", flush=True)
     elif mode == "trunc":
-        for g in (1, 2):
-            o = S.micro_kernel(g, n, 20)
+        for g, which in ((1, 1), (2, 6)):
+            o = S.micro_kernel(which, n, 20)
             print(f"trunc p={n} groups={g}: {o[0]:.1f} us/trunc (tsqr {o[1]:.1f} core {o[2]:.1f} apply {o[3]:.1f}); "
                   f"core cycles C {o[4]:.0f} QRCP {o[5]:.0f} spill {o[6]:.0f} Jacobi {o[7]:.0f} fin {o[8]:.0f}; "
                   f"sweeps {o[9]:.0f} r' {o[10]:.0f} k {o[11]:.0f} rank {o[12]:.0f}", flush=True)
+if mode == "trunck":   # python tests/gpu_micro.py trunck P K..
+    p = sizes[0]
+    for k in sizes[1:]:
+        o = S.micro_kernel(100 + k, p, 20)
+        print(f"trunc p={p} k={k}: {o[0]:.1f} us/trunc (tsqr {o[1]:.1f} core {o[2]:.1f} apply {o[3]:.1f}); "
+              f"core cycles C {o[4]:.0f} QRCP {o[5]:.0f} spill {o[6]:.0f} Jacobi {o[7]:.0f} fin {o[8]:.0f}; "
+              f"sweeps {o[9]:.0f} r' {o[10]:.0f} k {o[11]:.0f} rank {o[12]:.0f}", flush=True)
 if mode == "lat":
     o = S.micro_kernel(4, 0, 0)
     names = ["dfma", "dmul", "shfl", "lds", "rcp.approx", "rsqrt.approx", "rcp_nr", "bar384", "syncwarp", "dmma",
