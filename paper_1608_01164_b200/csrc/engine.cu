@@ -148,12 +148,23 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
         ws_side_.push_back(std::make_unique<Workspace>(
             i + 1 == nside ? size_t(1) << 20 : std::max<size_t>((size_t)3 * n * KIN_MAX, size_t(8) << 20)));
     }
-    events_.resize((size_t)tree_.nnodes() * (nside + 2) + 4 * nside + 4);
+    ncasc_ = nside;
+    {   // the deferred W12 truncations of the Cholesky get a stream (and workspace) of their own
+        cudaStream_t s;
+        SPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        sides_.push_back(s);
+        ws_side_.push_back(std::make_unique<Workspace>(std::max<size_t>((size_t)3 * n * KIN_MAX, size_t(8) << 20)));
+        wtr_idx_ = (int)sides_.size() - 1;
+    }
+    ev_base2_ = tree_.nnodes() * (nside + 2) + 4 * nside + 8;
+    events_.resize((size_t)ev_base2_ + 2 * (size_t)tree_.nnodes());
     for (auto& e : events_) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (int t = 0; t < std::max(1, tree_.depth); ++t) {
         double* p;
         SPG_CUDA(cudaMalloc(&p, sizeof(double) * (size_t)n * KCAP));
         chol_panels_.push_back(p);
+        SPG_CUDA(cudaMalloc(&p, sizeof(double) * (size_t)n * KCAP));
+        xpanels_.push_back(p);
     }
     // device tree
     std::vector<int> tb = tree_.begin, ts = tree_.size, tl = tree_.left, tr = tree_.right, tv = tree_.level,
@@ -257,6 +268,7 @@ Engine::~Engine() {
     if (scalar_mem_) cudaFree(scalar_mem_);
     if (host_pinned_) cudaFreeHost(host_pinned_);
     for (double* p : chol_panels_) cudaFree(p);
+    for (double* p : xpanels_) cudaFree(p);
     for (auto& e : events_) cudaEventDestroy(e);
     arena_.reset();
     ws_.reset();
@@ -845,9 +857,11 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
 // SPG_CHOL_SERIAL=1 restores the single-stream schedule (A/B checks).
 static const bool g_chol_serial = std::getenv("SPG_CHOL_SERIAL") != nullptr;
 
-void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work) {
+void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool defer_trunc) {
     cur_op_ = 6;
     W.tready = false;
+    chol_defer_trunc_ = defer_trunc && !g_chol_serial;
+    wtr_last_ev_ = -1;
     op_copy(p, M, work);
     const DHodlr* Wp = &W;
     push(p, [Wp](cudaStream_t st) { Wp->zero(st); });
@@ -856,12 +870,12 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work) {
         chol_rec(p, 0, work, W);
         return;
     }
-    const int nn = tree_.nnodes(), nside = (int)sides_.size();
+    const int nn = tree_.nnodes(), nside = ncasc_, nall = (int)sides_.size();
     last_leaf_ev_.assign(nn, -1);
     last_block_ev_.assign(nn, -1);
     const int ev_fork = nn * (nside + 2), ev_join = ev_fork + 1;
     record(p, ev_fork);
-    for (int i = 0; i < nside; ++i) {
+    for (int i = 0; i < nall; ++i) {
         side_sel_ = i;
         wait(p, ev_fork);
     }
@@ -869,7 +883,8 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work) {
     chol_deferred_ = true;
     chol_rec(p, 0, work, W);
     chol_deferred_ = false;
-    for (int i = 0; i < nside; ++i) {
+    chol_defer_trunc_ = false;
+    for (int i = 0; i < nall; ++i) {
         side_sel_ = i;
         record(p, ev_join + i);
         side_sel_ = -1;
@@ -882,7 +897,7 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work) {
 // stream, every piece with its own completion event (event slots: ready(x) = x,
 // leaves(x) = nn + x, blocks(x, depth d) = nn * (2 + d) + x)
 void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU, const double* QV, const int* qrank) {
-    const int nn = tree_.nnodes(), nside = (int)sides_.size();
+    const int nn = tree_.nnodes(), nside = ncasc_;
     std::vector<int> in, lv;
     tree_.subtree(root, in, lv);
     std::vector<LowRankUpd> upd;
@@ -947,6 +962,38 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     const int bl = tree_.begin[l], br = tree_.begin[r], s1 = tree_.size[l], s2 = tree_.size[r];
     chol_rec(p, l, M, W);
     if (chol_deferred_ && last_block_ev_[x] >= 0) wait(p, last_block_ev_[x]);   // m12 complete
+    if (chol_defer_trunc_) {
+        // X = W11^{-T} m12.U (the solve needs W11's own W12 blocks: wait for their truncations)
+        double* X = xpanels_[t];
+        copy(p, {CopyItem{M.upU(x), X + bl, s1, n, n, M.rup(x), 0, 1.0, nullptr}}, s1, KCAP);
+        if (wtr_last_ev_ >= 0 && !tree_.leaf(l)) wait(p, wtr_last_ev_);
+        hsolve(p, W, {HSolveItem{l, X + bl, n, M.rup(x), 0, 0}});
+        const int evx = ev_base2_ + x, evw = ev_base2_ + tree_.nnodes() + x;
+        record(p, evx);
+        {   // W12 = trunc(X, m12.V) on its own stream (lowrank.hpp:67-86)
+            side_sel_ = wtr_idx_;
+            wait(p, evx);
+            TTask tk{};
+            tk.p = s1; tk.s = s2; tk.ng = 1; tk.skipg = -1;
+            tk.g[0] = TGroup{X + bl, M.upV(x), n, n, M.rup(x), 0, 1.0, nullptr};
+            tk.ou = W.upU(x); tk.ov = W.upV(x); tk.ldou = tk.ldov = n; tk.orank = W.rup(x); tk.tag = 600000 + x;
+            trunc(p, {tk});
+            record(p, evw);
+            side_sel_ = -1;
+            wtr_last_ev_ = evw;
+        }
+        // Schur M22 -= V (X^T X) V^T with the untruncated pair (X, m12.V)
+        double* G = coef_ + (size_t)(4 * x + 2) * KCAP * KCAP;
+        double* P1 = chol_panels_[t];
+        gemm(p, {gitem(X + bl, n, 1, X + bl, n, 0, G, KCAP, 0, M.rup(x), 0, M.rup(x), s1, nullptr, -1.0, 0.0)},
+             {make_int3(KCAP, KCAP, s1)});
+        gemm(p, {gitem(M.upV(x), n, 0, G, KCAP, 0, P1 + br, n, s2, nullptr, 0, M.rup(x), 0, M.rup(x), 1.0, 0.0)},
+             {make_int3(s2, KCAP, KCAP)});
+        record(p, x);
+        cascade_chol(p, M, x, r, P1, M.slabV(t), M.rup(x));
+        chol_rec(p, r, M, W);
+        return;
+    }
     // b12 = trunc({W11^{-T} m12.U, m12.V})
     double* P0 = panel(0);
     copy(p, {CopyItem{M.upU(x), P0 + bl, s1, n, n, M.rup(x), 0, 1.0, nullptr}}, s1, KCAP);

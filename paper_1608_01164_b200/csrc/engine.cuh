@@ -180,7 +180,9 @@ public:
     // solved coupling bases tU / tV of a finished upper-triangular factor (bottom-up)
     void op_solve_prep(Plan& p, DHodlr& W);
     void op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C);
-    void op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work);
+    // defer_trunc: W12 = trunc(W11^{-T} M12) is taken off the critical path (own stream)
+    // and the Schur complement uses the untruncated pair (differs at the eps level)
+    void op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool defer_trunc = false);
     void op_solve_upper_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work);
     void op_solve_upperT_right(Plan& p, const DHodlr& B, const DHodlr& W, DHodlr& Y, DHodlr& work);
 
@@ -213,6 +215,12 @@ private:
     std::vector<std::unique_ptr<Workspace>> ws_side_;   // one stack per side stream
     std::vector<double*> chol_panels_;  // per-depth Schur panels (a deferred cascade reads its own)
     bool chol_deferred_ = false;
+    bool chol_defer_trunc_ = false;
+    int ncasc_ = 0;                     // cascade side streams (depth streams + the leaf stream)
+    int wtr_idx_ = 0;                   // side stream of the deferred W12 truncations
+    int ev_base2_ = 0;                  // event slots: x-ready(x) = ev_base2_ + x, w12-done(x) = ev_base2_ + nn + x
+    int wtr_last_ev_ = -1;              // latest W12 truncation event (FIFO stream: covers all earlier ones)
+    std::vector<double*> xpanels_;      // per-depth untruncated W11^{-T} M12.U panels
     std::vector<int> last_leaf_ev_, last_block_ev_;   // latest side-stream event touching a leaf / block
     void cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU, const double* QV, const int* qrank);
     std::unique_ptr<Arena> arena_;

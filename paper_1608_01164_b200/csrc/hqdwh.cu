@@ -457,7 +457,9 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
                 E.op_multiply(p, *X, *X, *Z);
                 E.op_scale_shift(p, *Z, 1.0, S.slots + 0, 1.0);
             });
-            timed(p, PH_CHOL, [&]() { E.op_cholesky(p, *Z, *W, *WK); });
+            // deferred W12 truncation (SPG_CHOL_REFERENCE_ORDER=1: the reference's order)
+            static const bool ref_order = std::getenv("SPG_CHOL_REFERENCE_ORDER") != nullptr;
+            timed(p, PH_CHOL, [&]() { E.op_cholesky(p, *Z, *W, *WK, !ref_order); });
             timed(p, PH_SOLVE, [&]() {
                 E.op_solve_prep(p, *W);
                 E.op_solve_upper_right(p, *X, *W, *Y, *WK);
