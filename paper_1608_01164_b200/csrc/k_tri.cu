@@ -8,6 +8,8 @@
 // shared-memory chunks by cp.async several chunks ahead of the recurrence, so the
 // chain never waits on L2/HBM latency -- without this a lone thread streaming
 // through global memory stalls on every cache-line miss.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -170,7 +172,8 @@ __device__ __forceinline__ double wsum(double v) {
 }
 
 __global__ void __launch_bounds__(32) k_est_l0_tri(int n, const double* __restrict__ bands, const double* alpha_p,
-                                                  double* work, double* vecs, double* out, unsigned* status) {
+                                                  double* work, double* vecs, double* out, unsigned* status,
+                                                  int lu_only) {
     __shared__ __align__(16) double sbuf[PST * PNA * PCH];
     const int lane = threadIdx.x;
     const double alpha = *alpha_p;
@@ -218,6 +221,7 @@ __global__ void __launch_bounds__(32) k_est_l0_tri(int n, const double* __restri
         if (lane == 0) { atomicOr(status, ST_SINGULAR); out[0] = 0.0; }
         return;
     }
+    if (lu_only) return;   // k_hager_tri continues
     __syncwarp();
     // hager_norm1 (estimates.hpp:40-68)
     double* x = vecs;
@@ -258,6 +262,262 @@ __global__ void __launch_bounds__(32) k_est_l0_tri(int n, const double* __restri
         __syncwarp();
     }
     if (lane == 0) out[0] = n1 / (sqrt((double)n) * (n1 * est));
+}
+
+// ------------------------------------------------------------------------------
+// Block-parallel Hager iterations (hager_norm1, estimates.hpp:40-68) on the factor of
+// the sequential LU above.  Every triangular solve of BandedLu::solve / solve_transposed
+// (banded_lu.hpp) is a first- or second-order linear recurrence, so it runs as an affine
+// scan: each of the 1024 threads composes the step maps of its chunk, a block scan gives
+// every chunk its incoming state, and the chunk is replayed to write the outputs.  Same
+// recurrences (and the same result up to rounding) as the sequential sweep, in
+// O(n / 1024 + log 1024) dependent steps instead of O(n).
+constexpr int HG_T = 1024;
+
+struct Aff1 { double a, b; };                          // c -> a c + b
+struct Aff2 { double m00, m01, m10, m11, v0, v1; };    // s -> M s + v
+__device__ __forceinline__ Aff1 cmp1(const Aff1& g, const Aff1& f) { return {g.a * f.a, fma(g.a, f.b, g.b)}; }
+__device__ __forceinline__ Aff2 cmp2(const Aff2& g, const Aff2& f) {   // g o f
+    return {g.m00 * f.m00 + g.m01 * f.m10, g.m00 * f.m01 + g.m01 * f.m11,
+            g.m10 * f.m00 + g.m11 * f.m10, g.m10 * f.m01 + g.m11 * f.m11,
+            g.m00 * f.v0 + g.m01 * f.v1 + g.v0, g.m10 * f.v0 + g.m11 * f.v1 + g.v1};
+}
+__device__ __forceinline__ Aff1 shfl_up(const Aff1& f, int d) {
+    return {__shfl_up_sync(0xffffffffu, f.a, d), __shfl_up_sync(0xffffffffu, f.b, d)};
+}
+__device__ __forceinline__ Aff2 shfl_up(const Aff2& f, int d) {
+    return {__shfl_up_sync(0xffffffffu, f.m00, d), __shfl_up_sync(0xffffffffu, f.m01, d),
+            __shfl_up_sync(0xffffffffu, f.m10, d), __shfl_up_sync(0xffffffffu, f.m11, d),
+            __shfl_up_sync(0xffffffffu, f.v0, d), __shfl_up_sync(0xffffffffu, f.v1, d)};
+}
+__device__ __forceinline__ Aff1 ident(Aff1) { return {1.0, 0.0}; }
+__device__ __forceinline__ Aff2 ident(Aff2) { return {1.0, 0.0, 0.0, 1.0, 0.0, 0.0}; }
+
+// exclusive block scan of thread maps in thread order (thread t gets f_{t-1} o ... o f_0)
+template <class F>
+__device__ F block_exscan(F f, F* sw) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    F inc = f;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const F o = shfl_up(inc, d);
+        if (lane >= d) inc = cmp(inc, o);
+    }
+    if (lane == 31) sw[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        F w = sw[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const F o = shfl_up(w, d);
+            if (lane >= d) w = cmp(w, o);
+        }
+        sw[lane] = w;   // inclusive over warps
+    }
+    __syncthreads();
+    F ex = shfl_up(inc, 1);
+    if (lane == 0) ex = ident(f);
+    if (warp > 0) ex = cmp(ex, sw[warp - 1]);
+    __syncthreads();
+    return ex;
+}
+__device__ __forceinline__ Aff1 cmp(const Aff1& g, const Aff1& f) { return cmp1(g, f); }
+__device__ __forceinline__ Aff2 cmp(const Aff2& g, const Aff2& f) { return cmp2(g, f); }
+
+struct HgShared {
+    Aff2 w2[32];
+    Aff1 w1[32];
+    double red[32];
+    int ired[32];
+};
+
+__device__ double block_sum(double v, HgShared& sh) {   // fixed-shape (deterministic)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = wsum(v);
+    __syncthreads();
+    if (lane == 0) sh.red[warp] = v;
+    __syncthreads();
+    double t = sh.red[lane];
+    t = wsum(t);
+    return t;
+}
+
+// y = A^{-1} x: L pass (interchanges) into t1, U pass into y
+__device__ void hg_solve(const TriLU& F, int n, const double* x, double* t1, double* y, HgShared& sh) {
+    const int tid = threadIdx.x;
+    const int m = (n + HG_T - 1) / HG_T;
+    // L pass: steps k = 0..n-2 on c (c_0 = x[0]); out[k] = sw ? x[k+1] : c_k; out[n-1] = c_{n-1}
+    {
+        const int k0 = tid * m, k1 = min(n - 1, k0 + m);
+        Aff1 f{1.0, 0.0};
+        for (int k = k0; k < k1; ++k) {
+            const double lm = F.lm[k], xn = x[k + 1];
+            const Aff1 g = F.sw[k] != 0.0 ? Aff1{1.0, -lm * xn} : Aff1{-lm, xn};
+            f = cmp1(g, f);
+        }
+        const Aff1 ex = block_exscan(f, sh.w1);
+        double c = fma(ex.a, x[0], ex.b);
+        for (int k = k0; k < k1; ++k) {
+            const double lm = F.lm[k], xn = x[k + 1];
+            if (F.sw[k] != 0.0) { t1[k] = xn; c = c - lm * xn; }
+            else { t1[k] = c; c = xn - lm * c; }
+        }
+        if (k0 < k1 && k1 == n - 1) t1[n - 1] = c;
+        __syncthreads();
+    }
+    // U pass: q = 0..n-1, j = n-1-q; state (a, bq) = (t1[n-1], t1[n-2]);
+    //   y[j] = ri_j a;  a' = bq - u1_j ri_j a;  bq' = t1[j-2] - u2_j ri_j a
+    {
+        const int q0 = tid * m, q1 = min(n, q0 + m);
+        Aff2 f{1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+        for (int q = q0; q < q1; ++q) {
+            const int j = n - 1 - q;
+            const double ri = F.ri[j];
+            const Aff2 g{-F.u1[j] * ri, 1.0, -F.u2[j] * ri, 0.0, 0.0, j >= 2 ? t1[j - 2] : 0.0};
+            f = cmp2(g, f);
+        }
+        const Aff2 ex = block_exscan(f, sh.w2);
+        const double s0 = t1[n - 1], s1 = n >= 2 ? t1[n - 2] : 0.0;
+        double a = ex.m00 * s0 + ex.m01 * s1 + ex.v0;
+        double bq = ex.m10 * s0 + ex.m11 * s1 + ex.v1;
+        for (int q = q0; q < q1; ++q) {
+            const int j = n - 1 - q;
+            const double xj = a * F.ri[j];
+            y[j] = xj;
+            a = bq - F.u1[j] * xj;
+            bq = (j >= 2 ? t1[j - 2] : 0.0) - F.u2[j] * xj;
+        }
+        __syncthreads();
+    }
+}
+
+// y = A^{-T} z: U^T pass into t1, L^T pass (interchanges) into y
+__device__ void hg_solve_t(const TriLU& F, int n, const double* z, double* t1, double* y, HgShared& sh) {
+    const int tid = threadIdx.x;
+    const int m = (n + HG_T - 1) / HG_T;
+    // U^T pass: j = 0..n-1, state (xm1, xm2) = (0, 0): xj = ri (z_j - u1 xm1 - u2 xm2)
+    {
+        const int j0 = tid * m, j1 = min(n, j0 + m);
+        Aff2 f{1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+        for (int j = j0; j < j1; ++j) {
+            const double ri = F.ri[j];
+            const Aff2 g{-ri * F.u1[j], -ri * F.u2[j], 1.0, 0.0, ri * z[j], 0.0};
+            f = cmp2(g, f);
+        }
+        const Aff2 ex = block_exscan(f, sh.w2);
+        double xm1 = ex.v0, xm2 = ex.v1;   // initial state (0, 0)
+        for (int j = j0; j < j1; ++j) {
+            const double s = F.u2[j] * xm2 + F.u1[j] * xm1;
+            const double xj = (z[j] - s) * F.ri[j];
+            t1[j] = xj;
+            xm2 = xm1;
+            xm1 = xj;
+        }
+        __syncthreads();
+    }
+    // L^T pass: q = 0..n-2, k = n-2-q, c1 = t1[n-1]:
+    //   sw: y[k+1] = t1[k] - lm c1 (c1 kept);  else y[k+1] = c1, c1 = t1[k] - lm c1;  y[0] = c1
+    {
+        const int q0 = tid * m, q1 = min(n - 1, q0 + m);
+        Aff1 f{1.0, 0.0};
+        for (int q = q0; q < q1; ++q) {
+            const int k = n - 2 - q;
+            if (F.sw[k] == 0.0) f = cmp1(Aff1{-F.lm[k], t1[k]}, f);
+        }
+        const Aff1 ex = block_exscan(f, sh.w1);
+        double c1 = fma(ex.a, t1[n - 1], ex.b);
+        for (int q = q0; q < q1; ++q) {
+            const int k = n - 2 - q;
+            const double nv = t1[k] - F.lm[k] * c1;
+            if (F.sw[k] != 0.0) {
+                y[k + 1] = nv;
+            } else {
+                y[k + 1] = c1;
+                c1 = nv;
+            }
+        }
+        if (q0 < q1 && q1 == n - 1) y[0] = c1;
+        if (n == 1 && tid == 0) y[0] = t1[0];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(HG_T) k_hager_tri(int n, const double* __restrict__ bands, const double* alpha_p,
+                                                   const double* work, double* vecs, double* out,
+                                                   const unsigned* status) {
+    __shared__ HgShared sh;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (*status & ST_SINGULAR) return;   // the LU failed (out already 0)
+    const TriLU F{const_cast<double*>(work), const_cast<double*>(work) + n, const_cast<double*>(work) + 2 * (size_t)n,
+                  const_cast<double*>(work) + 3 * (size_t)n, const_cast<double*>(work) + 4 * (size_t)n,
+                  const_cast<double*>(work) + 5 * (size_t)n};
+    const double alpha = *alpha_p;
+    // norm1 (banded.hpp:94-106)
+    double mx = 0.0;
+    for (int i = tid; i < n; i += HG_T) {
+        double cs = fabs(bands[i]);
+        if (i + 1 < n) cs += fabs(bands[n + i]);
+        if (i >= 1) cs += fabs(bands[n + i - 1]);
+        mx = fmax(mx, cs);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) sh.red[warp] = mx;
+    __syncthreads();
+    mx = sh.red[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const double n1 = mx / alpha;
+    double* x = vecs;
+    double* t1 = vecs + n;
+    double* y = vecs + 2 * (size_t)n;
+    double* z = vecs + 3 * (size_t)n;
+    const int m = (n + HG_T - 1) / HG_T;
+    const int i0 = tid * m, i1 = min(n, i0 + m);
+    for (int i = i0; i < i1; ++i) x[i] = 1.0 / n;
+    __syncthreads();
+    double est = 0.0;
+    for (int it = 0; it < 5; ++it) {
+        hg_solve(F, n, x, t1, y, sh);
+        double e = 0.0;
+        for (int i = i0; i < i1; ++i) e += fabs(y[i]);
+        e = block_sum(e, sh);
+        if (it > 0 && e <= est) break;
+        est = e;
+        for (int i = i0; i < i1; ++i) z[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+        __syncthreads();
+        hg_solve_t(F, n, z, t1, y, sh);   // y <- A^{-T} z
+        double zmax = 0.0, ztx = 0.0;
+        int j = 0x7fffffff;
+        for (int i = i0; i < i1; ++i) {
+            const double a = fabs(y[i]);
+            if (a > zmax) { zmax = a; j = i; }
+            ztx += y[i] * x[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double oz = __shfl_xor_sync(0xffffffffu, zmax, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+            if (oz > zmax || (oz == zmax && oj < j)) { zmax = oz; j = oj; }
+        }
+        __syncthreads();
+        if (lane == 0) { sh.red[warp] = zmax; sh.ired[warp] = j; }
+        __syncthreads();
+        zmax = sh.red[lane];
+        j = sh.ired[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double oz = __shfl_xor_sync(0xffffffffu, zmax, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+            if (oz > zmax || (oz == zmax && oj < j)) { zmax = oz; j = oj; }
+        }
+        ztx = block_sum(ztx, sh);
+        if (j == 0x7fffffff) j = 0;
+        if (zmax <= ztx) break;
+        for (int i = i0; i < i1; ++i) x[i] = i == j ? 1.0 : 0.0;
+        __syncthreads();
+    }
+    if (tid == 0) out[0] = n1 / (sqrt((double)n) * (n1 * est));
 }
 
 __device__ __forceinline__ void givens_cs_t(double f, double g, double& c, double& s) {   // givens.hpp:27-36
@@ -322,8 +582,13 @@ __global__ void __launch_bounds__(32) k_givens_tri(int n, const double* __restri
 
 void launch_est_l0_tri(int n, const double* bands, const double* alpha, double* work, double* out_l0,
                        unsigned* status, cudaStream_t st) {
-    k_est_l0_tri<<<1, 32, 0, st>>>(n, bands, alpha, work, work + 6 * (size_t)n, out_l0, status);
+    static const bool seq = std::getenv("SPG_HAGER_SEQ") != nullptr;   // A/B: the sequential sweeps
+    k_est_l0_tri<<<1, 32, 0, st>>>(n, bands, alpha, work, work + 6 * (size_t)n, out_l0, status, seq ? 0 : 1);
     SPG_LAUNCH_CHECK();
+    if (!seq && n >= 2) {
+        k_hager_tri<<<1, HG_T, 0, st>>>(n, bands, alpha, work, work + 6 * (size_t)n, out_l0, status);
+        SPG_LAUNCH_CHECK();
+    }
 }
 
 void launch_givens_tri(int n, const double* bands, const double* slots, double* rdiag, cudaStream_t st) {
