@@ -81,6 +81,13 @@ typedef struct spg_info {
  * device-resident P and U.  Mirrors specproj::hqdwh (qdwh.hpp:196-241). */
 int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double delta, spg_result** out);
 
+/* Spectral slicing: the projectors of A - mu_i I for several shifts mu_i (tools/specproj.cpp
+ * --shift semantics, per shift), run concurrently (at most max_concurrent at a time, each
+ * on its own engine and stream: the projectors are latency-bound, so independent ones
+ * fill the GPU).  out[i] receives the result of shifts[i]; on error every out[i] is NULL
+ * and the first failing shift's status is returned. */
+int spg_hqdwh_shifts(int n, int b, const double* bands, int nshift, const double* shifts, int n_min, double eps,
+                     double delta, int max_concurrent, spg_result** out);
 int spg_result_info(const spg_result* r, spg_info* info);
 /* per-iteration diagnostics, `out` has room for info.iterations entries */
 int spg_result_diag(const spg_result* r, spg_iter_diag* out);

@@ -220,18 +220,45 @@ inline HodlrMatrix fetch(const spg_result* r, int which, std::shared_ptr<const P
 }
 }  // namespace detail
 
-// Drop-in for specproj::hqdwh (qdwh.hpp:196-241) on the B200.
-inline ProjectorResult hqdwh(const BandedSymmetric& A, int n_min, double eps, double delta) {
+namespace detail {
+inline std::vector<double> pack(const BandedSymmetric& A) {
     std::vector<double> packed;
     for (int d = 0; d <= A.b; ++d) packed.insert(packed.end(), A.bands[d].begin(), A.bands[d].end());
+    return packed;
+}
+inline ProjectorResult collect(spg_result* r, int n, int n_min);
+}  // namespace detail
+
+// Drop-in for specproj::hqdwh (qdwh.hpp:196-241) on the B200.
+inline ProjectorResult hqdwh(const BandedSymmetric& A, int n_min, double eps, double delta) {
+    std::vector<double> packed = detail::pack(A);
     spg_result* r = nullptr;
     detail::check(spg_hqdwh(A.n, A.b, packed.data(), n_min, eps, delta, &r));
     std::unique_ptr<spg_result, void (*)(spg_result*)> guard(r, spg_result_free);
+    return detail::collect(r, A.n, n_min);
+}
+
+// Spectral slicing: projectors of A - mu I for every shift (concurrent on the device).
+inline std::vector<ProjectorResult> hqdwh_shifts(const BandedSymmetric& A, const std::vector<double>& shifts,
+                                                 int n_min, double eps, double delta, int max_concurrent = 2) {
+    std::vector<double> packed = detail::pack(A);
+    std::vector<spg_result*> rs(shifts.size(), nullptr);
+    detail::check(spg_hqdwh_shifts(A.n, A.b, packed.data(), (int)shifts.size(), shifts.data(), n_min, eps, delta,
+                                   max_concurrent, rs.data()));
+    std::vector<ProjectorResult> out;
+    for (spg_result* r : rs) {
+        std::unique_ptr<spg_result, void (*)(spg_result*)> guard(r, spg_result_free);
+        out.push_back(detail::collect(r, A.n, n_min));
+    }
+    return out;
+}
+
+inline ProjectorResult detail::collect(spg_result* r, int n, int n_min) {
     spg_info info{};
     detail::check(spg_result_info(r, &info));
     std::vector<spg_iter_diag> dg(static_cast<size_t>(info.iterations > 0 ? info.iterations : 1));
     detail::check(spg_result_diag(r, dg.data()));
-    auto tree = make_tree(A.n, n_min);
+    auto tree = make_tree(n, n_min);
     ProjectorResult out;
     out.P = detail::fetch(r, 0, tree);
     out.U = detail::fetch(r, 1, tree);

@@ -106,6 +106,8 @@ class RefLib:
             "ref_result_diag": ([vp, _dp], None),
             "ref_result_hodlr": ([vp, C.c_int], vp),
             "ref_synth_banded": ([C.c_int, C.c_int, C.c_double, C.c_ulonglong, _dp], C.c_int),
+            "ref_write_sbm": ([C.c_int, C.c_int, _dp, C.c_char_p], C.c_int),
+            "ref_read_sbm": ([C.c_char_p, C.POINTER(C.c_int), C.c_void_p], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -151,6 +153,23 @@ class RefLib:
         Uo = np.zeros((p, k)); Vo = np.zeros((s, k))
         r = self.L.ref_truncate(p, s, k, _d(U), _d(V), eps, _d(Uo), _d(Vo))
         return Uo[:, :r].copy(), Vo[:, :r].copy()
+
+    def write_sbm(self, path, bands):
+        """banded.hpp:117-129 (the reference's writer)."""
+        n, b = len(bands[0]), len(bands) - 1
+        if self.L.ref_write_sbm(n, b, _d(pack_bands(bands)), path.encode()):
+            raise RefError(self.err())
+
+    def read_sbm(self, path):
+        """banded.hpp:138-154 (the reference's reader)."""
+        nb = np.zeros(2, dtype=np.int32)
+        if self.L.ref_read_sbm(path.encode(), nb.ctypes.data_as(C.POINTER(C.c_int)), None):
+            raise RefError(self.err())
+        n, b = int(nb[0]), int(nb[1])
+        out = np.zeros((b + 1) * n - b * (b + 1) // 2)
+        if self.L.ref_read_sbm(path.encode(), nb.ctypes.data_as(C.POINTER(C.c_int)), out.ctypes.data_as(C.c_void_p)):
+            raise RefError(self.err())
+        return unpack_bands(out, n, b)
 
     def synth_banded(self, n, b, gap, seed):
         """synth.hpp:106-137 with SpectrumSpec::uniform_two_sided(n, gap) (the reference tests' inputs)."""

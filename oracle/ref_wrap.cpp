@@ -252,6 +252,30 @@ void* ref_first_iterate_m(int n, int b, const double* bands_scaled, int n_min, d
 }
 
 // ---- test matrices (synth.hpp:106-137): the reference tests' spectra -------------
+// SBM text through the reference's own writer / reader (banded.hpp:115-154)
+int ref_write_sbm(int n, int b, const double* bands, const char* path) {
+    try {
+        BandedSymmetric A(n, b);
+        std::size_t off = 0;
+        for (int d = 0; d <= b; ++d)
+            for (int i = 0; i + d < n; ++i) A.bands[d][i] = bands[off++];
+        write_sbm(std::string(path), A);
+        return 0;
+    } catch (const std::exception& e) { return classify(e); }
+}
+int ref_read_sbm(const char* path, int* nb, double* bands) {   // bands may be null (header only)
+    try {
+        BandedSymmetric A = read_sbm(std::string(path));
+        nb[0] = A.n; nb[1] = A.b;
+        if (bands) {
+            std::size_t off = 0;
+            for (int d = 0; d <= A.b; ++d)
+                for (int i = 0; i + d < A.n; ++i) bands[off++] = A.bands[d][i];
+        }
+        return 0;
+    } catch (const std::exception& e) { return classify(e); }
+}
+
 int ref_synth_banded(int n, int b, double gap, unsigned long long seed, double* bands) {
     try {
         BandedSymmetric A = synth_banded(SpectrumSpec::uniform_two_sided(n, gap), b, seed);

@@ -100,7 +100,7 @@ ABI_SYMBOLS = (
     "spg_make_dimer_chain", "spg_make_random_banded", "spg_kcap", "spg_ctx_create", "spg_ctx_free",
     "spg_ctx_upload", "spg_ctx_flat_size", "spg_ctx_download", "spg_ctx_op", "spg_ctx_from_banded",
     "spg_truncate", "spg_set_profile", "spg_measure_dmma_tflops", "spg_micro_kernel", "spg_host_alloc",
-    "spg_host_free",
+    "spg_host_free", "spg_hqdwh_shifts",
 )
 
 
@@ -143,6 +143,8 @@ def load_library(path: str | None = None):
         "spg_micro_kernel": ([C.c_int, C.c_int, C.c_int, _dp, C.c_int], C.c_int),
         "spg_host_alloc": ([C.c_longlong, C.POINTER(vp)], C.c_int),
         "spg_host_free": ([vp], None),
+        "spg_hqdwh_shifts": ([C.c_int, C.c_int, _dp, C.c_int, _dp, C.c_int, C.c_double, C.c_double, C.c_int,
+                              C.POINTER(vp)], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -478,13 +480,76 @@ def hqdwh(A: BandedSymmetric, n_min: int, eps: float, delta: float = 1e-15, pack
             raise ValueError("hqdwh: nonfinite input")
         packed = A.packed()
     _raise(L.spg_hqdwh(A.n, A.b, _d(packed), n_min, eps, delta, C.byref(h)))
+    return _result_from_handle(h, A.n, n_min)
+
+
+def _result_from_handle(h, n, n_min) -> ProjectorResult:
+    L = load_library()
     info = _Info()
     _raise(L.spg_result_info(h, C.byref(info)))
     diag = (_Diag * max(info.iterations, 1))()
     _raise(L.spg_result_diag(h, diag))
     per = [IterationDiag(d.k, d.l, d.c, d.max_rank, d.memory_bytes, d.wall_ms) for d in diag[:info.iterations]]
     infod = {name: getattr(info, name) for name, _ in _Info._fields_}
-    return ProjectorResult(info.iterations, info.alpha, info.l0, per, infod, h, PartitionTree(A.n, n_min))
+    return ProjectorResult(info.iterations, info.alpha, info.l0, per, infod, h, PartitionTree(n, n_min))
+
+
+def hqdwh_shifts(A: BandedSymmetric, shifts, n_min: int, eps: float, delta: float = 1e-15,
+                 max_concurrent: int = 2) -> list:
+    """Spectral slicing (the CLI's --shift, tools/specproj.cpp:160-161, for several shifts):
+    one projector of A - mu I per shift, run concurrently on the device (spg_hqdwh_shifts)."""
+    if not A.all_finite():
+        raise ValueError("hqdwh: nonfinite input")
+    sh = np.ascontiguousarray(shifts, dtype=np.float64)
+    hs = (C.c_void_p * len(sh))()
+    _raise(load_library().spg_hqdwh_shifts(A.n, A.b, _d(A.packed()), len(sh), _d(sh), n_min, eps, delta,
+                                           max_concurrent, hs))
+    return [_result_from_handle(C.c_void_p(h), A.n, n_min) for h in hs]
+
+
+# ------------------------------------------------------------------ wire formats (banded.hpp:115-154)
+def write_sbm(path: str, A: BandedSymmetric):
+    """SBM text: "SBM <n> <b>", then one line per diagonal (%.17g, full round trip)."""
+    with open(path, "w") as f:
+        f.write(f"SBM {A.n} {A.b}\n")
+        for d in range(A.b + 1):
+            f.write(" ".join("%.17g" % v for v in A.bands[d]) + "\n")
+
+
+def read_sbm(path: str) -> BandedSymmetric:
+    with open(path) as f:
+        tok = f.read().split()
+    if len(tok) < 3 or tok[0] != "SBM":
+        raise ValueError("read_sbm: malformed header")
+    n, b = int(tok[1]), int(tok[2])
+    need = sum(n - d for d in range(b + 1))
+    if len(tok) - 3 < need:
+        raise ValueError("read_sbm: truncated data")
+    vals = np.array([float(t) for t in tok[3:3 + need]])
+    if not np.all(np.isfinite(vals)):
+        raise ValueError("read_sbm: nonfinite entry")
+    return BandedSymmetric.from_packed(n, b, vals)
+
+
+def run_report(file: str, A: BandedSymmetric, n_min: int, eps: float, delta: float, shift: float,
+               r: ProjectorResult, wall_ms: float, errors=None, gap=None, seed=None) -> dict:
+    """The JSON run report of tools/specproj.cpp:82-118 (same keys and order)."""
+    P = r.P
+    mr, mem = P.diagnostics()
+    return {
+        "input": {"file": file, "n": A.n, "b": A.b, "gap": gap, "seed": seed},
+        "params": {"n_min": n_min, "eps": eps, "delta": delta, "shift": shift, "alpha": r.alpha, "l0": r.l0},
+        "iterations": r.iterations,
+        "per_iteration": [{"k": d.k, "l": d.l, "c": d.c, "max_rank": d.max_rank, "memory_bytes": d.memory_bytes,
+                           "wall_ms": d.wall_ms} for d in r.per_iteration],
+        "errors": errors,
+        "totals": {"wall_ms": wall_ms, "memory_bytes": int(mem), "max_rank": int(mr), "trace_p": P.trace()},
+    }
+
+
+def cli_path() -> str:
+    """The GPU-backed CLI (tools/specproj.cpp subcommands), built next to the library."""
+    return os.path.join(os.path.dirname(_LIB_PATH), "specproj_b200")
 
 
 def set_profile(on: bool = True):

@@ -17,6 +17,7 @@
 #include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/specproj_b200.h"
@@ -708,6 +709,45 @@ int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double d
         ensure_device();
         *out = run_hqdwh(n, b, bands, n_min, eps, delta);
     });
+}
+
+int spg_hqdwh_shifts(int n, int b, const double* bands, int nshift, const double* shifts, int n_min, double eps,
+                     double delta, int max_concurrent, spg_result** out) {
+    if (nshift <= 0 || !shifts || !out) return guarded([]() { throw StatusError(SPG_INVALID_ARGUMENT, "spg_hqdwh_shifts: no shifts"); });
+    for (int i = 0; i < nshift; ++i) out[i] = nullptr;
+    const int rc0 = guarded([&]() { ensure_device(); });
+    if (rc0 != SPG_OK) return rc0;
+    const long long blen = band_len(n, b);
+    std::vector<int> st(nshift, SPG_OK);
+    std::vector<std::string> msg(nshift);
+    std::atomic<int> next{0};
+    auto worker = [&]() {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        for (int i = next++; i < nshift; i = next++) {
+            std::vector<double> sb(bands, bands + blen);
+            for (int j = 0; j < n; ++j) sb[j] -= shifts[i];   // A - mu I: the diagonal is band 0
+            st[i] = guarded([&]() { out[i] = run_hqdwh(n, b, sb.data(), n_min, eps, delta); });
+            if (st[i] != SPG_OK) msg[i] = spg_last_error();
+        }
+    };
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int nw = std::max(1, std::min(max_concurrent > 0 ? max_concurrent : 2, nshift));
+        std::vector<std::thread> th;
+        for (int w = 0; w < nw; ++w)
+            th.emplace_back([&, dev]() { cudaSetDevice(dev); worker(); });
+        for (auto& t : th) t.join();
+    }
+    for (int i = 0; i < nshift; ++i)
+        if (st[i] != SPG_OK) {
+            for (int j = 0; j < nshift; ++j) { spg_result_free(out[j]); out[j] = nullptr; }
+            const std::string m = "shift " + std::to_string(i) + ": " + msg[i];
+            const int code = st[i];
+            return guarded([&]() { throw StatusError(code, m); });
+        }
+    return SPG_OK;
 }
 
 int spg_result_info(const spg_result* r, spg_info* info) {
