@@ -67,9 +67,11 @@ void* Arena::push_raw(const void* src, size_t bytes) {
 
 void Arena::commit(cudaStream_t st) {
     if (off_ > committed_) {
+        // pageable source: the call returns once the bytes are staged, so the host buffer may
+        // be reused at once; stream order puts the copy ahead of the launches that read it.
+        // No synchronization here -- plan building keeps overlapping the device's work.
         SPG_CUDA(cudaMemcpyAsync(dev_ + committed_, host_.data() + committed_, off_ - committed_,
                                  cudaMemcpyHostToDevice, st));
-        SPG_CUDA(cudaStreamSynchronize(st));
         committed_ = off_;
     }
 }

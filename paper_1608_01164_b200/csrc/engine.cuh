@@ -43,6 +43,10 @@ public:
     void commit(cudaStream_t st);   // upload everything staged since the last commit
     size_t used() const { return off_; }
     void reset() { off_ = 0; committed_ = 0; }
+    // descriptors pushed after a mark can be dropped again once their launches are done
+    // (the descriptors of captured graphs stay below the mark)
+    size_t mark() const { return off_; }
+    void release(size_t m) { off_ = m; committed_ = std::min(committed_, m); }
 private:
     char* dev_ = nullptr;
     size_t cap_ = 0, off_ = 0, committed_ = 0;

@@ -203,11 +203,16 @@ enum Phase { PH_SETUP, PH_FIRST, PH_MUL, PH_CHOL, PH_SOLVE, PH_SOLVET, PH_AXPBY,
 
 }  // namespace
 
+struct HqdwhState;
+void release_state(std::unique_ptr<HqdwhState> s);
 struct spg_result {
-    std::unique_ptr<Engine> eng;
-    std::unique_ptr<DHodlr> X, P;
+    std::unique_ptr<HqdwhState> state;   // engine + HODLR matrices (P, X = U) + cached graphs
     spg_info info{};
     std::vector<spg_iter_diag> diag;
+    Engine& eng() const;
+    const DHodlr& X() const;
+    const DHodlr& P() const;
+    ~spg_result();
 };
 
 struct spg_ctx {
@@ -281,43 +286,219 @@ void check_tree(const HTree& t) {
         if (t.size[f] > 1024) throw StatusError(SPG_INVALID_ARGUMENT, "leaf size > 1024 unsupported (choose n_min <= 1024)");
 }
 
+}  // namespace
+
 // ------------------------------------------------------------------ the driver
+// Everything of a projector that does not depend on the input values: the engine, the
+// seven HODLR matrices, the setup scratch and -- outside profile mode -- the CUDA graphs
+// of the first iterate, of one Cholesky-based iterate and of the final P = (I - X)/2.
+// States are cached by shape (n, b, n_min, eps, delta) and reused by later calls once
+// the result that held them is freed (a plan cache, like cuFFT plans): a repeated call
+// allocates nothing and builds nothing on the host.
+struct HqdwhState {
+    int n = 0, b = 0, n_min = 0;
+    double eps = 0.0, delta = 0.0;
+    bool graphs = false;
+    std::unique_ptr<Engine> eng;
+    std::unique_ptr<DHodlr> X, Z, W, Y, V, WK, P;
+    double *d_bands = nullptr, *d_tmp = nullptr, *d_rdiag = nullptr, *d_diag = nullptr;
+    int* d_piv = nullptr;
+    cudaGraphExec_t g_first = nullptr, g_iter = nullptr;
+    long long l_first = 0, l_iter = 0, nodes_iter = 0;
+    size_t arena_mark = 0;
+    long long leaf_entries = 0;
+    ~HqdwhState() {
+        if (g_first) cudaGraphExecDestroy(g_first);
+        if (g_iter) cudaGraphExecDestroy(g_iter);
+        cudaFree(d_bands); cudaFree(d_tmp); cudaFree(d_rdiag); cudaFree(d_diag); cudaFree(d_piv);
+        X.reset(); Z.reset(); W.reset(); Y.reset(); V.reset(); WK.reset(); P.reset();
+        eng.reset();
+    }
+    bool matches(int n_, int b_, int nm_, double e_, double d_) const {
+        return n == n_ && b == b_ && n_min == nm_ && eps == e_ && delta == d_;
+    }
+};
+
+namespace {
+std::mutex g_state_mu;
+std::vector<std::unique_ptr<HqdwhState>> g_state_cache;
+constexpr size_t kStateCache = 2;
+const bool g_no_state_cache = std::getenv("SPG_NO_PLAN_CACHE") != nullptr;
+
+std::unique_ptr<HqdwhState> take_cached_state(int n, int b, int n_min, double eps, double delta) {
+    std::lock_guard<std::mutex> lk(g_state_mu);
+    for (size_t i = 0; i < g_state_cache.size(); ++i)
+        if (g_state_cache[i]->matches(n, b, n_min, eps, delta)) {
+            auto s = std::move(g_state_cache[i]);
+            g_state_cache.erase(g_state_cache.begin() + i);
+            return s;
+        }
+    return nullptr;
+}
+}  // namespace
+
+void release_state(std::unique_ptr<HqdwhState> s) {
+    if (!s) return;
+    if (s->graphs && !g_no_state_cache) {
+        cudaStreamSynchronize(s->eng->stream());
+        std::lock_guard<std::mutex> lk(g_state_mu);
+        if (g_state_cache.size() >= kStateCache) g_state_cache.erase(g_state_cache.begin());   // oldest out
+        g_state_cache.push_back(std::move(s));
+    }
+}
+
+// plan builders of the three projector stages (qdwh.hpp:205-239)
+namespace {
+using TimedFn = std::function<void(Plan&, int, const std::function<void()>&)>;
+
+void push_diag(Plan& p, HqdwhState& st) {
+    Engine& E = *st.eng;
+    const DevTree dt = E.dtree();
+    const int* rk = st.X->rank;
+    Scalars S = E.sc();
+    double* dd = st.d_diag;
+    const long long le = st.leaf_entries;
+    p.launches.push_back([=](cudaStream_t s) {
+        k_diag<<<1, 256, 0, s>>>(rk, dt.nnodes, dt.left, dt.right, dt.size, S.counter, dd, le);
+        SPG_LAUNCH_CHECK();
+    });
+}
+
+// k = 0: QR-based first iterate (fast_qr.hpp:509-514 redesigned)
+void build_first(Plan& p, HqdwhState& st, const TimedFn& timed) {
+    Engine& E = *st.eng;
+    Scalars S = E.sc();
+    const int n = st.n, b = st.b;
+    timed(p, PH_FIRST, [&]() {
+        const DevTree dt = E.dtree();
+        const DHodlr* Wp = st.W.get();
+        const DHodlr* Zp = st.Z.get();
+        double *d_bands = st.d_bands, *d_tmp = st.d_tmp, *d_rdiag = st.d_rdiag;
+        p.launches.push_back([=](cudaStream_t s) {
+            launch_iter_params(S.sched, S.counter, S.slots, S.scal, s);
+            launch_givens_reduce(n, b, d_bands, S.slots, d_tmp, d_rdiag, s);
+            Wp->zero(s);
+            launch_from_band(dt, Wp->view(), 1, 2 * b, d_rdiag, nullptr, 1.0, s);
+            Zp->zero(s);
+            launch_from_band(dt, Zp->view(), 0, b, d_bands, S.slots + 5, 1.0, s);   // sqrt(c0) A / alpha
+        });
+        E.op_leaf_dinv(p, *st.W);                                 // diagonal-block inverses of R's leaves
+        E.op_solve_prep(p, *st.W);                                // solved coupling bases of HODLR(R)
+        E.op_solve_upper_right(p, *st.Z, *st.W, *st.Y, *st.WK);   // Q1 = B R^{-1}
+        E.op_solve_upperT_right(p, *st.Y, *st.W, *st.V, *st.WK);  // M  = Q1 R^{-T} = Q1 Q2^T
+        E.op_symmetrize(p, *st.V);                                // q1q2t symmetrizes M (fast_qr.hpp:513)
+        E.op_axpby(p, 1.0, S.slots + 1, *st.X, 1.0, S.slots + 4, *st.V, *st.X);
+        E.op_symmetrize(p, *st.X);
+    });
+    push_diag(p, st);
+}
+
+// k >= 1: Cholesky-based iterate (qdwh.hpp:217-232)
+void build_iter(Plan& p, HqdwhState& st, const TimedFn& timed) {
+    Engine& E = *st.eng;
+    Scalars S = E.sc();
+    timed(p, PH_MUL, [&]() {
+        p.launches.push_back([=](cudaStream_t s) { launch_iter_params(S.sched, S.counter, S.slots, S.scal, s); });
+        E.op_multiply(p, *st.X, *st.X, *st.Z);
+        E.op_scale_shift(p, *st.Z, 1.0, S.slots + 0, 1.0);
+    });
+    // deferred W12 truncation (SPG_CHOL_REFERENCE_ORDER=1: the reference's order)
+    static const bool ref_order = std::getenv("SPG_CHOL_REFERENCE_ORDER") != nullptr;
+    timed(p, PH_CHOL, [&]() { E.op_cholesky(p, *st.Z, *st.W, *st.WK, !ref_order); });
+    timed(p, PH_SOLVE, [&]() {
+        E.op_solve_prep(p, *st.W);
+        E.op_solve_upper_right(p, *st.X, *st.W, *st.Y, *st.WK);
+    });
+    timed(p, PH_SOLVET, [&]() { E.op_solve_upperT_right(p, *st.Y, *st.W, *st.V, *st.WK); });
+    timed(p, PH_AXPBY, [&]() {
+        E.op_axpby(p, 1.0, S.slots + 1, *st.X, 1.0, S.slots + 2, *st.V, *st.X);
+        E.op_symmetrize(p, *st.X);
+    });
+    push_diag(p, st);
+}
+
+cudaGraphExec_t capture(HqdwhState& st, Plan& p, long long& launches, long long* nodes) {
+    Engine& E = *st.eng;
+    cudaStream_t s = E.stream();
+    E.arena().commit(s);
+    cudaGraph_t g;
+    const long long l0 = g_launches.load();
+    SPG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    p.run(s);
+    SPG_CUDA(cudaStreamEndCapture(s, &g));
+    cudaGraphExec_t ge;
+    SPG_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    launches = g_launches.load() - l0;
+    g_launches -= launches;   // counted again at every replay
+    if (nodes) {
+        size_t nn = 0;
+        SPG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+        *nodes = (long long)nn;
+    }
+    SPG_CUDA(cudaGraphDestroy(g));
+    return ge;
+}
+
+std::unique_ptr<HqdwhState> make_state(int n, int b, int n_min, double eps, double delta, bool profile) {
+    auto st = std::make_unique<HqdwhState>();
+    st->n = n; st->b = b; st->n_min = n_min; st->eps = eps; st->delta = delta;
+    st->eng = std::make_unique<Engine>(n, n_min, eps);
+    Engine& E = *st->eng;
+    E.set_profile(profile);
+    check_tree(E.tree());
+    st->X = E.new_hodlr(); st->Z = E.new_hodlr(); st->W = E.new_hodlr(); st->Y = E.new_hodlr();
+    st->V = E.new_hodlr(); st->WK = E.new_hodlr(); st->P = E.new_hodlr();
+    const int wbl = 3 * b + 1;
+    const size_t tmp_doubles = (size_t)n * std::max(wbl, 4 * b + 4) + 8 * (size_t)n + 128;
+    SPG_CUDA(cudaMalloc(&st->d_bands, sizeof(double) * band_len(n, b)));
+    SPG_CUDA(cudaMalloc(&st->d_tmp, sizeof(double) * tmp_doubles));
+    SPG_CUDA(cudaMalloc(&st->d_rdiag, sizeof(double) * (size_t)(2 * b + 1) * n));
+    SPG_CUDA(cudaMalloc(&st->d_diag, sizeof(double) * 2 * 64));
+    SPG_CUDA(cudaMalloc(&st->d_piv, sizeof(int) * n));
+    for (int f : E.tree().leaves) st->leaf_entries += (long long)E.tree().size[f] * E.tree().size[f];
+    return st;
+}
+
+void build_graphs(HqdwhState& st) {
+    const TimedFn untimed = [](Plan&, int, const std::function<void()>& body) { body(); };
+    {
+        Plan p;
+        build_first(p, st, untimed);
+        st.g_first = capture(st, p, st.l_first, nullptr);
+    }
+    {
+        Plan p;
+        build_iter(p, st, untimed);
+        st.g_iter = capture(st, p, st.l_iter, &st.nodes_iter);
+    }
+    st.arena_mark = st.eng->arena().mark();
+    st.graphs = true;
+}
+}  // namespace
+
 spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double eps, double delta) {
     if (n < 2 || b < 1 || b >= n) throw StatusError(SPG_INVALID_ARGUMENT, "BandedSymmetric: n >= 2, 1 <= b < n required");
     const long long blen = band_len(n, b);
     for (long long i = 0; i < blen; ++i)
         if (!std::isfinite(bands_host[i])) throw StatusError(SPG_INVALID_ARGUMENT, "hqdwh: nonfinite input");
     const auto hc0 = std::chrono::steady_clock::now();
+    auto hms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hc0).count(); };
+    const bool profile = g_profile.load() != 0;
+    const bool use_graph = !profile && !std::getenv("SPG_NO_GRAPH");
     auto R = std::make_unique<spg_result>();
-    R->eng = std::make_unique<Engine>(n, n_min, eps);
-    Engine& E = *R->eng;
-    E.set_profile(g_profile.load() != 0);
-    check_tree(E.tree());
+    std::unique_ptr<HqdwhState> state = use_graph && !g_no_state_cache ? take_cached_state(n, b, n_min, eps, delta) : nullptr;
+    const bool cached = state != nullptr;
+    if (!state) state = make_state(n, b, n_min, eps, delta, profile);
+    HqdwhState& stt = *state;
+    Engine& E = *stt.eng;
     cudaStream_t st = E.stream();
     const long long launches0 = g_launches.load();
     Scalars& S = E.sc();
-
-    auto X = E.new_hodlr();
-    auto hms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hc0).count(); };
-    auto Z = E.new_hodlr();
-    auto W = E.new_hodlr();
-    auto Y = E.new_hodlr();
-    auto V = E.new_hodlr();
-    auto WK = E.new_hodlr();
-    auto P = E.new_hodlr();
-
-    // device scratch for the setup kernels
+    double *d_bands = stt.d_bands, *d_tmp = stt.d_tmp, *d_diag = stt.d_diag;
+    int* d_piv = stt.d_piv;
     const int wbl = 3 * b + 1;
-    double *d_bands, *d_tmp, *d_rdiag, *d_diag;
-    int* d_piv;
-    const size_t tmp_doubles = (size_t)n * std::max(wbl, 4 * b + 4) + 8 * (size_t)n + 128;
-    SPG_CUDA(cudaMalloc(&d_bands, sizeof(double) * blen));
-    SPG_CUDA(cudaMalloc(&d_tmp, sizeof(double) * tmp_doubles));
-    SPG_CUDA(cudaMalloc(&d_rdiag, sizeof(double) * (size_t)(2 * b + 1) * n));
-    SPG_CUDA(cudaMalloc(&d_diag, sizeof(double) * 2 * 64));
-    SPG_CUDA(cudaMalloc(&d_piv, sizeof(int) * n));
-
     const double h_alloc = hms();
+
     // ---- timing instrumentation: per-run event tables, no host sync inside the loop
     std::vector<cudaEvent_t> evs;
     auto mkev = [&]() { cudaEvent_t e; SPG_CUDA(cudaEventCreate(&e)); evs.push_back(e); return e; };
@@ -328,9 +509,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     std::vector<int> used((size_t)nruns * nmarks, 0);
     int cur_run = 0;
     int* cur_run_p = &cur_run;
-    bool phase_events = true;   // off while building a plan that is captured into a CUDA graph
-    auto timed = [&](Plan& p, int phase, const std::function<void()>& body) {
-        if (!phase_events) { body(); return; }
+    const TimedFn timed = [&](Plan& p, int phase, const std::function<void()>& body) {
         cudaEvent_t* tab = evtab.data();
         int* up = used.data();
         p.launches.push_back([=](cudaStream_t s) {
@@ -373,8 +552,8 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         commit_run(p);
     }
     // The setup results (iteration count, alpha, l0, status) are read back only after
-    // the first iterate has been queued and the iteration graph has been built and
-    // instantiated, so that host work overlaps the device's setup and first iterate.
+    // the first iterate has been queued and the iteration graph built (when it is not
+    // cached), so that host work overlaps the device's setup and first iterate.
     // (pinned destinations: a pageable D2H copy would block the host until the setup ends)
     double* hp = E.host_pinned();
     SPG_CUDA(cudaMemcpyAsync(hp, S.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
@@ -394,144 +573,73 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         if (count == -1) throw StatusError(SPG_INVALID_ARGUMENT, "qdwh: nonpositive lower bound l0");
         if (count < 0) throw StatusError(SPG_DOMAIN, "qdwh_params: l must lie in (0, 1]");
     };
-
-    // ---------------- X0 = from_banded(A / alpha)
-    {
-        Plan p;
+    auto push_x0 = [&](Plan& p) {   // X0 = from_banded(A / alpha)
         const DevTree dt = E.dtree();
-        const DHodlr* Xp = X.get();
+        const DHodlr* Xp = stt.X.get();
         p.launches.push_back([=](cudaStream_t s) {
             Xp->zero(s);
             launch_from_band(dt, Xp->view(), 0, b, d_bands, S.scal + 2, 1.0, s);
         });
+    };
+    {
+        Plan p;
+        push_x0(p);
         commit_run(p);
     }
-
-    // per-iteration diagnostics kernel
-    const long long leaf_entries = [&]() { long long e = 0; for (int f : E.tree().leaves) e += (long long)E.tree().size[f] * E.tree().size[f]; return e; }();
-    auto push_diag = [&](Plan& p) {
-        const DevTree dt = E.dtree();
-        const int* rk = X->rank;
-        p.launches.push_back([=](cudaStream_t s) {
-            k_diag<<<1, 256, 0, s>>>(rk, dt.nnodes, dt.left, dt.right, dt.size, S.counter, d_diag, leaf_entries);
-            SPG_LAUNCH_CHECK();
-        });
-    };
     std::vector<cudaEvent_t> it_ev;
-
     // ---------------- k = 0: QR-based first iterate (queued before the count is known;
     // undone below when the schedule has no iteration at all)
     {
-        Plan p;
         cudaEvent_t e0 = mkev();
         it_ev.push_back(e0);
-        p.launches.push_back([e0](cudaStream_t s) { SPG_CUDA(cudaEventRecord(e0, s)); });
-        timed(p, PH_FIRST, [&]() {
-            const DevTree dt = E.dtree();
-            const DHodlr* Wp = W.get();
-            const DHodlr* Zp = Z.get();
-            p.launches.push_back([=](cudaStream_t s) {
-                launch_iter_params(S.sched, S.counter, S.slots, S.scal, s);
-                launch_givens_reduce(n, b, d_bands, S.slots, d_tmp, d_rdiag, s);
-                Wp->zero(s);
-                launch_from_band(dt, Wp->view(), 1, 2 * b, d_rdiag, nullptr, 1.0, s);
-                Zp->zero(s);
-                launch_from_band(dt, Zp->view(), 0, b, d_bands, S.slots + 5, 1.0, s);   // sqrt(c0) A / alpha
-            });
-            E.op_leaf_dinv(p, *W);                         // diagonal-block inverses of R's leaves
-            E.op_solve_prep(p, *W);                        // solved coupling bases of HODLR(R)
-            E.op_solve_upper_right(p, *Z, *W, *Y, *WK);    // Q1 = B R^{-1}
-            E.op_solve_upperT_right(p, *Y, *W, *V, *WK);   // M  = Q1 R^{-T} = Q1 Q2^T
-            E.op_symmetrize(p, *V);                        // q1q2t symmetrizes M (fast_qr.hpp:513)
-            E.op_axpby(p, 1.0, S.slots + 1, *X, 1.0, S.slots + 4, *V, *X);
-            E.op_symmetrize(p, *X);
-        });
-        push_diag(p);
-        commit_run(p);
-    }
-
-    // ---------------- k >= 1: Cholesky-based iterates (one plan, replayed; rebuilt per run in profile mode)
-    {
-        auto build_iter = [&](Plan& p) {
-            timed(p, PH_MUL, [&]() {
-                p.launches.push_back([=](cudaStream_t s) { launch_iter_params(S.sched, S.counter, S.slots, S.scal, s); });
-                E.op_multiply(p, *X, *X, *Z);
-                E.op_scale_shift(p, *Z, 1.0, S.slots + 0, 1.0);
-            });
-            // deferred W12 truncation (SPG_CHOL_REFERENCE_ORDER=1: the reference's order)
-            static const bool ref_order = std::getenv("SPG_CHOL_REFERENCE_ORDER") != nullptr;
-            timed(p, PH_CHOL, [&]() { E.op_cholesky(p, *Z, *W, *WK, !ref_order); });
-            timed(p, PH_SOLVE, [&]() {
-                E.op_solve_prep(p, *W);
-                E.op_solve_upper_right(p, *X, *W, *Y, *WK);
-            });
-            timed(p, PH_SOLVET, [&]() { E.op_solve_upperT_right(p, *Y, *W, *V, *WK); });
-            timed(p, PH_AXPBY, [&]() {
-                E.op_axpby(p, 1.0, S.slots + 1, *X, 1.0, S.slots + 2, *V, *X);
-                E.op_symmetrize(p, *X);
-            });
-            push_diag(p);
-            E.arena().commit(st);
-        };
-        // Default: the iteration plan is captured once into a CUDA graph and replayed
-        // count-1 times (all per-iteration scalars are read from device memory, so the
-        // graph is iteration-invariant).  Profile mode rebuilds the plan per run so every
-        // batch keeps its own event pair; SPG_NO_GRAPH=1 replays the plan without a graph.
-        const bool use_graph = !E.profile() && !std::getenv("SPG_NO_GRAPH");
-        Plan p;
-        cudaGraphExec_t gexec = nullptr;
-        long long per_iter_launches = 0;
-        if (use_graph) {
-            auto hclock = []() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
-            const double h0 = hclock();
-            phase_events = false;
-            build_iter(p);
-            phase_events = true;
-            const double h1 = hclock();
-            cudaGraph_t g;
-            const long long l0c = g_launches.load();
-            SPG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-            p.run(st);
-            SPG_CUDA(cudaStreamEndCapture(st, &g));
-            const double h2 = hclock();
-            SPG_CUDA(cudaGraphInstantiate(&gexec, g, 0));
-            const double h3 = hclock();
-            if (std::getenv("SPG_HOST_TIMING"))
-                std::fprintf(stderr, "host: build %.1f ms, capture %.1f ms, instantiate %.1f ms\n", h1 - h0, h2 - h1, h3 - h2);
-            size_t nn = 0;
-            SPG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
-            SPG_CUDA(cudaGraphDestroy(g));
-            per_iter_launches = g_launches.load() - l0c;   // kernels captured once (replayed count-1 times)
-            R->info.graph_nodes = (long long)nn;
-            R->info.graph_used = 1;
-        } else if (!E.profile()) {
-            build_iter(p);
+        SPG_CUDA(cudaEventRecord(e0, st));
+        if (stt.graphs) {
+            SPG_CUDA(cudaGraphLaunch(stt.g_first, st));
+            g_launches += stt.l_first;
+        } else if (use_graph) {
+            // first call of this shape: the first iterate runs as a plan while its graph and
+            // the iteration graph are captured after it (host work overlapping the device)
+            Plan p;
+            build_first(p, stt, timed);
+            commit_run(p);
+        } else {
+            Plan p;
+            build_first(p, stt, timed);
+            commit_run(p);
         }
+    }
+    // ---------------- k >= 1: Cholesky-based iterates (graph replay; rebuilt per run in profile mode)
+    {
+        if (use_graph && !stt.graphs) {
+            const double h0 = hms();
+            build_graphs(stt);
+            if (std::getenv("SPG_HOST_TIMING"))
+                std::fprintf(stderr, "host: graphs built in %.1f ms (arena %.1f MB)\n", hms() - h0, E.arena().used() / 1048576.0);
+        }
+        R->info.graph_used = stt.graphs ? 1 : 0;
+        R->info.graph_nodes = stt.nodes_iter;
+        Plan p;
+        if (!stt.graphs && !profile) build_iter(p, stt, timed);
         finish_setup();
-        if (gexec) g_launches += per_iter_launches * ((long long)count - 2);
         if (count == 0) {   // no iteration: X = X0 = A / alpha (the queued first iterate is discarded)
             Plan p0;
-            const DevTree dt = E.dtree();
-            const DHodlr* Xp = X.get();
-            p0.launches.push_back([=](cudaStream_t s) {
-                Xp->zero(s);
-                launch_from_band(dt, Xp->view(), 0, b, d_bands, S.scal + 2, 1.0, s);
-            });
+            push_x0(p0);
             commit_run(p0);
             it_ev.clear();
         }
         for (int k = 1; k < count; ++k) {
             cur_run = k;
-            if (E.profile()) { p = Plan(); build_iter(p); }
+            if (profile) { p = Plan(); build_iter(p, stt, timed); E.arena().commit(st); }
             cudaEvent_t e0 = mkev();
             it_ev.push_back(e0);
             SPG_CUDA(cudaEventRecord(e0, st));
-            if (gexec) SPG_CUDA(cudaGraphLaunch(gexec, st));
-            else p.run(st);
-        }
-        if (gexec) {
-            SPG_CUDA(cudaStreamSynchronize(st));
-            SPG_CUDA(cudaGraphExecDestroy(gexec));
+            if (stt.graphs) {
+                SPG_CUDA(cudaGraphLaunch(stt.g_iter, st));
+                g_launches += stt.l_iter;
+            } else {
+                E.arena().commit(st);
+                p.run(st);
+            }
         }
     }
     {
@@ -540,16 +648,20 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         SPG_CUDA(cudaEventRecord(e0, st));
     }
     // ---------------- P = (I - X) / 2  (qdwh.hpp:235-239)
+    const size_t amark = E.arena().mark();
     {
         Plan p;
-        E.op_copy(p, *X, *P);
-        E.op_scale_shift(p, *P, -0.5, nullptr, 0.5);
+        E.op_copy(p, *stt.X, *stt.P);
+        E.op_scale_shift(p, *stt.P, -0.5, nullptr, 0.5);
         p.launches.push_back([t_end](cudaStream_t s) { SPG_CUDA(cudaEventRecord(t_end, s)); });
         commit_run(p);
     }
     SPG_CUDA(cudaStreamSynchronize(st));
     SPG_CUDA(cudaGetLastError());
-    if (std::getenv("SPG_HOST_TIMING")) std::fprintf(stderr, "host: engine+alloc %.1f ms, run_hqdwh to sync %.1f ms\n", h_alloc, hms());
+    if (stt.graphs) E.arena().release(std::max(amark, stt.arena_mark));   // per-call descriptors
+    if (std::getenv("SPG_HOST_TIMING"))
+        std::fprintf(stderr, "host: state %s %.1f ms, run_hqdwh to sync %.1f ms\n", cached ? "cached" : "built", h_alloc,
+                     hms());
     check_status_dev(S.status);
 
     // ---------------- report
@@ -575,6 +687,11 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
                 default: I.ms_axpby_sym += ms; break;
             }
         }
+    if (I.ms_first == 0.0 && it_ev.size() >= 2) {   // first iterate replayed as a graph: its event pair
+        float w = 0.f;
+        SPG_CUDA(cudaEventElapsedTime(&w, it_ev[0], it_ev[1]));
+        I.ms_first = w;
+    }
     std::vector<double> sched(4 * 64), dg(2 * 64);
     SPG_CUDA(cudaMemcpy(sched.data(), S.sched, sizeof(double) * 4 * 64, cudaMemcpyDeviceToHost));
     SPG_CUDA(cudaMemcpy(dg.data(), d_diag, sizeof(double) * 2 * 64, cudaMemcpyDeviceToHost));
@@ -614,8 +731,8 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     // diagnostics of P
     {
         std::vector<int> rk(2 * E.tree().nnodes());
-        SPG_CUDA(cudaMemcpy(rk.data(), P->rank, sizeof(int) * rk.size(), cudaMemcpyDeviceToHost));
-        long long ent = leaf_entries;
+        SPG_CUDA(cudaMemcpy(rk.data(), stt.P->rank, sizeof(int) * rk.size(), cudaMemcpyDeviceToHost));
+        long long ent = stt.leaf_entries;
         int mx = 0;
         for (int id = 0; id < E.tree().nnodes(); ++id) {
             if (E.tree().leaf(id)) continue;
@@ -626,18 +743,18 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         I.max_rank = mx;
         I.memory_bytes = 8 * ent;
         double* dtr = d_tmp;   // setup scratch, free by now
-        k_trace<<<1, 256, 0, st>>>(E.dtree(), P->view(), dtr);
+        k_trace<<<1, 256, 0, st>>>(E.dtree(), stt.P->view(), dtr);
         SPG_LAUNCH_CHECK();
         SPG_CUDA(cudaMemcpyAsync(hp + 8, dtr, sizeof(double), cudaMemcpyDeviceToHost, st));
         SPG_CUDA(cudaStreamSynchronize(st));
         I.trace = hp[8];
     }
     for (auto e : evs) cudaEventDestroy(e);
-    cudaFree(d_bands); cudaFree(d_tmp); cudaFree(d_rdiag); cudaFree(d_diag); cudaFree(d_piv);
-    R->X = std::move(X);
-    R->P = std::move(P);
+    R->state = std::move(state);
     return R.release();
 }
+
+namespace {
 
 template <class F>
 int guarded(F&& f) {
@@ -763,19 +880,20 @@ int spg_result_diag(const spg_result* r, spg_iter_diag* out) {
 }
 
 int spg_result_flat_size(const spg_result* r, int which, long long* nd) {
-    return guarded([&]() { export_flat(*r->eng, which == 0 ? *r->P : *r->X, nullptr, nullptr, nd); });
+    return guarded([&]() { export_flat(r->eng(), which == 0 ? r->P() : r->X(), nullptr, nullptr, nd); });
 }
 
 int spg_result_export(const spg_result* r, int which, int* ranks, double* data) {
-    return guarded([&]() { export_flat(*r->eng, which == 0 ? *r->P : *r->X, ranks, data, nullptr); });
+    return guarded([&]() { export_flat(r->eng(), which == 0 ? r->P() : r->X(), ranks, data, nullptr); });
 }
 
 int spg_result_apply(const spg_result* r, int which, int m, const double* X, double* Y) {
     return guarded([&]() {
-        Engine& E = *r->eng;
+        Engine& E = r->eng();
         const int n = E.tree().n;
         if (m < 1 || m > KCAP) throw StatusError(SPG_INVALID_ARGUMENT, "spg_result_apply: 1 <= m <= KCAP");
-        const DHodlr& H = which == 0 ? *r->P : *r->X;
+        const DHodlr& H = which == 0 ? r->P() : r->X();
+        const size_t amark = E.arena().mark();
         cudaStream_t st = E.stream();
         std::vector<double> cm((size_t)n * m);
         for (int i = 0; i < n; ++i)
@@ -797,8 +915,14 @@ int spg_result_apply(const spg_result* r, int which, int m, const double* X, dou
         for (int i = 0; i < n; ++i)
             for (int c = 0; c < m; ++c) Y[(size_t)i * m + c] = cm[i + (size_t)c * n];
         cudaFree(dx); cudaFree(dy); cudaFree(dm);
+        E.arena().release(amark);
     });
 }
+
+Engine& spg_result::eng() const { return *state->eng; }
+const DHodlr& spg_result::X() const { return *state->X; }
+const DHodlr& spg_result::P() const { return *state->P; }
+spg_result::~spg_result() { release_state(std::move(state)); }
 
 void spg_result_free(spg_result* r) { delete r; }
 

@@ -72,12 +72,27 @@ static int micro_trunc(int ngroups, int p, int reps, double* out, int nout, int 
     long long* tr;
     SPG_CUDA(cudaMalloc(&tr, sizeof(long long) * 16));
     SPG_CUDA(cudaMemset(tr, 0, sizeof(long long) * 16));
+    long long* ttr;
+    SPG_CUDA(cudaMalloc(&ttr, sizeof(long long) * 64));
+    SPG_CUDA(cudaMemset(ttr, 0, sizeof(long long) * 64));
     set_core_trace(tr);
+    set_tsqr_trace(ttr);
     set_trunc_events(ev);
     pl.run(st);
     SPG_CUDA(cudaStreamSynchronize(st));
     set_trunc_events(nullptr);
     set_core_trace(nullptr);
+    set_tsqr_trace(nullptr);
+    {
+        std::vector<long long> tt(64);
+        SPG_CUDA(cudaMemcpy(tt.data(), ttr, sizeof(long long) * 64, cudaMemcpyDeviceToHost));
+        if (std::getenv("SPG_TSQR_TRACE")) {
+            for (int pn = 0; pn < 14 && tt[3 * pn] != 0; ++pn)
+                std::printf("  tsqr panel %d: factor %lld apply %lld cycles\n", pn, tt[3 * pn + 1] - tt[3 * pn],
+                            tt[3 * pn + 2] - tt[3 * pn + 1]);
+        }
+        cudaFree(ttr);
+    }
     std::vector<long long> h(16);
     SPG_CUDA(cudaMemcpy(h.data(), tr, sizeof(long long) * 16, cudaMemcpyDeviceToHost));
     int rr = 0;

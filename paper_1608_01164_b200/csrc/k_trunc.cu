@@ -63,6 +63,9 @@ __device__ __forceinline__ double* z_area(const TTask& t, double* ws, int side) 
 }
 
 // ------------------------------------------------------------------ TSQR
+__device__ long long* g_tsqr_trace = nullptr;   // micro-benchmarks: clock64 per panel phase (CTA 0, sub-block 0)
+void set_tsqr_trace(long long* p) { SPG_CUDA(cudaMemcpyToSymbol(g_tsqr_trace, &p, sizeof(p))); }
+#define TSQR_TRACE(slot) do { if (g_tsqr_trace && b == 0 && blockIdx.x == 0 && threadIdx.x == 0) g_tsqr_trace[slot] = clock64(); } while (0)
 // Streaming Householder QR of the rows [r0, r0+nrows) of an implicit matrix with
 // k columns, starting from R = 0:  [0_k; A] = Q [R; 0].  Each 128-row sub-block
 // is folded into R by k reflectors y_j = [e_j; v_j] acting on (R row j, block
@@ -91,6 +94,7 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
         for (int pn = 0; pn < npan; ++pn) {
             const int j0 = pn * TS_NB, nb = min(TS_NB, k - j0);
             double* Tp = sTT + KIN_MAX + pn * TS_NB * TS_NB;   // T (column-major 8 x 8)
+            TSQR_TRACE(3 * pn);
             if (warp == 0) {
                 double x[TS_NB][SB / 32];
 #pragma unroll
@@ -160,6 +164,7 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                         for (int t = 0; t < SB / 32; ++t) sB[(lane + 32 * t) + (j0 + a) * SB] = x[a][t];
             }
             __syncthreads();
+            TSQR_TRACE(3 * pn + 1);
             // Q_panel^T on the remaining columns: w = Y^T a, w = T^T w, a -= Y w
             for (int c = j0 + nb + warp; c < k; c += nwarps) {
                 double av[SB / 32], w[TS_NB];
@@ -205,6 +210,7 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                     if (lane == a && a < nb) sR[(j0 + a) + c * KIN_MAX] = ra[a] - wt[a];
             }
             __syncthreads();
+            TSQR_TRACE(3 * pn + 2);
         }
         // store reflector tails (SB x k), taus and the panel T's of this sub-block
         double* dst = refl + (long long)b * SB * KIN_MAX;

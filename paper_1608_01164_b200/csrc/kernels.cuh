@@ -18,6 +18,7 @@ void launch_core2(const TTask* tasks, int ntasks, double* ws, double eps, unsign
 void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* status, cudaStream_t st);
 void set_trunc_events(cudaEvent_t* ev);   // micro-benchmarks (4 events: tsqr | core | apply)
 void set_core_trace(long long* p);        // micro-benchmarks (clock64 per core phase, task 0)
+void set_tsqr_trace(long long* p);        // micro-benchmarks (clock64 per TSQR panel phase, CTA 0)
 
 // ------------------------------------------------------------ batched DMMA GEMM
 // C = alpha * op(A) op(B) + beta * C, column-major.  Dimensions are constants
