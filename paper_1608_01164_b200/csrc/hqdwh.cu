@@ -376,7 +376,7 @@ void build_first(Plan& p, HqdwhState& st, const TimedFn& timed) {
         double *d_bands = st.d_bands, *d_tmp = st.d_tmp, *d_rdiag = st.d_rdiag;
         p.launches.push_back([=](cudaStream_t s) {
             launch_iter_params(S.sched, S.counter, S.slots, S.scal, s);
-            launch_givens_reduce(n, b, d_bands, S.slots, d_tmp, d_rdiag, s);
+            launch_givens_reduce(n, b, d_bands, S.slots, d_tmp, d_rdiag, s, S.status);
             Wp->zero(s);
             launch_from_band(dt, Wp->view(), 1, 2 * b, d_rdiag, nullptr, 1.0, s);
             Zp->zero(s);

@@ -165,10 +165,12 @@ static int micro_lat(double* out, int nout) {
 }
 
 void core_hist_ctl(int enable, double* out, int nout);
+void seq_trace_read(long long* out);
 int micro_kernel(int which, int n, int reps, double* out, int nout) {
     if (which == 2) { core_hist_ctl(n, nullptr, 0); return 0; }        // enable (n=1) / disable (n=0) + clear
     if (which == 3) { core_hist_ctl(-1, out, nout); return 0; }       // read 4 x 128 bins
     if (which == 4) return micro_lat(out, nout);                      // latency calibration
+    if (which == 5) { long long t[16]; seq_trace_read(t); for (int i = 0; i < nout && i < 16; ++i) out[i] = (double)t[i]; return 0; }
     if (which == 1) return micro_trunc(1, n, reps, out, nout);
     if (which == 6) return micro_trunc(2, n, reps, out, nout);
     if (which >= 100) return micro_trunc(1, n, reps, out, nout, which - 100);   // one group of k = which - 100

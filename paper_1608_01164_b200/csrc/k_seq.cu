@@ -5,6 +5,8 @@
 //     (estimate_l0 / hager_norm1 / BandedLu, estimates.hpp:40-80, banded_lu.hpp:16-93)
 //   * Givens reduction of [s A; I] -> R (reduce_banded = reduce_tridiag for b = 1,
 //     fast_qr.hpp:83-232)
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -114,6 +116,8 @@ __device__ void lu_solve_t_w(BLUw& L, WinI& piv, Win& x, int lane) {
 }
 
 constexpr int WIN_LU = 4096, WIN_X = 1024;
+__device__ long long g_seq_trace[16];   // diagnostics: clock64 at the phase ends of k_est_l0_w / k_givens_w
+void seq_trace_read(long long* out) { SPG_CUDA(cudaMemcpyFromSymbol(out, g_seq_trace, sizeof(long long) * 16)); }
 
 __global__ void __launch_bounds__(32) k_est_l0_w(int n, int b, const double* __restrict__ bands, const double* alpha_p,
                                                 double* lu, int* piv, double* vecs, double* out, unsigned* status) {
@@ -150,6 +154,7 @@ __global__ void __launch_bounds__(32) k_est_l0_w(int n, int b, const double* __r
         lu[idx] = v;
     }
     __syncwarp();
+    if (lane == 0) g_seq_trace[0] = clock64();
     BLUw L{Win{lu, (long long)n * wd, sLU, (WIN_LU / wd) * wd, 0, 0}, n, b, wd};
     L.w.load(0, lane);
     // factor (banded_lu.hpp:66-88)
@@ -189,6 +194,7 @@ __global__ void __launch_bounds__(32) k_est_l0_w(int n, int b, const double* __r
         __syncwarp();
     }
     L.w.flush(lane);
+    if (lane == 0) g_seq_trace[1] = clock64();
     if (singular) {
         if (lane == 0) { atomicOr(status, ST_SINGULAR); out[0] = 0.0; }
         return;
@@ -244,6 +250,7 @@ __global__ void __launch_bounds__(32) k_est_l0_w(int n, int b, const double* __r
         for (int i = lane; i < n; i += 32) x[i] = (i == j) ? 1.0 : 0.0;
         __syncwarp();
     }
+    if (lane == 0) g_seq_trace[2] = clock64();
     if (lane == 0) {
         const double cond1 = n1 * est;
         out[0] = n1 / (sqrt((double)n) * cond1);
@@ -305,6 +312,7 @@ __global__ void __launch_bounds__(32) k_givens_w(int n, int b, double* R, double
     Win wa{auxg, n, sA, WIN_V, 0, 0};
     Win wj{junkg, (long long)n * jw, sJ, (WIN_J / jw) * jw, 0, 0};
     wr.load(0, lane); wn.load(0, lane); wa.load(0, lane); wj.load(0, lane);
+    if (lane == 0) g_seq_trace[3] = clock64();
     auto RA = [&](int i, int k) -> double& { return wr.at((long long)i * w + (k - i + b)); };
     auto JK = [&](int t, int k) -> double& { return wj.at((long long)t * jw + (k - (t + 1))); };
     auto rowN = [&](int i) -> double& { return wn.at(i); };
@@ -379,13 +387,120 @@ __global__ void __launch_bounds__(32) k_givens_w(int n, int b, double* R, double
         }
     }
     wr.flush(lane);
+    if (lane == 0) g_seq_trace[4] = clock64();
     __threadfence_block();
     for (int d = 0; d <= 2 * b; ++d)
         for (int i = lane; i < n; i += 32) rdiag[(long long)d * n + i] = i + d < n ? R[(long long)i * w + (d + b)] : 0.0;
 }
 
+// ------------------------------------------------------------ R from a band Cholesky
+// The first iterate only needs an upper-banded R with R^T R = [sA; I]^T [sA; I] =
+// s^2 A^2 + I (Q1 Q2^T = s A R^{-1} R^{-T}), and R^{-1} R^{-T} does not see
+// the row signs that distinguish the Givens R of reduce_tridiag / reduce_banded
+// (fast_qr.hpp:83-232) from the Cholesky factor.  Both have the same backward error
+// (|R^T R - H| ~ u |H|).  So R is taken as L^T, H = L L^T the band Cholesky of
+// H = s^2 A^2 + I (bandwidth w = 2b): one dependent square root per row instead of
+// ~3b dependent Givens rotations.
+//   k_form_h: H in lower band storage Hb[d n + i] = H(i + d, i), d = 0..w (parallel)
+//   k_band_chol: one warp; the (w+1)-row window lives in a 64 x 64 shared-memory ring
+//     (row r, column c at [r & 63][c & 63]); rows enter by cp.async 8 steps ahead.
+__global__ void k_form_h(int n, int b, const double* __restrict__ bands, const double* slots, double* Hb) {
+    const double sA = slots[5];   // sqrt(c0) / alpha
+    const double s2 = sA * sA;
+    const int w = 2 * b;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * (w + 1);
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int d = (int)(idx / n), i = (int)(idx % n), j = i + d;   // H(j, i), j >= i
+        double h = 0.0;
+        if (j < n) {
+            const int m0 = max(0, j - b), m1 = min(n - 1, i + b);
+            for (int m = m0; m <= m1; ++m) {
+                const int dj = j >= m ? j - m : m - j, di = i >= m ? i - m : m - i;
+                h = fma(bands[boff(n, dj) + min(j, m)], bands[boff(n, di) + min(i, m)], h);
+            }
+            h = s2 * h + (d == 0 ? 1.0 : 0.0);
+        }
+        Hb[idx] = h;
+    }
+}
+
+constexpr int BC_RING = 64, BC_LD = 65, BC_AHEAD = 8;
+__global__ void __launch_bounds__(32) k_band_chol(int n, int b, const double* __restrict__ Hb, double* rdiag,
+                                                 unsigned* status) {
+    __shared__ double S[BC_RING * BC_LD];
+    __shared__ double sL[33];
+    const int lane = threadIdx.x;
+    const int w = 2 * b;
+    auto slot = [&](int r, int c) -> double& { return S[(r & (BC_RING - 1)) * BC_LD + (c & (BC_RING - 1))]; };
+    // row r of the window: entries c in [r - w, r]
+    auto load_row = [&](int r) {
+        if (r < n)
+            for (int q = lane; q <= w; q += 32) {
+                const int c = r - w + q;
+                if (c >= 0) {
+                    const unsigned dst = (unsigned)__cvta_generic_to_shared(&slot(r, c));
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(Hb + (long long)(r - c) * n + c)
+                                 : "memory");
+                }
+            }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    for (int r = 0; r <= w + BC_AHEAD; ++r) load_row(r);
+    bool fail = false;
+    for (int k = 0; k < n; ++k) {
+        // rows up to k + w have landed (groups issued: rows 0 .. k + w + AHEAD)
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(BC_AHEAD) : "memory");
+        __syncwarp();
+        double d = slot(k, k);
+        if (!(d > 0.0)) { fail = true; d = 1.0; }
+        double y;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+        y = fma(0.5 * y, fma(-d * y, y, 1.0), y);
+        y = fma(0.5 * y, fma(-d * y, y, 1.0), y);
+        double ljj = d * y;
+        ljj = fma(0.5 * y, fma(-ljj, ljj, d), ljj);
+        const int rmax = min(w, n - 1 - k);
+        double l = 0.0;
+        if (lane >= 1 && lane <= rmax) {
+            l = slot(k + lane, k) * y;
+            sL[lane] = l;
+            rdiag[(long long)lane * n + k] = l;          // R(k, k + lane) = L(k + lane, k)
+        }
+        if (w == 32 && rmax == 32 && lane == 0) {          // the 33rd row of a b = 16 window
+            const double l32 = slot(k + 32, k) * y;
+            sL[32] = l32;
+            rdiag[(long long)32 * n + k] = l32;
+        }
+        if (lane == 0) {
+            rdiag[k] = ljj;
+            for (int q = rmax + 1; q <= w; ++q) rdiag[(long long)q * n + k] = 0.0;
+        }
+        __syncwarp();
+        // trailing update of the window: row r = k + i, columns k+1 .. r
+        for (int i = 1 + lane; i <= rmax; i += 32) {
+            const double li = sL[i];
+            const int r = k + i;
+            for (int q = 1; q <= i; ++q) slot(r, k + q) = fma(-li, sL[q], slot(r, k + q));
+        }
+        __syncwarp();
+        load_row(k + w + 1 + BC_AHEAD);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (fail && lane == 0) atomicOr(status, ST_NPD);
+}
+
+static const bool g_first_givens = std::getenv("SPG_FIRST_GIVENS") != nullptr;   // A/B: the Givens sweep
+
 void launch_givens_reduce(int n, int b, const double* bands, const double* slots, double* work, double* rdiag,
-                          cudaStream_t st) {
+                          cudaStream_t st, unsigned* status) {
+    if (!g_first_givens && b <= 16 && n >= 2) {   // R = chol(s^2 A^2 + I)^T (see k_band_chol)
+        const long long tot = (long long)n * (2 * b + 1);
+        k_form_h<<<(int)std::min<long long>(4096, (tot + 255) / 256), 256, 0, st>>>(n, b, bands, slots, work);
+        SPG_LAUNCH_CHECK();
+        k_band_chol<<<1, 32, 0, st>>>(n, b, work, rdiag, status);
+        SPG_LAUNCH_CHECK();
+        return;
+    }
     if (b == 1 && n >= 2) {   // tridiagonal: k_tri.cu
         launch_givens_tri(n, bands, slots, rdiag, st);
         return;

@@ -180,6 +180,6 @@ void launch_est_l0_tri(int n, const double* bands, const double* alpha, double* 
 void launch_givens_tri(int n, const double* bands, const double* slots, double* rdiag, cudaStream_t st);
 // work: n*(3b+1) + 2n + n*max(b-1,1) doubles; slots[5] = sqrt(c0)/alpha
 void launch_givens_reduce(int n, int b, const double* bands, const double* slots, double* work, double* rdiag,
-                          cudaStream_t st);
+                          cudaStream_t st, unsigned* status);
 
 }  // namespace spg
