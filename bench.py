@@ -57,6 +57,12 @@ def cpu_scale_factor():
     return f, f"model n*log2(n/n_min)^2 ratio {f:.2f}"
 
 
+def metric_name(cfg):
+    """The BASELINE metric (projector wall time) on the configuration being run."""
+    kind = "tridiagonal dimer chain" if cfg["b"] == 1 else f"banded b={cfg['b']}"
+    return f"hqdwh projector time (n={cfg['n']} {kind}, t2={cfg['t2']})"
+
+
 def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -177,7 +183,7 @@ def bench_reference(args, cfg):
     sample = (f"reference hqdwh (unmodified /root/reference headers, oracle/_ref) on the same dimer-chain family "
               f"at n={CPU_SAMPLE['n']} (t2={CPU_SAMPLE['t2']}, leaf {CPU_SAMPLE['nmin']}, eps {CPU_SAMPLE['eps']}): "
               f"mean {statistics.mean(times):.2f} s over {len(times)} runs, scaled to n={cfg['n']} by {how}")
-    out = {"metric": "hqdwh projector time (n=65536 tridiagonal dimer chain, t2=0.999)", "value": v, "unit": "s",
+    out = {"metric": metric_name(cfg), "value": v, "unit": "s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded dimer chain, SURVEY.md §8d)", "impl": "reference",
@@ -290,7 +296,7 @@ def bench_ours(args, cfg):
                    "sample": f"reference hqdwh (oracle/_ref) on the n={CPU_SAMPLE['n']} t2={CPU_SAMPLE['t2']} "
                              f"dimer chain: {times[0]:.2f} s on 1 host core, scaled by {how}"}
     out = {
-        "metric": "hqdwh projector time (n=65536 tridiagonal dimer chain, t2=0.999)",
+        "metric": metric_name(cfg),
         "value": value, "unit": "s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
         "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded dimer chain, SURVEY.md §8d)",
