@@ -51,6 +51,31 @@ __device__ __forceinline__ double csum(double v) {
     return v;
 }
 
+// all-reduce of 4 values across the warp by recursive halving (10 double shuffles
+// instead of 20); every lane ends with the four sums (fixed order: deterministic)
+__device__ __forceinline__ void warp_allreduce4(double (&v)[4]) {
+    const int lane = threadIdx.x & 31;
+    double h2[2], h1;
+    {
+        const bool lo = !(lane & 16);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double keep = lo ? v[i] : v[i + 2], send = lo ? v[i + 2] : v[i];
+            h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+    }
+    {
+        const bool lo = !(lane & 8);
+        const double keep = lo ? h2[0] : h2[1], send = lo ? h2[1] : h2[0];
+        h1 = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 4);
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = __shfl_sync(0xffffffffu, h1, ((c >> 1) & 1) * 16 + (c & 1) * 8);
+}
+
 __device__ __forceinline__ int core_kin(const TTask& t) {
     int k = 0;
     for (int g = 0; g < t.ng; ++g) k += t.g[g].kp ? *t.g[g].kp : t.g[g].kc;
@@ -537,10 +562,7 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         double d[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) d[m] = v0 * a0[m] + v1 * a1[m];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int m = 0; m < 4; ++m) d[m] += __shfl_xor_sync(0xffffffffu, d[m], o);
+        warp_allreduce4(d);
         bool redo = false;
         double ns[4];
 #pragma unroll
@@ -741,10 +763,7 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
                 double d[4];
 #pragma unroll
                 for (int m = 0; m < 4; ++m) d[m] = v0 * x0[m] + v1 * x1[m];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) d[m] += __shfl_xor_sync(0xffffffffu, d[m], o);
+                warp_allreduce4(d);
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const double w = tau * d[m];
