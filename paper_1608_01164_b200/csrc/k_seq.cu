@@ -257,10 +257,336 @@ __global__ void __launch_bounds__(32) k_est_l0_w(int n, int b, const double* __r
     }
 }
 
+// ------------------------------------------------------------ l0 for 2 <= b <= 16, register-resident
+// estimate_l0 / hager_norm1 / BandedLu (estimates.hpp:40-80, banded_lu.hpp:16-93), same
+// arithmetic order per entry as the reference, organised for one SM:
+//   factor: 64 threads, thread t owns the window columns c = t (mod 64); a column holds its
+//     b+1 active rows in registers (row k+i in reg[i] at step k).  Per step the owner of
+//     column k picks the pivot, swaps, forms the multipliers and publishes them (shared
+//     memory, double-buffered by step parity); every other column of the window applies
+//     the interchange and its rank-1 update in registers, stores U(k, c) and shifts.
+//   solves: warp 0, element j on lane j mod 32 (rotating window, no data movement), the
+//     needed columns of the factor staged 32 at a time through shared memory by cp.async.
+constexpr int EB_B = 16, EB_CH = 32;
+__device__ __forceinline__ double eb_a(const double* bands, int n, int b, double ia, int r, int c) {
+    if (r < 0 || c < 0 || r >= n || c >= n) return 0.0;
+    const int d = r >= c ? r - c : c - r;
+    return d <= b ? bands[boff(n, d) + (r < c ? r : c)] * ia : 0.0;
+}
+struct EbStage {   // 32 consecutive columns [c0, c0 + 32) of lu (ld wd) + invd / piv / a vector, cp.async
+    double* lu;
+    double* aux;   // 2 x 32 doubles
+    int* ip;       // 32 ints
+};
+__device__ __forceinline__ void eb_cpa(void* dst, const void* src, int bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+
+__global__ void __launch_bounds__(64) k_est_l0_band(int n, int b, const double* __restrict__ bands,
+                                                   const double* alpha_p, double* lu, int* piv, double* vecs,
+                                                   double* out, unsigned* status) {
+    __shared__ double sM[2][EB_B + 2];
+    __shared__ int sP[2];
+    __shared__ double sRed[2];
+    __shared__ int sSing;
+    __shared__ double sLu[3][EB_CH * (3 * EB_B + 1)];
+    __shared__ double sAux[3][2][EB_CH];
+    __shared__ int sPiv[3][EB_CH];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double alpha = *alpha_p, ia = 1.0 / alpha;
+    const int wd = 3 * b + 1, b2 = 2 * b;
+    double* invd = vecs;                       // 1 / U(j, j)
+    double* x = vecs + n;
+    double* y = vecs + 2 * (size_t)n;
+    double* z = vecs + 3 * (size_t)n;
+    double* t1 = vecs + 4 * (size_t)n;
+    // ---- norm1 (banded.hpp:94-106) -> n1 = |A|_1 / alpha
+    double m = 0.0;
+    for (int i = tid; i < n; i += 64) {
+        double cs = fabs(bands[i]);
+        for (int d = 1; d <= b; ++d) {
+            const double* dg = bands + boff(n, d);
+            if (i + d < n) cs += fabs(dg[i]);
+            if (i - d >= 0) cs += fabs(dg[i - d]);
+        }
+        m = fmax(m, cs);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) sRed[warp] = m;
+    if (tid == 0) sSing = 0;
+    __syncthreads();
+    const double n1 = fmax(sRed[0], sRed[1]) / alpha;
+    if (tid == 0) g_seq_trace[5] = clock64();
+    // ---- factor (banded_lu.hpp:66-88)
+    // band rows of A / alpha staged ahead in a shared ring: sRow[r % EB_RING][c - r + b] = A(r, c)
+    constexpr int EB_RING = 16;
+    __shared__ double sRow[EB_RING][2 * EB_B + 1];
+    auto stage_row = [&](int r) {
+        if (tid <= 2 * b) {
+            const int c = r - b + tid;
+            double* dst = &sRow[r % EB_RING][tid];
+            if (r < n && c >= 0 && c < n) {
+                const int d = r >= c ? r - c : c - r;
+                eb_cpa(dst, bands + boff(n, d) + (r < c ? r : c), 8);
+            } else {
+                *dst = 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    constexpr int EB_AHEAD = 8;
+    for (int q = 0; q < EB_AHEAD; ++q) stage_row(1 + b + q);   // rows needed at steps 0 .. AHEAD-1
+    double reg[EB_B + 1];
+    int mycol = tid;
+    {
+        const int k0 = max(0, mycol - b2);
+#pragma unroll
+        for (int i = 0; i <= EB_B; ++i) reg[i] = i <= b ? eb_a(bands, n, b, ia, k0 + i, mycol) : 0.0;
+    }
+    for (int k = 0; k < n; ++k) {
+        const int par = k & 1;
+        const int bb = min(b, n - 1 - k);
+        stage_row(k + 1 + b + EB_AHEAD);   // row needed EB_AHEAD steps from now
+        if (tid == (k & 63)) {   // column k: pivot, interchange, multipliers
+            double best = fabs(reg[0]);
+            int po = 0;
+#pragma unroll
+            for (int i = 1; i <= EB_B; ++i)
+                { const double av = fabs(reg[i]); const bool t = i <= bb && av > best; best = t ? av : best; po = t ? i : po; }
+            piv[k] = k + po;
+            if (best == 0.0) sSing = 1;
+            double top = reg[0];
+#pragma unroll
+            for (int i = 1; i <= EB_B; ++i)
+                { const double ri = reg[i]; reg[i] = i == po ? top : ri; top = i == po ? ri : top; }   // branch-free: keeps reg[] in registers
+            const double inv = best == 0.0 ? 0.0 : 1.0 / top;
+            lu[(long long)k * wd + b2] = top;
+            invd[k] = inv;
+#pragma unroll
+            for (int i = 1; i <= EB_B; ++i) {
+                const double mm = i <= bb ? reg[i] * inv : 0.0;
+                sM[par][i] = mm;
+                if (i <= bb) lu[(long long)k * wd + b2 + i] = mm;
+            }
+            sP[par] = po;
+        }
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(EB_AHEAD) : "memory");   // row k + 1 + b landed
+        __syncthreads();
+        const int po = sP[par];
+        if (mycol > k && mycol <= k + b2 + 1 && mycol < n && mycol == k + b2 + 1) {
+            // the step before the column enters: only its newest row arrives (rows above are zero)
+            const int rn = k + 1 + b, dc = mycol - rn + b;
+            const double an = (rn < n && dc >= 0 && dc <= 2 * b) ? sRow[rn % EB_RING][dc] * ia : 0.0;
+#pragma unroll
+            for (int i = 0; i <= EB_B; ++i)
+                reg[i] = i == b ? an : reg[i];
+        } else if (mycol > k && mycol <= k + b2 && mycol < n) {
+            double top = reg[0];
+#pragma unroll
+            for (int i = 1; i <= EB_B; ++i)
+                { const double ri = reg[i]; reg[i] = i == po ? top : ri; top = i == po ? ri : top; }   // branch-free: keeps reg[] in registers
+            lu[(long long)mycol * wd + (k - mycol + b2)] = top;   // U(k, mycol)
+#pragma unroll
+            for (int i = 1; i <= EB_B; ++i) {
+                const double mm = sM[par][i];
+                reg[i] = (i <= bb && mm != 0.0) ? reg[i] - mm * top : reg[i];
+            }
+            // shift: rows k+1 .. k+b+1
+#pragma unroll
+            for (int i = 0; i < EB_B; ++i) reg[i] = reg[i + 1];
+            const int rn = k + 1 + b, dc = mycol - rn + b;
+            const double an = (rn < n && dc >= 0 && dc <= 2 * b) ? sRow[rn % EB_RING][dc] * ia : 0.0;
+#pragma unroll
+            for (int i = 0; i <= EB_B; ++i)
+                reg[i] = i == b ? an : reg[i];
+        }
+        if (tid == (k & 63)) {   // retire column k, take column k + 64 (enters at step k + 64 - 2b;
+            mycol += 64;         // its first nonzero row arrives from the ring the step before)
+#pragma unroll
+            for (int i = 0; i <= EB_B; ++i) reg[i] = 0.0;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) g_seq_trace[6] = clock64();
+    if (sSing) {
+        if (tid == 0) { atomicOr(status, ST_SINGULAR); out[0] = 0.0; }
+        return;
+    }
+    if (warp != 0) return;
+    // ---- Hager (estimates.hpp:40-68) with the BandedLu solves on warp 0
+    const int nch = (n + EB_CH - 1) / EB_CH;
+    // chunk q = columns [32q, 32q + 32) of lu (+ invd, piv, an optional vector) into slot q % 3
+    auto stage = [&](int q, const double* v) {
+        if (q >= 0 && q < nch) {
+            const int sl = q % 3, c0 = q * EB_CH, cols = min(EB_CH, n - c0);
+            for (int e = lane; e < cols * wd; e += 32) eb_cpa(&sLu[sl][e], lu + (long long)c0 * wd + e, 8);
+            if (lane < cols) {
+                eb_cpa(&sAux[sl][0][lane], invd + c0 + lane, 8);
+                if (v) eb_cpa(&sAux[sl][1][lane], v + c0 + lane, 8);
+                eb_cpa(&sPiv[sl][lane], piv + c0 + lane, 4);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto wait_but1 = [&]() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); __syncwarp(); };
+    auto wait_all = [&]() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); __syncwarp(); };
+    // entry (r, c) of the factor, column c staged
+    auto F = [&](int c, int r) -> double { return sLu[(c >> 5) % 3][(c & 31) * wd + (r - c + b2)]; };
+    // y = A^{-1} v (BandedLu::solve): L forward with the interchanges into t1, U backward into yo
+    auto solve = [&](const double* v, double* yo) {
+        double xv = lane < n ? v[lane] : 0.0;   // lane e: element j = e (mod 32), j in [k, k + 31]
+        stage(0, v);
+        stage(1, v);
+        for (int q = 0; q < nch; ++q) {
+            stage(q + 2, v);
+            wait_but1();
+            const int sl = q % 3;
+            const int kend = min(n, (q + 1) * EB_CH);
+            for (int k = q * EB_CH; k < kend; ++k) {
+                const int a = k & 31, pp = sPiv[sl][a] & 31;
+                xv = __shfl_sync(0xffffffffu, xv, lane == a ? pp : (lane == pp ? a : lane));
+                const double xk = __shfl_sync(0xffffffffu, xv, a);
+                const int d = (lane - k) & 31;
+                if (d >= 1 && d <= b && k + d < n) xv -= F(k, k + d) * xk;
+                if (lane == a) {   // the lane takes element k + 32 (staged: no global latency on the chain)
+                    t1[k] = xk;
+                    xv = k + 32 < n ? sAux[((k + 32) >> 5) % 3][1][a] : 0.0;
+                }
+            }
+            __syncwarp();
+        }
+        wait_all();
+        {   // lane e: element in [n - 32, n - 1]
+            const int e = (n - 1) - ((n - 1 - lane) & 31);
+            xv = e >= 0 ? t1[e] : 0.0;
+        }
+        stage(nch - 1, t1);
+        stage(nch - 2, t1);
+        for (int qq = 0; qq < nch; ++qq) {
+            const int q = nch - 1 - qq;
+            stage(q - 2, t1);
+            wait_but1();
+            for (int j = min(n, (q + 1) * EB_CH) - 1; j >= q * EB_CH; --j) {
+                const int a = j & 31;
+                const double xj = __shfl_sync(0xffffffffu, xv, a) * sAux[q % 3][0][a];
+                if (lane != a) {
+                    const int r = j - ((j - lane) & 31);
+                    if (r >= j - b2 && r >= 0) xv -= F(j, r) * xj;
+                } else {
+                    yo[j] = xj;
+                    const int rn = j - 32;
+                    double nv = rn >= 0 ? sAux[(rn >> 5) % 3][1][rn & 31] : 0.0;
+                    if (rn >= 0 && rn >= j - b2) nv -= F(j, rn) * xj;
+                    xv = nv;
+                }
+            }
+            __syncwarp();
+        }
+        wait_all();
+    };
+    // y = A^{-T} v (BandedLu::solve_transposed): U^T forward (sums pushed to the pending
+    // elements) into t1, then L^T backward (dot over the next b, then the interchange) into yo
+    auto solve_t = [&](const double* v, double* yo) {
+        double acc = 0.0;   // lane e: pending sum of its element in [j, j + 31]
+        stage(0, v);
+        stage(1, v);
+        for (int q = 0; q < nch; ++q) {
+            stage(q + 2, v);
+            wait_but1();   // chunks q and q + 1 resident (U(j, r) for r <= j + 2b <= j + 32)
+            const int sl = q % 3;
+            const int jend = min(n, (q + 1) * EB_CH);
+            for (int j = q * EB_CH; j < jend; ++j) {
+                const int a = j & 31;
+                const double xj = __shfl_sync(0xffffffffu, (sAux[sl][1][a] - acc) * sAux[sl][0][a], a);
+                if (lane != a) {
+                    const int r = j + ((lane - j) & 31);
+                    if (r <= j + b2 && r < n) acc += F(r, j) * xj;   // U(j, r)
+                } else {
+                    t1[j] = xj;
+                    const int rn = j + 32;
+                    acc = (rn < n && rn <= j + b2) ? F(rn, j) * xj : 0.0;
+                }
+            }
+            __syncwarp();
+        }
+        wait_all();
+        acc = 0.0;   // L^T pass: lane e holds the current value of its element in [k, k + 31]
+        stage(nch - 1, t1);
+        stage(nch - 2, t1);
+        for (int qq = 0; qq < nch; ++qq) {
+            const int q = nch - 1 - qq;
+            stage(q - 2, t1);
+            wait_but1();
+            for (int k = min(n, (q + 1) * EB_CH) - 1; k >= q * EB_CH; --k) {
+                const int a = k & 31;
+                if (lane == a) {   // element k + 32 (final) leaves, element k enters
+                    if (k + 32 < n) yo[k + 32] = acc;
+                    acc = sAux[q % 3][1][a];
+                }
+                const int r = k + ((lane - k) & 31);
+                double part = (r > k && r <= k + b && r < n) ? F(k, r) * acc : 0.0;   // L(r, k) x[r]
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                if (lane == a) acc -= part;
+                const int pp = sPiv[q % 3][a] & 31;
+                acc = __shfl_sync(0xffffffffu, acc, lane == a ? pp : (lane == pp ? a : lane));
+            }
+            __syncwarp();
+        }
+        wait_all();
+        if (lane < n) yo[lane] = acc;   // window [0, 31]: final
+        __syncwarp();
+    };
+    for (int i = lane; i < n; i += 32) x[i] = 1.0 / n;
+    __syncwarp();
+    double est = 0.0;
+    for (int it = 0; it < 5; ++it) {
+        solve(x, y);
+        double e = 0.0;
+        for (int i = lane; i < n; i += 32) e += fabs(y[i]);
+        e = wsum32(e);
+        if (it > 0 && e <= est) break;
+        est = e;
+        for (int i = lane; i < n; i += 32) z[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+        __syncwarp();
+        solve_t(z, y);
+        double zmax = 0.0, ztx = 0.0;
+        int jm = 0x7fffffff;
+        for (int i = lane; i < n; i += 32) {
+            const double av = fabs(y[i]);
+            if (av > zmax) { zmax = av; jm = i; }
+            ztx += y[i] * x[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double oz = __shfl_xor_sync(0xffffffffu, zmax, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, jm, o);
+            if (oz > zmax || (oz == zmax && oj < jm)) { zmax = oz; jm = oj; }
+        }
+        ztx = wsum32(ztx);
+        if (jm == 0x7fffffff) jm = 0;
+        if (zmax <= ztx) break;
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) x[i] = i == jm ? 1.0 : 0.0;
+        __syncwarp();
+    }
+    if (lane == 0) { out[0] = n1 / (sqrt((double)n) * (n1 * est)); g_seq_trace[7] = clock64(); }
+}
+
+static const bool g_l0_window = std::getenv("SPG_L0_WINDOW") != nullptr;   // A/B: the windowed single-warp kernel
+
 void launch_estimate_l0(int n, int b, const double* bands, const double* alpha, double* lu_work, int* piv,
                         double* vecs, double* out_l0, unsigned* status, cudaStream_t st) {
     if (b == 1 && n >= 2) {   // tridiagonal: k_tri.cu (caller provides >= 9 n doubles at lu_work)
         launch_est_l0_tri(n, bands, alpha, lu_work, out_l0, status, st);
+        return;
+    }
+    if (b <= EB_B && !g_l0_window) {   // (caller provides >= 5 n doubles at vecs)
+        k_est_l0_band<<<1, 64, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status);
+        SPG_LAUNCH_CHECK();
         return;
     }
     k_est_l0_w<<<1, 32, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status);
