@@ -168,6 +168,10 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
         SPG_CUDA(cudaMalloc(&p, sizeof(double) * (size_t)n * KCAP));
         xpanels_.push_back(p);
     }
+    int max_leaf = 0;
+    for (int x = 0; x < tree_.nnodes(); ++x) if (tree_.leaf(x)) max_leaf = std::max(max_leaf, tree_.size[x]);
+    if (max_leaf > C4_LEAF_MAX)
+        SPG_CUDA(cudaMalloc(&leaf_scr_, sizeof(double) * (size_t)(TRM_NMAX / 2) * (TRM_NMAX / 2)));
     // device tree
     std::vector<int> tb = tree_.begin, ts = tree_.size, tl = tree_.left, tr = tree_.right, tv = tree_.level,
                      to = tree_.leaf_ord;
@@ -271,6 +275,7 @@ Engine::~Engine() {
     if (host_pinned_) cudaFreeHost(host_pinned_);
     for (double* p : chol_panels_) cudaFree(p);
     for (double* p : xpanels_) cudaFree(p);
+    if (leaf_scr_) cudaFree(leaf_scr_);
     for (auto& e : events_) cudaEventDestroy(e);
     arena_.reset();
     ws_.reset();
@@ -944,11 +949,39 @@ void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU,
     side_sel_ = -1;
 }
 
+// Leaves above the fast leaf kernel's size (C4_LEAF_MAX < s <= TRM_NMAX, s % 64 == 0) as a
+// 2x2 block Cholesky: W11 = chol(M11); W12 = W11^{-T} M21^T (DMMA row-strip TRSM);
+// S = M22 - W12^T W12 (DMMA GEMM); W22 = chol(S).  Same factor as the unblocked
+// recursion of cholesky.hpp up to summation order (SPG_CHOL_SPLIT_OFF=1: one kernel).
+static const bool g_no_split = std::getenv("SPG_CHOL_SPLIT_OFF") != nullptr;
+
+void Engine::leaf_chol_split(Plan& p, const double* Ml, double* Wl, double* D, int s) {
+    const int h = s / 2;
+    unsigned* status = sc_.status;
+    double* S = leaf_scr_;
+    const CholItem* c1 = arena_->push(std::vector<CholItem>{CholItem{Ml, Wl, h, s, s, D, nullptr, 1}});
+    const CholItem* c2 = arena_->push(std::vector<CholItem>{
+        CholItem{S, Wl + h + (size_t)h * s, h, h, s, D + (size_t)(h / 32) * 1024, nullptr, 1}});
+    const TrsmItem* tr = arena_->push(std::vector<TrsmItem>{TrsmItem{Wl, Wl + (size_t)h * s, h, s, s, nullptr, h, 0, 0, D}});
+    push_timed(p, PC_LEAF, [=](cudaStream_t st) {
+        launch_leaf_split_prep(Ml, Wl, S, s, h, st);
+        launch_leaf_cholesky(c1, 1, status, st, h);
+        launch_leaf_trsm_rows(tr, 1, h, h, st);
+    });
+    gemm(p, {gitem(Wl + (size_t)h * s, s, 1, Wl + (size_t)h * s, s, 0, S, h, h, nullptr, h, nullptr, h, nullptr, -1.0, 1.0)},
+         {make_int3(h, h, h)});
+    push_timed(p, PC_LEAF, [=](cudaStream_t st) { launch_leaf_cholesky(c2, 1, status, st, h); });
+}
+
 void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     const int n = tree_.n;
     if (tree_.leaf(x)) {
         if (chol_deferred_ && last_leaf_ev_[x] >= 0) wait(p, last_leaf_ev_[x]);
         const int s = tree_.size[x];
+        if (s > C4_LEAF_MAX && s <= TRM_NMAX && s % 64 == 0 && leaf_scr_ && !g_no_split) {
+            leaf_chol_split(p, M.leaf(x), W.leaf(x), W.leaf_dinv(x), s);
+            return;
+        }
         std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s, W.leaf_dinv(x), nullptr, 1}};   // W memset above
         const CholItem* d = arena_->push(ci);
         unsigned* status = sc_.status;

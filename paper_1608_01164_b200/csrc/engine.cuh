@@ -225,8 +225,10 @@ private:
     int ev_base2_ = 0;                  // event slots: x-ready(x) = ev_base2_ + x, w12-done(x) = ev_base2_ + nn + x
     int wtr_last_ev_ = -1;              // latest W12 truncation event (FIFO stream: covers all earlier ones)
     std::vector<double*> xpanels_;      // per-depth untruncated W11^{-T} M12.U panels
+    double* leaf_scr_ = nullptr;        // Schur block of a split leaf Cholesky (main stream only)
     std::vector<int> last_leaf_ev_, last_block_ev_;   // latest side-stream event touching a leaf / block
     void cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU, const double* QV, const int* qrank);
+    void leaf_chol_split(Plan& p, const double* Ml, double* Wl, double* D, int s);
     std::unique_ptr<Arena> arena_;
     std::unique_ptr<Workspace> ws_;
     DevTree dtree_{};

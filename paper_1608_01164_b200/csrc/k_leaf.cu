@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
 //                       (K < J-32 from W in L2, K in [J-32, J) from prv)
 //   (c) warps 0-3: cur[32:64] <- cur[32:64] D_J  (the rows the next (a) needs)
 // Same arithmetic contract as cholesky_upper (dense_factor.hpp:201-223): W = L^T.
-constexpr int C4_NMAX = 256, C4_THREADS = 384, C4_NW = C4_THREADS / 32, C4_HELP = C4_NW - 2;
+constexpr int C4_NMAX = C4_LEAF_MAX, C4_THREADS = 384, C4_NW = C4_THREADS / 32, C4_HELP = C4_NW - 2;
 constexpr int C4_DP = 36;   // pitch of the D tiles (conflict-free m8n8k4 B-fragment reads)
 __host__ __device__ inline int c4_ldp(int n) { return ((n + 15) / 16) * 16 + 4; }
 static size_t chol4_smem(int n) {
@@ -1153,6 +1153,34 @@ void launch_leaf_trsm_rows(const TrsmItem* d, int nitems, int maxn, int maxrhs, 
     if (!nitems) return;
     dim3 g((maxrhs + TRM_RS - 1) / TRM_RS, nitems);
     k_leaf_trsm_rows<<<g, TRM_THREADS, trm_smem(maxn), st>>>(d);
+    SPG_LAUNCH_CHECK();
+}
+
+// Two-by-two split of a large leaf's Cholesky (h = n / 2): W12 <- M21^T (the lower
+// triangle is the reference's input, cholesky.hpp reads it), S <- M22.  32x32 tiles,
+// transposed through shared memory so both sides are coalesced.
+__global__ void __launch_bounds__(256) k_leaf_split_prep(const double* __restrict__ M, double* __restrict__ W,
+                                                       double* __restrict__ S, int n, int h) {
+    __shared__ double t[32][33];
+    const int bi = blockIdx.x * 32, bj = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int h2 = n - h;
+    for (int r = ty; r < 32; r += 8) {   // M21 tile: rows h + bj + tx, column bi + r
+        const int i = h + bj + tx, j = bi + r;
+        t[tx][r] = (bj + tx < h2 && j < h) ? M[i + (long long)j * n] : 0.0;
+        const int a = bi + tx, b = bj + r;   // S(a, b) = M22(a, b), a, b < h2 (grid covers h2 x h2 when h2 >= h)
+        if (a < h2 && b < h2) S[a + (long long)b * h2] = M[(h + a) + (long long)(h + b) * n];
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {   // W(bi + tx, h + bj + r) = M21(bj + r, bi + tx)
+        const int i = bi + tx, j = bj + r;
+        if (i < h && j < h2) W[i + (long long)(h + j) * n] = t[r][tx];
+    }
+}
+
+void launch_leaf_split_prep(const double* M, double* W, double* S, int n, int h, cudaStream_t st) {
+    const int g = (std::max(h, n - h) + 31) / 32;
+    k_leaf_split_prep<<<dim3(g, g), 256, 0, st>>>(M, W, S, n, h);
     SPG_LAUNCH_CHECK();
 }
 

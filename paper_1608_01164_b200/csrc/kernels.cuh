@@ -128,7 +128,10 @@ void launch_leaf_trsm(const TrsmItem* d, const int2* d_ctas, int nctas, unsigned
 // leaves with n % 32 == 0, n <= TRM_NMAX, D present, X row-major RHS (rhs_t = 1) viewed as
 // X <- X W^{-1} (mode 0) / X W^{-T} (mode 1) on a column-major leaf; DMMA, one CTA per 32 rows
 constexpr int TRM_NMAX = 576;
+constexpr int C4_LEAF_MAX = 256;   // largest leaf of the single-kernel fast leaf Cholesky (k_leaf_chol4)
 void launch_leaf_trsm_rows(const TrsmItem* d, int nitems, int maxn, int maxrhs, cudaStream_t st);
+// leaf Cholesky split (h = n / 2): W12 <- M21^T and S <- M22 (ld n - h)
+void launch_leaf_split_prep(const double* M, double* W, double* S, int n, int h, cudaStream_t st);
 
 // ------------------------------------------------------------ HODLR subtree solves
 struct DevTree {

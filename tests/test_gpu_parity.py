@@ -222,6 +222,20 @@ def test_hqdwh_vs_reference_dense(reflib):
         reflib.L.ref_result_free(ref["handle"])
 
 
+def test_hqdwh_split_leaves_vs_reference(reflib):
+    # leaves above 256 (320, 512): the leaf Cholesky runs as a 2x2 block split
+    for n, t2, nmin, b in [(2560, 0.9, 320, 1), (4096, 0.95, 512, 8)]:
+        A = S.dimer_chain(n, 1.0, t2, 0.2 * (1 - t2), 23, b=b, s=0.02 / (2 * b + 1)) if b > 1 else \
+            S.dimer_chain(n, 1.0, t2, 0.2 * (1 - t2), 23)
+        r = S.hqdwh(A, nmin, 1e-10)
+        ref = reflib.hqdwh(A.bands, nmin, 1e-10)
+        Pr = reflib.to_dense(ref["P"], n)
+        assert r.iterations == ref["iterations"]
+        D = r.P.to_dense() - Pr
+        assert np.abs(np.linalg.eigvalsh(0.5 * (D + D.T))).max() <= 1e-8
+        reflib.L.ref_result_free(ref["handle"])
+
+
 def test_smallgap_config(golden_dir):
     # BASELINE config 2: n=16384, t2=0.999, leaf 256, eps 1e-10 (randomized norms above dense scale)
     g = load(golden_dir, "smallgap")
