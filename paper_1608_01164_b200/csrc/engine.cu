@@ -218,7 +218,8 @@ void Engine::push_timed(Plan& p, int cls, Launch l) {
     cudaEvent_t a, b;
     SPG_CUDA(cudaEventCreate(&a));
     SPG_CUDA(cudaEventCreate(&b));
-    prof_.push_back({cls, cur_op_, a, b});
+    prof_.push_back({cls, cur_op_, a, b, prof_ntask_, prof_rows_});
+    prof_ntask_ = prof_rows_ = 0;
     push(p, [a](cudaStream_t s) { SPG_CUDA(cudaEventRecord(a, s)); });
     push(p, std::move(l));
     push(p, [b](cudaStream_t s) { SPG_CUDA(cudaEventRecord(b, s)); });
@@ -256,6 +257,21 @@ void Engine::prof_sum(double* ms, long long* nb) const {
         for (const auto& kv : agg)
             std::fprintf(stderr, "prof op=%d cls=%s ms=%.2f batches=%d\n", kv.first.first, cn[kv.first.second],
                          kv.second.first, kv.second.second);
+        // truncation batches by (max rows, task count) buckets
+        std::map<std::pair<int, int>, std::pair<double, int>> tb;
+        for (const auto& r : prof_) {
+            if (r.cls != PC_TRUNC) continue;
+            float t = 0.f;
+            SPG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+            int nt = 1;
+            while (nt < r.ntask) nt *= 2;
+            auto& e = tb[{r.rows, nt}];
+            e.first += t;
+            e.second += 1;
+        }
+        for (const auto& kv : tb)
+            std::fprintf(stderr, "trunc rows=%d ntask<=%d ms=%.2f batches=%d avg_us=%.1f\n", kv.first.first,
+                         kv.first.second, kv.second.first, kv.second.second, 1e3 * kv.second.first / kv.second.second);
     }
 }
 
@@ -333,6 +349,11 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     double* ws = wsp.base();
     const double eps = eps_;
     unsigned* status = sc_.status;
+    if (profile_) {
+        prof_ntask_ = (int)tasks.size();
+        prof_rows_ = 0;
+        for (const auto& t : tasks) prof_rows_ = std::max(prof_rows_, std::max(t.p, t.s));
+    }
     push_timed(p, PC_TRUNC, [b, ws, eps, status](cudaStream_t st) { launch_truncate(b, ws, eps, status, st); });
     wsp.release(mark);
 }

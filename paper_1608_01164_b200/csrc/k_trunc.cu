@@ -143,10 +143,19 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                 for (int jj = 0; jj < TS_NB; ++jj) {
                     if (jj >= nb) break;
                     const int j = j0 + jj;
-                    double s2 = 0.0;
+                    // one reduction per column: d[jj] = |x_jj|^2, d[c] = x_jj . x_c (c != jj); the
+                    // reflector v_jj = scal x_jj, so v_jj . x_c = scal d[c] (c > jj: panel update,
+                    // c < jj: x_c = v_c, the T column's Gram entries)
+                    double d[TS_NB];
 #pragma unroll
-                    for (int t = 0; t < SB / 32; ++t) s2 += x[jj][t] * x[jj][t];
-                    s2 = warp_sum(s2);
+                    for (int c = 0; c < TS_NB; ++c) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int t = 0; t < SB / 32; ++t) s += x[jj][t] * x[c][t];
+                        d[c] = s;
+                    }
+                    warp_allreduce8(d);
+                    const double s2 = d[jj];
                     const double alpha = sR[j + j * KIN_MAX];
                     double tau = 0.0, scal = 0.0;
                     if (s2 > 0.0) {
@@ -159,17 +168,8 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                     }
 #pragma unroll
                     for (int t = 0; t < SB / 32; ++t) x[jj][t] *= scal;   // scal = 0 -> v = 0
-                    // d[c] = v_jj . x_c (c > jj, panel update) and g[a] = v_a . v_jj (a < jj, T column)
-                    double d[TS_NB];
 #pragma unroll
-                    for (int c = 0; c < TS_NB; ++c) {
-                        double s = 0.0;
-                        if (c != jj)
-#pragma unroll
-                            for (int t = 0; t < SB / 32; ++t) s += x[jj][t] * x[c][t];
-                        d[c] = s;
-                    }
-                    warp_allreduce8(d);
+                    for (int c = 0; c < TS_NB; ++c) d[c] *= scal;
                     double rjc[TS_NB];
 #pragma unroll
                     for (int c = 0; c < TS_NB; ++c) rjc[c] = (c > jj && c < nb) ? sR[j + (j0 + c) * KIN_MAX] : 0.0;
