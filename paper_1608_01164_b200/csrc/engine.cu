@@ -91,7 +91,9 @@ void DHodlr::alloc(const HTree& tree, Arena& arena) {
     t = &tree;
     leaf_off.clear();
     long long off = 0;
-    for (int id : tree.leaves) { leaf_off.push_back(off); off += (long long)tree.size[id] * tree.size[id]; }
+    // every leaf starts on a 32-byte boundary (odd leaf sizes: the vector loads of the
+    // leaf kernels need 16-byte aligned rows of even leading dimension and block bases)
+    for (int id : tree.leaves) { leaf_off.push_back(off); off += ((long long)tree.size[id] * tree.size[id] + 3) & ~3LL; }
     leaf_doubles = off;
     slab_doubles = (size_t)std::max(tree.depth, 1) * KCAP * tree.n;
     SPG_CUDA(cudaMalloc(&leaves, sizeof(double) * (leaf_doubles + 2 * slab_doubles)));
@@ -170,7 +172,7 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     }
     int max_leaf = 0;
     for (int x = 0; x < tree_.nnodes(); ++x) if (tree_.leaf(x)) max_leaf = std::max(max_leaf, tree_.size[x]);
-    if (max_leaf > C4_LEAF_MAX)
+    if (max_leaf > C4_LEAF_MAX || std::getenv("SPG_CHOL_SPLIT_MIN"))
         SPG_CUDA(cudaMalloc(&leaf_scr_, sizeof(double) * (size_t)(TRM_NMAX / 2) * (TRM_NMAX / 2)));
     // device tree
     std::vector<int> tb = tree_.begin, ts = tree_.size, tl = tree_.left, tr = tree_.right, tv = tree_.level,
@@ -975,6 +977,8 @@ void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU,
 // S = M22 - W12^T W12 (DMMA GEMM); W22 = chol(S).  Same factor as the unblocked
 // recursion of cholesky.hpp up to summation order (SPG_CHOL_SPLIT_OFF=1: one kernel).
 static const bool g_no_split = std::getenv("SPG_CHOL_SPLIT_OFF") != nullptr;
+static const int g_split_min = std::getenv("SPG_CHOL_SPLIT_MIN") ? std::atoi(std::getenv("SPG_CHOL_SPLIT_MIN"))
+                                                                  : C4_LEAF_MAX + 1;   // smallest split leaf
 
 void Engine::leaf_chol_split(Plan& p, const double* Ml, double* Wl, double* D, int s) {
     const int h = s / 2;
@@ -999,7 +1003,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     if (tree_.leaf(x)) {
         if (chol_deferred_ && last_leaf_ev_[x] >= 0) wait(p, last_leaf_ev_[x]);
         const int s = tree_.size[x];
-        if (s > C4_LEAF_MAX && s <= TRM_NMAX && s % 64 == 0 && leaf_scr_ && !g_no_split) {
+        if (s >= g_split_min && s <= TRM_NMAX && s % 64 == 0 && leaf_scr_ && !g_no_split) {
             leaf_chol_split(p, M.leaf(x), W.leaf(x), W.leaf_dinv(x), s);
             return;
         }

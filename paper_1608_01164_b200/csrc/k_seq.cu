@@ -815,6 +815,152 @@ __global__ void __launch_bounds__(32) k_band_chol(int n, int b, const double* __
     if (fail && lane == 0) atomicOr(status, ST_NPD);
 }
 
+// w = 2 (tridiagonal A): the whole window is three scalars, so one thread runs the
+// recurrence in registers -- per row two FMAs, the refined rsqrt and two products --
+// with the band entries loaded 16 rows ahead (independent of the chain).  Same
+// operations in the same order as k_band_chol, so the factor is bitwise identical:
+//   d_k = h0_k - l2_{k-2}^2 - l1_{k-1}^2,  l1_k = (h1_k - l2_{k-1} l1_{k-1}) / L_kk,  l2_k = h2_k / L_kk
+constexpr int BC1_AHEAD = 16;
+__global__ void __launch_bounds__(32) k_band_chol_w2(int n, const double* __restrict__ Hb, double* rdiag,
+                                                    unsigned* status) {
+    if (threadIdx.x != 0) return;
+    double a0[BC1_AHEAD], a1[BC1_AHEAD], a2[BC1_AHEAD];
+#pragma unroll
+    for (int u = 0; u < BC1_AHEAD; ++u) {
+        a0[u] = u < n ? __ldcs(Hb + u) : 1.0;
+        a1[u] = u < n ? __ldcs(Hb + n + u) : 0.0;
+        a2[u] = u < n ? __ldcs(Hb + 2LL * n + u) : 0.0;
+    }
+    double l1p = 0.0, l2p = 0.0, l2pp = 0.0;   // l1_{k-1}, l2_{k-1}, l2_{k-2}
+    bool fail = false;
+    for (int k0 = 0; k0 < n; k0 += BC1_AHEAD) {
+#pragma unroll
+        for (int u = 0; u < BC1_AHEAD; ++u) {
+            const int k = k0 + u;
+            if (k < n) {
+                const double h0 = a0[u], h1 = a1[u], h2 = a2[u];
+                const int kn = k + BC1_AHEAD;
+                if (kn < n) {
+                    a0[u] = __ldcs(Hb + kn);
+                    a1[u] = __ldcs(Hb + n + kn);
+                    a2[u] = __ldcs(Hb + 2LL * n + kn);
+                }
+                double d = fma(-l1p, l1p, fma(-l2pp, l2pp, h0));
+                const double s1 = fma(-l2p, l1p, h1);
+                if (!(d > 0.0)) { fail = true; d = 1.0; }
+                double y;
+                asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+                y = fma(0.5 * y, fma(-d * y, y, 1.0), y);
+                y = fma(0.5 * y, fma(-d * y, y, 1.0), y);
+                double ljj = d * y;
+                ljj = fma(0.5 * y, fma(-ljj, ljj, d), ljj);
+                const double l1 = s1 * y, l2 = h2 * y;
+                rdiag[k] = ljj;
+                rdiag[(long long)n + k] = k + 1 < n ? l1 : 0.0;
+                rdiag[2LL * n + k] = k + 2 < n ? l2 : 0.0;
+                l2pp = l2p;
+                l2p = l2;
+                l1p = l1;
+            }
+        }
+    }
+    if (fail) atomicOr(status, ST_NPD);
+}
+
+// 2 < w <= 32: the window in registers, one row per lane.  Row r lives on lane r & 31
+// from the step it enters (r - W) until it is factored (step r), its entry for column
+// c in slot c & 31 (W = 32: the entering column r - 32 shares the slot with the
+// diagonal and is kept apart in `ent`).  With the step loop unrolled by 32 (u = k & 31
+// static) every slot index and shuffle source is a constant, so step k is one pivot
+// broadcast, the refined rsqrt, w broadcasts of L(k+q, k) and one FMA per live entry.
+// The band is padded to W in {4, 8, 16, 32} (zero entries stay zero).  Entering rows
+// are staged 32 at a time through a double-buffered shared-memory block by cp.async.
+// Same operations in the same order as k_band_chol: bitwise identical factor.
+template <int W>
+__global__ void __launch_bounds__(32) k_band_chol_reg(int n, int w, const double* __restrict__ Hb, double* rdiag,
+                                                     unsigned* status) {
+    constexpr int NS = W >= 16 ? 32 : 2 * W;   // register slots per row (> W; W = 32 keeps column r - 32 in `ent`)
+    constexpr int LD = W + 2;                  // sF[buf][row][delta]
+    __shared__ double sF[2][32 * LD];
+    const int lane = threadIdx.x;
+    auto issue_chunk = [&](int q) {
+        double* dst0 = sF[q & 1];
+        for (int idx = lane; idx < 32 * (W + 1); idx += 32) {
+            const int rr = idx & 31, dl = idx >> 5, r = 32 * q + rr, c = r - dl;
+            double* dst = dst0 + rr * LD + dl;
+            if (r < n && c >= 0 && dl <= w) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                             "l"(Hb + (long long)dl * n + c) : "memory");
+            } else {
+                *dst = 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    double e[NS], ent = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) e[s] = 0.0;
+    issue_chunk(0);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+    if (lane < W) {   // rows 0 .. W-1 (entering before step 0): e[c % NS] = H(lane, c)
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (c <= lane && lane - c <= W) e[c & (NS - 1)] = sF[0][lane * LD + (lane - c)];
+    }
+    if (n > 32) issue_chunk(1);
+    bool fail = false;
+    for (int k0 = 0; k0 < n; k0 += NS) {
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {   // slot of column k is u
+            const int k = k0 + u;
+            if (k >= n) break;
+            const int pl = k & 31;
+            double dk = __shfl_sync(0xffffffffu, e[u], pl);
+            if (!(dk > 0.0)) { fail = true; dk = 1.0; }
+            double y;
+            asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(dk));
+            y = fma(0.5 * y, fma(-dk * y, y, 1.0), y);
+            y = fma(0.5 * y, fma(-dk * y, y, 1.0), y);
+            double ljj = dk * y;
+            ljj = fma(0.5 * y, fma(-ljj, ljj, dk), ljj);
+            if (lane == pl) rdiag[k] = ljj;
+            {   // row k + W enters on lane (k + W) & 31 (W = 32: the pivot lane, after the broadcast)
+                const int r = k + W;
+                if ((r & 31) == 0 && r < n) {   // first row of chunk r / 32: wait for it, prefetch the next
+                    asm volatile("cp.async.wait_all;\n" ::: "memory");
+                    __syncwarp();
+                    if (r + 32 < n) issue_chunk(r / 32 + 1);
+                }
+                if (lane == (r & 31) && r < n) {
+                    const double* src = sF[(r >> 5) & 1] + (r & 31) * LD;
+#pragma unroll
+                    for (int dl = 0; dl <= W; ++dl) {
+                        const double v = src[dl];
+                        if (dl == 32) ent = v;
+                        else e[(u + W - dl) & (NS - 1)] = v;
+                    }
+                }
+            }
+            const int i = W == 32 && lane == pl ? 32 : ((lane - pl) & 31);   // my row is k + i
+            const bool live = i >= 1 && i <= W && k + i < n;
+            const double cv = (W == 32 && i == 32) ? ent : e[u];
+            const double li = live ? cv * y : 0.0;
+            if (i >= 1 && i <= w) rdiag[(long long)i * n + k] = li;
+            // trailing update: row k + i, columns k + q (q = 1 .. i): -= L(k+i, k) L(k+q, k)
+#pragma unroll
+            for (int q = 1; q <= W; ++q) {
+                const double lq = __shfl_sync(0xffffffffu, li, (pl + q) & 31);
+                if (q <= i && live) e[(u + q) & (NS - 1)] = fma(-li, lq, e[(u + q) & (NS - 1)]);
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (fail && lane == 0) atomicOr(status, ST_NPD);
+}
+
+static const bool g_band_chol_window = std::getenv("SPG_BAND_CHOL_WINDOW") != nullptr;   // A/B: the windowed kernel
+
 static const bool g_first_givens = std::getenv("SPG_FIRST_GIVENS") != nullptr;   // A/B: the Givens sweep
 
 void launch_givens_reduce(int n, int b, const double* bands, const double* slots, double* work, double* rdiag,
@@ -823,7 +969,13 @@ void launch_givens_reduce(int n, int b, const double* bands, const double* slots
         const long long tot = (long long)n * (2 * b + 1);
         k_form_h<<<(int)std::min<long long>(4096, (tot + 255) / 256), 256, 0, st>>>(n, b, bands, slots, work);
         SPG_LAUNCH_CHECK();
-        k_band_chol<<<1, 32, 0, st>>>(n, b, work, rdiag, status);
+        const int w = 2 * b;
+        if (g_band_chol_window) k_band_chol<<<1, 32, 0, st>>>(n, b, work, rdiag, status);
+        else if (w == 2) k_band_chol_w2<<<1, 32, 0, st>>>(n, work, rdiag, status);
+        else if (w <= 4) k_band_chol_reg<4><<<1, 32, 0, st>>>(n, w, work, rdiag, status);
+        else if (w <= 8) k_band_chol_reg<8><<<1, 32, 0, st>>>(n, w, work, rdiag, status);
+        else if (w <= 16) k_band_chol_reg<16><<<1, 32, 0, st>>>(n, w, work, rdiag, status);
+        else k_band_chol_reg<32><<<1, 32, 0, st>>>(n, w, work, rdiag, status);
         SPG_LAUNCH_CHECK();
         return;
     }

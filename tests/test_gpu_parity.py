@@ -236,6 +236,18 @@ def test_hqdwh_split_leaves_vs_reference(reflib):
         reflib.L.ref_result_free(ref["handle"])
 
 
+def test_odd_leaves_banded_first_iterate():
+    # odd leaf sizes (leaf storage alignment) and every band-Cholesky kernel width (b = 1..16)
+    for b, n, nmin in [(1, 3037, 128), (2, 3074, 128), (3, 3111, 100), (5, 1185, 64), (12, 1444, 90), (16, 1592, 128)]:
+        A = S.dimer_chain(n, 1.0, 0.8, 0.05, 100 + b, b=b, s=0.02 / (2 * b + 1))
+        r = S.hqdwh(A, nmin, 1e-10)
+        H = np.zeros((n, n))
+        for d in range(b + 1):
+            H += np.diag(A.bands[d], d) + (np.diag(A.bands[d], -d) if d else 0)
+        nneg = int((np.linalg.eigvalsh(H) < 0).sum())
+        assert round(r.P.trace()) == nneg and abs(r.P.trace() - nneg) < 1e-8, (b, n, r.P.trace(), nneg)
+
+
 def test_smallgap_config(golden_dir):
     # BASELINE config 2: n=16384, t2=0.999, leaf 256, eps 1e-10 (randomized norms above dense scale)
     g = load(golden_dir, "smallgap")
