@@ -104,6 +104,14 @@ __device__ __forceinline__ double* z_area(const TTask& t, double* ws, int side) 
 __device__ long long* g_tsqr_trace = nullptr;   // micro-benchmarks: clock64 per panel phase (CTA 0, sub-block 0)
 void set_tsqr_trace(long long* p) { SPG_CUDA(cudaMemcpyToSymbol(g_tsqr_trace, &p, sizeof(p))); }
 #define TSQR_TRACE(slot) do { if (g_tsqr_trace && b == 0 && blockIdx.x == 0 && threadIdx.x == 0) g_tsqr_trace[slot] = clock64(); } while (0)
+constexpr int LDB = SB + 4;   // leading dimension of the staged sub-block (conflict-free DMMA fragments)
+__device__ __forceinline__ void dmma_q(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+__constant__ int g_tsqr_v1_dev = 0;   // SPG_TSQR_V1=1: per-column trailing update (A/B checks)
+
 // Streaming Householder QR of the rows [r0, r0+nrows) of an implicit matrix with
 // k columns, starting from R = 0:  [0_k; A] = Q [R; 0].  Each 128-row sub-block
 // is folded into R by k reflectors y_j = [e_j; v_j] acting on (R row j, block
@@ -138,11 +146,19 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
 #pragma unroll
                 for (int a = 0; a < TS_NB; ++a)
 #pragma unroll
-                    for (int t = 0; t < SB / 32; ++t) x[a][t] = a < nb ? sB[(lane + 32 * t) + (j0 + a) * SB] : 0.0;
+                    for (int t = 0; t < SB / 32; ++t) x[a][t] = a < nb ? sB[(lane + 32 * t) + (j0 + a) * LDB] : 0.0;
 #pragma unroll
                 for (int jj = 0; jj < TS_NB; ++jj) {
                     if (jj >= nb) break;
                     const int j = j0 + jj;
+                    // R row j of the panel (untouched since the panel began) and this lane's row of
+                    // the panel T, loaded ahead of the reduction
+                    double rowv[TS_NB], tz[TS_NB];
+#pragma unroll
+                    for (int c = 0; c < TS_NB; ++c) {
+                        rowv[c] = (c >= jj && c < nb) ? sR[j + (j0 + c) * KIN_MAX] : 0.0;
+                        tz[c] = (c < jj && lane < TS_NB) ? Tp[lane + c * TS_NB] : 0.0;
+                    }
                     // one reduction per column: d[jj] = |x_jj|^2, d[c] = x_jj . x_c (c != jj); the
                     // reflector v_jj = scal x_jj, so v_jj . x_c = scal d[c] (c > jj: panel update,
                     // c < jj: x_c = v_c, the T column's Gram entries)
@@ -156,61 +172,63 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                     }
                     warp_allreduce8(d);
                     const double s2 = d[jj];
-                    const double alpha = sR[j + j * KIN_MAX];
-                    double tau = 0.0, scal = 0.0;
+                    const double alpha = rowv[jj];
+                    double tau = 0.0, scal = 0.0, beta = alpha;
                     if (s2 > 0.0) {
                         const double nrm = nr_sqrt(fma(alpha, alpha, s2));
-                        const double beta = alpha > 0.0 ? -nrm : nrm;
+                        beta = alpha > 0.0 ? -nrm : nrm;
                         tau = (beta - alpha) * nr_rcp(beta);
                         scal = nr_rcp(alpha - beta);
-                        __syncwarp();
-                        if (lane == 0) sR[j + j * KIN_MAX] = beta;
                     }
 #pragma unroll
                     for (int t = 0; t < SB / 32; ++t) x[jj][t] *= scal;   // scal = 0 -> v = 0
 #pragma unroll
                     for (int c = 0; c < TS_NB; ++c) d[c] *= scal;
-                    double rjc[TS_NB];
-#pragma unroll
-                    for (int c = 0; c < TS_NB; ++c) rjc[c] = (c > jj && c < nb) ? sR[j + (j0 + c) * KIN_MAX] : 0.0;
-                    __syncwarp();
+                    double rnew[TS_NB];
 #pragma unroll
                     for (int c = 0; c < TS_NB; ++c) {
+                        rnew[c] = 0.0;
                         if (c <= jj || c >= nb) continue;
-                        const double w = tau * (d[c] + rjc[c]);
+                        const double w = tau * (d[c] + rowv[c]);
 #pragma unroll
                         for (int t = 0; t < SB / 32; ++t) x[c][t] -= w * x[jj][t];
-                        if (lane == 0) sR[j + (j0 + c) * KIN_MAX] = rjc[c] - w;
+                        rnew[c] = rowv[c] - w;
                     }
                     // T(:, jj) = [-tau T(0:jj, 0:jj) g(0:jj); tau]; lane a < jj owns row a
                     double z = 0.0;
 #pragma unroll
                     for (int bq = 0; bq < TS_NB; ++bq)
-                        if (bq < jj && bq >= lane) z += Tp[lane + bq * TS_NB] * d[bq];
+                        if (bq < jj && bq >= lane) z += tz[bq] * d[bq];
+                    __syncwarp();   // every lane has read R row j
+                    if (lane == 0) {
+                        sR[j + j * KIN_MAX] = beta;
+#pragma unroll
+                        for (int c = 0; c < TS_NB; ++c)
+                            if (c > jj && c < nb) sR[j + (j0 + c) * KIN_MAX] = rnew[c];
+                        sTT[j] = tau;
+                    }
                     if (lane < jj) Tp[lane + jj * TS_NB] = -tau * z;
                     if (lane == jj) Tp[jj + jj * TS_NB] = tau;
-                    if (lane == 0) sTT[j] = tau;
-                    __syncwarp();
                 }
 #pragma unroll
                 for (int a = 0; a < TS_NB; ++a)
                     if (a < nb)
 #pragma unroll
-                        for (int t = 0; t < SB / 32; ++t) sB[(lane + 32 * t) + (j0 + a) * SB] = x[a][t];
+                        for (int t = 0; t < SB / 32; ++t) sB[(lane + 32 * t) + (j0 + a) * LDB] = x[a][t];
             }
             __syncthreads();
             TSQR_TRACE(3 * pn + 1);
             // Q_panel^T on the remaining columns: w = Y^T a, w = T^T w, a -= Y w
-            for (int c = j0 + nb + warp; c < k; c += nwarps) {
+            if (g_tsqr_v1_dev) for (int c = j0 + nb + warp; c < k; c += nwarps) {
                 double av[SB / 32], w[TS_NB];
 #pragma unroll
-                for (int t = 0; t < SB / 32; ++t) av[t] = sB[(lane + 32 * t) + c * SB];
+                for (int t = 0; t < SB / 32; ++t) av[t] = sB[(lane + 32 * t) + c * LDB];
 #pragma unroll
                 for (int a = 0; a < TS_NB; ++a) {
                     double s = 0.0;
                     if (a < nb)
 #pragma unroll
-                        for (int t = 0; t < SB / 32; ++t) s += sB[(lane + 32 * t) + (j0 + a) * SB] * av[t];
+                        for (int t = 0; t < SB / 32; ++t) s += sB[(lane + 32 * t) + (j0 + a) * LDB] * av[t];
                     w[a] = s;
                 }
                 warp_allreduce8(w);
@@ -233,20 +251,67 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                     double s = av[t];
 #pragma unroll
                     for (int a = 0; a < TS_NB; ++a)
-                        if (a < nb) s -= sB[(lane + 32 * t) + (j0 + a) * SB] * wt[a];
-                    sB[(lane + 32 * t) + c * SB] = s;
+                        if (a < nb) s -= sB[(lane + 32 * t) + (j0 + a) * LDB] * wt[a];
+                    sB[(lane + 32 * t) + c * LDB] = s;
                 }
                 __syncwarp();
 #pragma unroll
                 for (int a = 0; a < TS_NB; ++a)
                     if (lane == a && a < nb) sR[(j0 + a) + c * KIN_MAX] = ra[a] - wt[a];
             }
+            else {
+                // 8-column tiles on DMMA, one warp per tile:
+                //   W = Y^T A + R[j0:j0+8, tile];  W' = T^T W;  R[j0:j0+8, tile] -= W';  A -= Y W'
+                const int gi = lane >> 2, gk = lane & 3;
+                const int cbeg = j0 + nb, ntile = (k - cbeg + 7) / 8;
+                for (int tl = warp; tl < ntile; tl += nwarps) {
+                    const int c0 = cbeg + 8 * tl;
+                    const bool bv = c0 + gi < k;
+                    const double* ya = sB + (j0 + gi) * LDB + gk;
+                    const double* ab = sB + (c0 + gi) * LDB + gk;
+                    double acc[4][2] = {};
+#pragma unroll
+                    for (int ks = 0; ks < SB / 4; ++ks)
+                        dmma_q(acc[ks & 3][0], acc[ks & 3][1], ya[4 * ks], bv ? ab[4 * ks] : 0.0);
+                    const int cA = c0 + 2 * gk, cB = cA + 1;
+                    const double r0 = cA < k ? sR[(j0 + gi) + cA * KIN_MAX] : 0.0;
+                    const double r1 = cB < k ? sR[(j0 + gi) + cB * KIN_MAX] : 0.0;
+                    const double w0 = ((acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0])) + r0;
+                    const double w1 = ((acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1])) + r1;
+                    // B fragments W[4s + gk][gi] from the accumulator layout (lane 4 r + c / 2 holds W[r][c])
+                    double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int src = (4 * q + gk) * 4 + (gi >> 1);
+                        const double x0 = __shfl_sync(0xffffffffu, w0, src), x1 = __shfl_sync(0xffffffffu, w1, src);
+                        dmma_q(p0, p1, Tp[(4 * q + gk) + TS_NB * gi], (gi & 1) ? x1 : x0);   // T(4q+gk, gi)
+                    }
+                    if (cA < k) sR[(j0 + gi) + cA * KIN_MAX] = r0 - p0;
+                    if (cB < k) sR[(j0 + gi) + cB * KIN_MAX] = r1 - p1;
+                    double bq[2];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int src = (4 * q + gk) * 4 + (gi >> 1);
+                        const double x0 = __shfl_sync(0xffffffffu, p0, src), x1 = __shfl_sync(0xffffffffu, p1, src);
+                        bq[q] = (gi & 1) ? x1 : x0;
+                    }
+#pragma unroll 4
+                    for (int mt = 0; mt < SB / 8; ++mt) {
+                        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) dmma_q(d0, d1, sB[(mt * 8 + gi) + (j0 + 4 * q + gk) * LDB], bq[q]);
+                        double* o = sB + (mt * 8 + gi) + (long long)cA * LDB;
+                        if (cA < k) o[0] -= d0;
+                        if (cB < k) o[LDB] -= d1;
+                    }
+                }
+            }
             __syncthreads();
             TSQR_TRACE(3 * pn + 2);
         }
         // store reflector tails (SB x k), taus and the panel T's of this sub-block
         double* dst = refl + (long long)b * SB * KIN_MAX;
-        for (int i = tid; i < SB * k; i += blockDim.x) dst[i] = sB[i];
+        for (int i = tid; i < SB * k; i += blockDim.x) dst[i] = sB[(i % SB) + (i / SB) * LDB];
         for (int i = tid; i < TS_TAUT; i += blockDim.x) taut_out[(long long)b * TS_TAUT + i] = sTT[i];
     }
     __syncthreads();
@@ -262,7 +327,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
     extern __shared__ double smem[];
     double* sR = smem;                        // KIN_MAX^2
     double* sB = sR + KIN_MAX * KIN_MAX;      // SB * KIN_MAX
-    double* sTau = sB + SB * KIN_MAX;         // TS_TAUT: taus + panel T's
+    double* sTau = sB + LDB * KIN_MAX;        // TS_TAUT: taus + panel T's
     const int3 it = items[blockIdx.x];
     const TTask& t = tasks[it.x];
     const int side = it.y;
@@ -300,12 +365,12 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
             const bool in = gi < nr;
             constexpr int CPT = TS_THREADS / SB;   // column groups per pass
             for (int c = threadIdx.x >> 7; c < k; c += CPT) {
-                if (in) cpa8(B + (long long)c * SB + i, sCol[c] + gi);
-                else B[(long long)c * SB + i] = 0.0;
+                if (in) cpa8(B + (long long)c * LDB + i, sCol[c] + gi);
+                else B[(long long)c * LDB + i] = 0.0;
             }
             cpa_wait_all();   // own copies landed: scale them in place
             for (int c = threadIdx.x >> 7; c < k; c += CPT)
-                if (in) B[(long long)c * SB + i] *= sScl[c];
+                if (in) B[(long long)c * LDB + i] *= sScl[c];
         };
         stream_qr(k, nr, base, base + nsub * SB * KIN_MAX, base + nsub * SB * KIN_MAX + nsub * TS_TAUT, sR, sB,
                   sTau, load);
@@ -328,8 +393,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
                 Rs = seg_area(t, ws, side, s) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + TS_TAUT);
             }
             for (int c = threadIdx.x >> 7; c < k; c += CPT) {
-                if (Rs) cpa8(B + (long long)c * SB + i, Rs + lr + (long long)c * KIN_MAX);
-                else B[(long long)c * SB + i] = 0.0;
+                if (Rs) cpa8(B + (long long)c * LDB + i, Rs + lr + (long long)c * KIN_MAX);
+                else B[(long long)c * LDB + i] = 0.0;
             }
             cpa_wait_all();
         };
@@ -769,7 +834,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
 }
 
 // ------------------------------------------------------------------ host side
-size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + SB * KIN_MAX + TS_TAUT); }
+size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + LDB * KIN_MAX + TS_TAUT); }
 size_t trunc_smem_core() { return sizeof(double) * (2 * KIN_MAX * KIN_MAX); }
 size_t trunc_smem_apply() {
     return std::max(sizeof(double) * (KIN_MAX * KCAP + SB * KIN_MAX + TS_TAUT), apply_dmma_smem());
@@ -779,6 +844,10 @@ void trunc_init_attributes() {
     if (std::getenv("SPG_APPLY_V1")) {
         const int one = 1;
         SPG_CUDA(cudaMemcpyToSymbol(g_apply_v1_dev, &one, sizeof(int)));
+    }
+    if (std::getenv("SPG_TSQR_V1")) {
+        const int one = 1;
+        SPG_CUDA(cudaMemcpyToSymbol(g_tsqr_v1_dev, &one, sizeof(int)));
     }
     SPG_CUDA(cudaFuncSetAttribute(k_tsqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_tsqr()));
     SPG_CUDA(cudaFuncSetAttribute(k_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_core()));
