@@ -220,7 +220,7 @@ void Engine::push_timed(Plan& p, int cls, Launch l) {
     cudaEvent_t a, b;
     SPG_CUDA(cudaEventCreate(&a));
     SPG_CUDA(cudaEventCreate(&b));
-    prof_.push_back({cls, cur_op_, a, b, prof_ntask_, prof_rows_});
+    prof_.push_back({cls, cur_op_, a, b, prof_ntask_, prof_rows_, side_sel_});
     prof_ntask_ = prof_rows_ = 0;
     push(p, [a](cudaStream_t s) { SPG_CUDA(cudaEventRecord(a, s)); });
     push(p, std::move(l));
@@ -259,6 +259,18 @@ void Engine::prof_sum(double* ms, long long* nb) const {
         for (const auto& kv : agg)
             std::fprintf(stderr, "prof op=%d cls=%s ms=%.2f batches=%d\n", kv.first.first, cn[kv.first.second],
                          kv.second.first, kv.second.second);
+        if (const char* tl = std::getenv("SPG_PROF_TIMELINE")) {   // op,cls,stream,ntask,rows,start_ms,end_ms
+            if (FILE* f = std::fopen(tl, "w")) {
+                std::fprintf(f, "op,cls,stream,ntask,rows,t0,t1\n");
+                for (const auto& r : prof_) {
+                    float t0 = 0.f, t1 = 0.f;
+                    SPG_CUDA(cudaEventElapsedTime(&t0, prof_[0].a, r.a));
+                    SPG_CUDA(cudaEventElapsedTime(&t1, prof_[0].a, r.b));
+                    std::fprintf(f, "%d,%s,%d,%d,%d,%.4f,%.4f\n", r.op, cn[r.cls], r.side, r.ntask, r.rows, t0, t1);
+                }
+                std::fclose(f);
+            }
+        }
         // truncation batches by (max rows, task count) buckets
         std::map<std::pair<int, int>, std::pair<double, int>> tb;
         for (const auto& r : prof_) {

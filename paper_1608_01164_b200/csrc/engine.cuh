@@ -245,7 +245,7 @@ private:
     std::vector<std::unique_ptr<DHodlr>> owned_;
     int cur_op_ = 0;
     bool profile_ = false;
-    struct ProfRec { int cls, op; cudaEvent_t a, b; int ntask, rows; };
+    struct ProfRec { int cls, op; cudaEvent_t a, b; int ntask, rows, side; };
     int prof_ntask_ = 0, prof_rows_ = 0;   // shape of the next timed truncation batch
     std::vector<ProfRec> prof_;
 };

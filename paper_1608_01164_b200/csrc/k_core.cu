@@ -550,7 +550,14 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
             a1[m] = (act[m] && lane + 32 > j && lane + 32 < k) ? col[lane + 32] : 0.0;
             aj[m] = act[m] ? col[j] : 0.0;
         }
-        const double s2 = csum(x0 * x0 + x1 * x1);
+        // one reduction for |x|^2 and the four x . a_m (v = scal x, so v . a_m = scal (x . a_m))
+        double q8[8];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) q8[m] = x0 * a0[m] + x1 * a1[m];
+        q8[4] = x0 * x0 + x1 * x1;
+        q8[5] = q8[6] = q8[7] = 0.0;
+        warp_allreduce8(q8);
+        const double s2 = q8[4];
         double tau = 0.0, scal = 0.0, beta = alpha;
         if (s2 > 0.0) {
             const double nrm = sqrt_nr(fma(alpha, alpha, s2));
@@ -561,8 +568,7 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         const double v0 = x0 * scal, v1 = x1 * scal;
         double d[4];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) d[m] = v0 * a0[m] + v1 * a1[m];
-        warp_allreduce4(d);
+        for (int m = 0; m < 4; ++m) d[m] = scal * q8[m];
         bool redo = false;
         double ns[4];
 #pragma unroll

@@ -22,44 +22,6 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// all-reduce of 8 values across the warp by recursive halving (reduce-scatter over lane
-// bits 4..2, full reduction over bits 1..0, then gather): 17 double shuffles instead of
-// 40 for eight independent butterflies; every lane ends with all eight sums.  The
-// summation order is fixed (deterministic) but differs from the plain butterfly.
-__device__ __forceinline__ void warp_allreduce8(double (&v)[8]) {
-    const int lane = threadIdx.x & 31;
-    double h4[4], h2[2], h1;
-    {
-        const bool lo = !(lane & 16);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const double keep = lo ? v[i] : v[i + 4], send = lo ? v[i + 4] : v[i];
-            h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-    }
-    {
-        const bool lo = !(lane & 8);
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const double keep = lo ? h4[i] : h4[i + 2], send = lo ? h4[i + 2] : h4[i];
-            h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
-    }
-    {
-        const bool lo = !(lane & 4);
-        const double keep = lo ? h2[0] : h2[1], send = lo ? h2[1] : h2[0];
-        h1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
-    h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
-    // lane L holds the sum of value index c = 4*(bit4) + 2*(bit3) + (bit2) of L
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        const int src = ((c >> 2) & 1) * 16 + ((c >> 1) & 1) * 8 + (c & 1) * 4;
-        v[c] = __shfl_sync(0xffffffffu, h1, src);
-    }
-}
-
 __device__ __forceinline__ bool task_skip(const TTask& t) {
     if (t.skipg < 0) return false;
     const TGroup& g = t.g[t.skipg];
@@ -105,6 +67,7 @@ __device__ long long* g_tsqr_trace = nullptr;   // micro-benchmarks: clock64 per
 void set_tsqr_trace(long long* p) { SPG_CUDA(cudaMemcpyToSymbol(g_tsqr_trace, &p, sizeof(p))); }
 #define TSQR_TRACE(slot) do { if (g_tsqr_trace && b == 0 && blockIdx.x == 0 && threadIdx.x == 0) g_tsqr_trace[slot] = clock64(); } while (0)
 constexpr int LDB = SB + 4;   // leading dimension of the staged sub-block (conflict-free DMMA fragments)
+constexpr int TS_XS = 6 * 64; // split-tile partials: G * ntile <= 6 tiles of 8 x 8
 __device__ __forceinline__ void dmma_q(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
@@ -126,7 +89,7 @@ __constant__ int g_tsqr_v1_dev = 0;   // SPG_TSQR_V1=1: per-column trailing upda
 // Loader: fills Bk (SB x k, col-major ld SB) with rows [row0, row0+SB) (zero padded).
 template <class Loader>
 __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, double* Rout,
-                          double* sR, double* sB, double* sTT, const Loader& load) {
+                          double* sR, double* sB, double* sTT, double* sX, const Loader& load) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = blockDim.x >> 5;
     for (int i = tid; i < KIN_MAX * KIN_MAX; i += blockDim.x) sR[i] = 0.0;
@@ -263,21 +226,47 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                 // 8-column tiles on DMMA, one warp per tile:
                 //   W = Y^T A + R[j0:j0+8, tile];  W' = T^T W;  R[j0:j0+8, tile] -= W';  A -= Y W'
                 const int gi = lane >> 2, gk = lane & 3;
+                // few tiles: G warps per tile split the rows (partial W summed through sX)
                 const int cbeg = j0 + nb, ntile = (k - cbeg + 7) / 8;
-                for (int tl = warp; tl < ntile; tl += nwarps) {
+                const int G = ntile == 1 ? 4 : (ntile <= 3 ? 2 : 1);
+                for (int wt = warp; wt < ntile * G; wt += nwarps) {
+                    const int tl = wt / G, g = wt % G;
                     const int c0 = cbeg + 8 * tl;
                     const bool bv = c0 + gi < k;
                     const double* ya = sB + (j0 + gi) * LDB + gk;
                     const double* ab = sB + (c0 + gi) * LDB + gk;
                     double acc[4][2] = {};
+                    const int ks0 = g * (SB / 4) / G, ks1 = (g + 1) * (SB / 4) / G;
+                    if (G == 1) {
 #pragma unroll
-                    for (int ks = 0; ks < SB / 4; ++ks)
-                        dmma_q(acc[ks & 3][0], acc[ks & 3][1], ya[4 * ks], bv ? ab[4 * ks] : 0.0);
+                        for (int ks = 0; ks < SB / 4; ++ks)
+                            dmma_q(acc[ks & 3][0], acc[ks & 3][1], ya[4 * ks], bv ? ab[4 * ks] : 0.0);
+                    } else {
+#pragma unroll 2
+                        for (int ks = ks0; ks < ks1; ks += 4)   // ks0, ks1 multiples of 4
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                dmma_q(acc[q][0], acc[q][1], ya[4 * (ks + q)], bv ? ab[4 * (ks + q)] : 0.0);
+                    }
+                    double w0 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+                    double w1 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+                    if (G > 1) {
+                        double* sc = sX + tl * G * 64;
+                        sc[g * 64 + 2 * lane] = w0;
+                        sc[g * 64 + 2 * lane + 1] = w1;
+                        asm volatile("bar.sync %0, %1;\n" ::"r"(1 + tl), "r"(G * 32) : "memory");
+                        w0 = sc[2 * lane];
+                        w1 = sc[2 * lane + 1];
+                        for (int q = 1; q < G; ++q) {
+                            w0 += sc[q * 64 + 2 * lane];
+                            w1 += sc[q * 64 + 2 * lane + 1];
+                        }
+                    }
                     const int cA = c0 + 2 * gk, cB = cA + 1;
                     const double r0 = cA < k ? sR[(j0 + gi) + cA * KIN_MAX] : 0.0;
                     const double r1 = cB < k ? sR[(j0 + gi) + cB * KIN_MAX] : 0.0;
-                    const double w0 = ((acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0])) + r0;
-                    const double w1 = ((acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1])) + r1;
+                    w0 += r0;
+                    w1 += r1;
                     // B fragments W[4s + gk][gi] from the accumulator layout (lane 4 r + c / 2 holds W[r][c])
                     double p0 = 0.0, p1 = 0.0;
 #pragma unroll
@@ -286,8 +275,8 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                         const double x0 = __shfl_sync(0xffffffffu, w0, src), x1 = __shfl_sync(0xffffffffu, w1, src);
                         dmma_q(p0, p1, Tp[(4 * q + gk) + TS_NB * gi], (gi & 1) ? x1 : x0);   // T(4q+gk, gi)
                     }
-                    if (cA < k) sR[(j0 + gi) + cA * KIN_MAX] = r0 - p0;
-                    if (cB < k) sR[(j0 + gi) + cB * KIN_MAX] = r1 - p1;
+                    if (g == 0 && cA < k) sR[(j0 + gi) + cA * KIN_MAX] = r0 - p0;
+                    if (g == 0 && cB < k) sR[(j0 + gi) + cB * KIN_MAX] = r1 - p1;
                     double bq[2];
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
@@ -296,7 +285,7 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                         bq[q] = (gi & 1) ? x1 : x0;
                     }
 #pragma unroll 4
-                    for (int mt = 0; mt < SB / 8; ++mt) {
+                    for (int mt = g * (SB / 8) / G; mt < (g + 1) * (SB / 8) / G; ++mt) {
                         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
                         for (int q = 0; q < 2; ++q) dmma_q(d0, d1, sB[(mt * 8 + gi) + (j0 + 4 * q + gk) * LDB], bq[q]);
@@ -328,6 +317,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
     double* sR = smem;                        // KIN_MAX^2
     double* sB = sR + KIN_MAX * KIN_MAX;      // SB * KIN_MAX
     double* sTau = sB + LDB * KIN_MAX;        // TS_TAUT: taus + panel T's
+    double* sX = sTau + TS_TAUT;              // TS_XS: partial W of the split trailing tiles
     const int3 it = items[blockIdx.x];
     const TTask& t = tasks[it.x];
     const int side = it.y;
@@ -373,7 +363,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
                 if (in) B[(long long)c * LDB + i] *= sScl[c];
         };
         stream_qr(k, nr, base, base + nsub * SB * KIN_MAX, base + nsub * SB * KIN_MAX + nsub * TS_TAUT, sR, sB,
-                  sTau, load);
+                  sTau, sX, load);
     } else {
         const int ns = t.nseg[side];
         if (ns <= 1) return;
@@ -399,7 +389,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
             cpa_wait_all();
         };
         stream_qr(k, mrows, mb, mb + nsubm * SB * KIN_MAX, mb + nsubm * SB * KIN_MAX + nsubm * TS_TAUT, sR, sB,
-                  sTau, load);
+                  sTau, sX, load);
     }
 }
 
@@ -834,7 +824,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
 }
 
 // ------------------------------------------------------------------ host side
-size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + LDB * KIN_MAX + TS_TAUT); }
+size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + LDB * KIN_MAX + TS_TAUT + TS_XS); }
 size_t trunc_smem_core() { return sizeof(double) * (2 * KIN_MAX * KIN_MAX); }
 size_t trunc_smem_apply() {
     return std::max(sizeof(double) * (KIN_MAX * KCAP + SB * KIN_MAX + TS_TAUT), apply_dmma_smem());
