@@ -137,6 +137,7 @@ __global__ void k_rank_op(const RankOp* ops, int nops) {
 Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin), eps_(eps) {
     SPG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     trunc_init_attributes();
+    gemm_init_attributes();
     leaf_init_attributes();
     hsolve_init_attributes();
     arena_ = std::make_unique<Arena>(size_t(512) << 20);

@@ -22,10 +22,21 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 
 __device__ __forceinline__ int dimv(int c, const int* p) { return p ? *p : c; }
 
+// Pipeline: GST-stage cp.async ring of (A, B) k-tiles; tile t + GST - 1 is in flight
+// while tile t is multiplied, so the L2/HBM latency hides behind the DMMA work.
+constexpr int GST = 4;
+constexpr int G_TILE = GBK * (GBM + GPAD);   // doubles per operand tile
+__host__ __device__ constexpr size_t gemm_smem_bytes() { return sizeof(double) * (size_t)GST * 2 * G_TILE; }
+
+__device__ __forceinline__ void cpa8g(double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+
 __global__ void __launch_bounds__(G_THREADS) k_gemm(const GemmItem* __restrict__ items, const int4* __restrict__ ctas,
                                                   double* flops) {
-    __shared__ double As[GBK][GBM + GPAD];
-    __shared__ double Bs[GBK][GBN + GPAD];
+    extern __shared__ double gsm[];
     const int4 cm = ctas[blockIdx.x];
     const GemmItem& g = items[cm.x];
     const int M = dimv(g.M, g.Mp), N = dimv(g.N, g.Np), K = dimv(g.K, g.Kp);
@@ -41,46 +52,66 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm(const GemmItem* __restrict__
     }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;   // warp tile 32 x 16
+    const double* __restrict__ A = g.A;
+    const double* __restrict__ B = g.B;
+    const long long lda = g.lda, ldb = g.ldb;
+    const int ta = g.ta, tb = g.tb;
+    // As[kk][mm] = A(m0+mm, k0+kk), Bs[kk][nn] = B(k0+kk, n0+nn), row pitch GBM + GPAD
+    auto load_tile = [&](int stage, int k0) {
+        double* As = gsm + (size_t)stage * 2 * G_TILE;
+        double* Bs = As + G_TILE;
+        if (k0 < kend) {
+#pragma unroll
+            for (int r = 0; r < GBK * GBM / G_THREADS; ++r) {
+                const int idx = tid + r * G_THREADS;
+                int mm, kk;
+                if (!ta) { mm = idx % GBM; kk = idx / GBM; } else { kk = idx % GBK; mm = idx / GBK; }
+                const int m = m0 + mm, k = k0 + kk;
+                double* d = As + kk * (GBM + GPAD) + mm;
+                if (m < M && k < kend) cpa8g(d, ta ? A + k + (long long)m * lda : A + m + (long long)k * lda);
+                else *d = 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < GBK * GBN / G_THREADS; ++r) {
+                const int idx = tid + r * G_THREADS;
+                int nn, kk;
+                if (!tb) { kk = idx % GBK; nn = idx / GBK; } else { nn = idx % GBN; kk = idx / GBN; }
+                const int n = n0 + nn, k = k0 + kk;
+                double* d = Bs + kk * (GBN + GPAD) + nn;
+                if (n < N && k < kend) cpa8g(d, tb ? B + n + (long long)k * ldb : B + k + (long long)n * ldb);
+                else *d = 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
     double acc[4][2][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    for (int k0 = kbeg; k0 < kend; k0 += GBK) {
-        // A tile: As[kk][mm] = A(m0+mm, k0+kk)
-        for (int idx = tid; idx < GBK * GBM; idx += G_THREADS) {
-            int mm, kk;
-            if (!g.ta) { mm = idx % GBM; kk = idx / GBM; } else { kk = idx % GBK; mm = idx / GBK; }
-            const int m = m0 + mm, k = k0 + kk;
-            double v = 0.0;
-            if (m < M && k < kend) v = g.ta ? g.A[k + (long long)m * g.lda] : g.A[m + (long long)k * g.lda];
-            As[kk][mm] = v;
-        }
-        // B tile: Bs[kk][nn] = B(k0+kk, n0+nn)
-        for (int idx = tid; idx < GBK * GBN; idx += G_THREADS) {
-            int nn, kk;
-            if (!g.tb) { kk = idx % GBK; nn = idx / GBK; } else { nn = idx % GBN; kk = idx / GBN; }
-            const int n = n0 + nn, k = k0 + kk;
-            double v = 0.0;
-            if (n < N && k < kend) v = g.tb ? g.B[n + (long long)k * g.ldb] : g.B[k + (long long)n * g.ldb];
-            Bs[kk][nn] = v;
-        }
-        __syncthreads();
+    const int ntiles = kend > kbeg ? (kend - kbeg + GBK - 1) / GBK : 0;
+#pragma unroll
+    for (int s = 0; s < GST - 1; ++s) load_tile(s, kbeg + s * GBK);
+    for (int t = 0; t < ntiles; ++t) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(GST - 2) : "memory");   // tile t landed (own copies)
+        __syncthreads();   // all copies of tile t landed; tile t - 1 consumed by every warp
+        load_tile((t + GST - 1) % GST, kbeg + (t + GST - 1) * GBK);
+        const double* As = gsm + (size_t)(t % GST) * 2 * G_TILE;
+        const double* Bs = As + G_TILE;
 #pragma unroll
         for (int ks = 0; ks < GBK; ks += 4) {
             double af[4], bf[2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) af[i] = As[ks + (lane & 3)][wm + i * 8 + (lane >> 2)];
+            for (int i = 0; i < 4; ++i) af[i] = As[(ks + (lane & 3)) * (GBM + GPAD) + wm + i * 8 + (lane >> 2)];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) bf[j] = Bs[ks + (lane & 3)][wn + j * 8 + (lane >> 2)];
+            for (int j = 0; j < 2; ++j) bf[j] = Bs[(ks + (lane & 3)) * (GBN + GPAD) + wn + j * 8 + (lane >> 2)];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
-        __syncthreads();
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     const double alpha = g.alphap ? g.alpha * *g.alphap : g.alpha;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -117,9 +148,13 @@ __global__ void k_gemm_reduce(const GemmItem* __restrict__ items, const int* __r
     }
 }
 
+void gemm_init_attributes() {
+    SPG_CUDA(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes()));
+}
+
 void launch_gemm(const GemmBatch& b, cudaStream_t st) {
     if (b.nctas == 0) return;
-    k_gemm<<<b.nctas, G_THREADS, 0, st>>>(b.d_items, b.d_ctas, b.flops);
+    k_gemm<<<b.nctas, G_THREADS, gemm_smem_bytes(), st>>>(b.d_items, b.d_ctas, b.flops);
     SPG_LAUNCH_CHECK();
     if (b.nred) {
         k_gemm_reduce<<<b.nred, 256, 0, st>>>(b.d_items, b.d_red_items);

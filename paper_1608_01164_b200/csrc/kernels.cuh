@@ -49,6 +49,7 @@ struct GemmBatch {
     double* flops = nullptr;           // device counter of algorithmic flops (2MNK)
 };
 void launch_gemm(const GemmBatch& b, cudaStream_t st);
+void gemm_init_attributes();
 
 // ------------------------------------------------------------ leaf / elementwise ops
 struct LeafItem {          // one dense block (column-major, ld = ld)
