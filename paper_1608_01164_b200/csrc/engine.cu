@@ -374,29 +374,44 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
 }
 
 // ---------------------------------------------------------------- GEMM batch
+static const bool g_gemm_split_v1 = std::getenv("SPG_GEMM_SPLIT_V1") != nullptr;   // A/B: split-K only for K >= 2048
+
 void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>& caps) {
     if (items.empty()) return;
-    const long long mark = ws_->mark();
+    Workspace& wsp = side_sel_ >= 0 ? *ws_side_[side_sel_] : *ws_;   // split-K partials: this stream's stack
+    const long long mark = wsp.mark();
     std::vector<int4> ctas;
     std::vector<int> red;
+    // split-K only while the batch leaves SMs idle: aim at ~2 CTAs per SM, >= 8 k-tiles per split
+    long long base = 0;
+    for (size_t i = 0; i < items.size(); ++i)
+        if (caps[i].x > 0 && caps[i].y > 0) base += (long long)((caps[i].x + 63) / 64) * ((caps[i].y + 63) / 64);
+    const int fill = (int)std::max<long long>(1, (2 * 148) / std::max<long long>(1, base));
     for (size_t i = 0; i < items.size(); ++i) {
         GemmItem& g = items[i];
         const int mM = caps[i].x, mN = caps[i].y, mK = caps[i].z;
         if (mM <= 0 || mN <= 0) continue;
         const int tm = (mM + 63) / 64, tn = (mN + 63) / 64;
         g.nsplit = 1;
-        if (mK >= 2048 && tm * tn <= 8) {
+        const int ns = std::min({64, (mK + 127) / 128, fill});
+        if (ns >= 2 && tm * tn <= 8 && !g_gemm_split_v1) {
+            g.nsplit = ns;
+            g.Mcap = mM;
+            g.Ncap = mN;
+            g.partial = wsp.ptr(wsp.alloc((long long)g.nsplit * mM * mN));
+            red.push_back((int)i);
+        } else if (g_gemm_split_v1 && mK >= 2048 && tm * tn <= 8) {
             g.nsplit = std::min(64, (mK + 1023) / 1024);
             g.Mcap = mM;
             g.Ncap = mN;
-            g.partial = ws_->ptr(ws_->alloc((long long)g.nsplit * mM * mN));
+            g.partial = wsp.ptr(wsp.alloc((long long)g.nsplit * mM * mN));
             red.push_back((int)i);
         }
         for (int s = 0; s < g.nsplit; ++s)
             for (int a = 0; a < tm; ++a)
                 for (int c = 0; c < tn; ++c) ctas.push_back(make_int4((int)i, a, c, s));
     }
-    if (ctas.empty()) { ws_->release(mark); return; }
+    if (ctas.empty()) { wsp.release(mark); return; }
     GemmBatch b;
     b.d_items = arena_->push(items);
     b.d_ctas = arena_->push(ctas);
@@ -404,8 +419,13 @@ void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>&
     b.d_red_items = arena_->push(red);
     b.nred = (int)red.size();
     b.flops = sc_.counters + 1;
+    if (profile_) {   // timeline shape: CTAs, largest K
+        prof_ntask_ = (int)ctas.size();
+        prof_rows_ = 0;
+        for (const auto& c : caps) prof_rows_ = std::max(prof_rows_, c.z);
+    }
     push_timed(p, PC_GEMM, [b](cudaStream_t st) { launch_gemm(b, st); });
-    ws_->release(mark);
+    wsp.release(mark);
 }
 
 static GemmItem gitem(const double* A, int lda, int ta, const double* B, int ldb, int tb, double* C, int ldc, int M,
