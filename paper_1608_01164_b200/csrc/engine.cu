@@ -382,19 +382,27 @@ void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>&
     const long long mark = wsp.mark();
     std::vector<int4> ctas;
     std::vector<int> red;
-    // split-K only while the batch leaves SMs idle: aim at ~2 CTAs per SM, >= 8 k-tiles per split
-    long long base = 0;
+    // split-K balances the batch: no CTA runs more than `chunk` k-tiles of 16, chunk = the
+    // batch's k-tiles spread over >= 2 CTAs per SM (and >= 8 k-tiles per split)
+    long long base = 0, ktiles = 0;
     for (size_t i = 0; i < items.size(); ++i)
-        if (caps[i].x > 0 && caps[i].y > 0) base += (long long)((caps[i].x + 63) / 64) * ((caps[i].y + 63) / 64);
-    const int fill = (int)std::max<long long>(1, (2 * 148) / std::max<long long>(1, base));
+        if (caps[i].x > 0 && caps[i].y > 0) {
+            const long long t = (long long)((caps[i].x + 63) / 64) * ((caps[i].y + 63) / 64);
+            base += t;
+            ktiles += t * ((caps[i].z + 15) / 16);
+        }
+    const long long chunk = std::max<long long>(8, (ktiles + 2 * 148 - 1) / std::max<long long>(2 * 148, base));
     for (size_t i = 0; i < items.size(); ++i) {
         GemmItem& g = items[i];
         const int mM = caps[i].x, mN = caps[i].y, mK = caps[i].z;
         if (mM <= 0 || mN <= 0) continue;
         const int tm = (mM + 63) / 64, tn = (mN + 63) / 64;
         g.nsplit = 1;
-        const int ns = std::min({64, (mK + 127) / 128, fill});
-        if (ns >= 2 && tm * tn <= 8 && !g_gemm_split_v1) {
+        int ns = (int)std::min<long long>(64, ((mK + 15) / 16 + chunk - 1) / chunk);
+        // partials stay within a quarter of the stream's workspace
+        const long long room = (long long)wsp.capacity() / 4 - (wsp.mark() - mark);
+        while (ns >= 2 && (long long)ns * mM * mN > room) ns /= 2;
+        if (ns >= 2 && !g_gemm_split_v1) {
             g.nsplit = ns;
             g.Mcap = mM;
             g.Ncap = mN;
