@@ -571,6 +571,11 @@ void Engine::hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items) {
     const DevTree dt = dtree_;
     const DevHodlrView wv = W.view();
     unsigned* status = sc_.status;
+    if (profile_) {
+        prof_ntask_ = (int)items.size();
+        prof_rows_ = 0;
+        for (const auto& it : items) prof_rows_ = std::max(prof_rows_, tree_.size[it.root]);
+    }
     push_timed(p, PC_HSOLVE, [dt, wv, d, dc, nc, status](cudaStream_t st) { launch_hsolve(dt, wv, d, dc, nc, status, st); });
 }
 

@@ -332,6 +332,18 @@ __global__ void __launch_bounds__(H2_THREADS) k_hsolve2(DevTree t, DevHodlrView 
                 const bool bv = gi < ncols;
                 double c0 = 0.0, c1 = 0.0;
                 int ks = ks0;
+                for (; ks + 8 <= ks1; ks += 8) {   // 8 k-steps of loads in flight per round trip
+                    double a[8], bb[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int rr = 4 * (ks + u) + gk;
+                        const bool rv = rr < nin;
+                        a[u] = (av && rv) ? Pin[rr + a_i * ldp] : 0.0;
+                        bb[u] = (bv && rv) ? Xb[(rin0 + rr) + gi * ldx] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) dmma84(c0, c1, a[u], bb[u]);
+                }
                 for (; ks + 4 <= ks1; ks += 4) {
                     double a[4], bb[4];
 #pragma unroll
