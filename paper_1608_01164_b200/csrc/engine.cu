@@ -161,8 +161,16 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
         ws_side_.push_back(std::make_unique<Workspace>(std::max<size_t>((size_t)3 * n * KIN_MAX, size_t(8) << 20)));
         wtr_idx_ = (int)sides_.size() - 1;
     }
+    {   // bases tV_x = W_{r(x)}^{-T} V_x built during the Cholesky (subtree-parallel solves inside it)
+        cudaStream_t s;
+        SPG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        sides_.push_back(s);
+        ws_side_.push_back(std::make_unique<Workspace>(std::max<size_t>((size_t)2 * n * KCAP, size_t(8) << 20)));
+        tv_idx_ = (int)sides_.size() - 1;
+    }
     ev_base2_ = tree_.nnodes() * (nside + 2) + 4 * nside + 8;
-    events_.resize((size_t)ev_base2_ + 2 * (size_t)tree_.nnodes());
+    ev_base3_ = ev_base2_ + 2 * tree_.nnodes();
+    events_.resize((size_t)ev_base3_ + 2 * (size_t)tree_.nnodes());
     for (auto& e : events_) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (int t = 0; t < std::max(1, tree_.depth); ++t) {
         double* p;
@@ -549,6 +557,9 @@ void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs) {
 }
 
 static const bool g_psolve_off = std::getenv("SPG_PSOLVE_OFF") != nullptr;
+static const bool g_chol_tv_off = std::getenv("SPG_CHOL_TV_OFF") != nullptr;   // A/B: sequential subtree solves in the Cholesky
+// subtrees of at least this depth are solved subtree-parallel inside the Cholesky (smaller: k_hsolve2)
+static const int g_chol_tv_min = std::getenv("SPG_CHOL_TV_MIN") ? std::atoi(std::getenv("SPG_CHOL_TV_MIN")) : 5;
 
 void Engine::hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items) {
     if (items.empty()) return;
@@ -937,6 +948,23 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
     cur_op_ = 6;
     W.tready = false;
     chol_defer_trunc_ = defer_trunc && !g_chol_serial;
+    chol_tv_ = chol_defer_trunc_ && !g_psolve_off && !g_chol_tv_off;
+    if (chol_tv_) {   // forward subtree solves inside the factorisation go subtree-parallel
+        if (!W.tU) {
+            SPG_CUDA(cudaMalloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
+            W.tV = W.tU + W.slab_doubles;
+        }
+        W.tready = true;
+        tv_need_.assign(tree_.nnodes(), 0);   // internal nodes inside a subtree-parallel solve
+        std::vector<int> in, lv;
+        for (int x = 0; x < tree_.nnodes(); ++x) {
+            if (tree_.leaf(x)) continue;
+            const int l = tree_.left[x];
+            if (tree_.depth - tree_.level[l] < g_chol_tv_min) continue;
+            tree_.subtree(l, in, lv);
+            for (int y : in) tv_need_[y] = 1;
+        }
+    }
     wtr_last_ev_ = -1;
     op_copy(p, M, work);
     const DHodlr* Wp = &W;
@@ -966,6 +994,8 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
         side_sel_ = -1;
         wait(p, ev_join + i);
     }
+    if (chol_tv_) W.tready = false;   // tU is not built here (op_solve_prep rebuilds both)
+    chol_tv_ = false;
 }
 
 // deferred Schur cascade of node x into the subtree `root` = r(x): the leaf updates
@@ -1073,7 +1103,15 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
         double* X = xpanels_[t];
         copy(p, {CopyItem{M.upU(x), X + bl, s1, n, n, M.rup(x), 0, 1.0, nullptr}}, s1, KCAP);
         if (wtr_last_ev_ >= 0 && !tree_.leaf(l)) wait(p, wtr_last_ev_);
-        hsolve(p, W, {HSolveItem{l, X + bl, n, M.rup(x), 0, 0}});
+        if (chol_tv_ && tree_.depth - tree_.level[l] >= g_chol_tv_min) {   // subtree-parallel: tV inside l built
+            wait(p, ev_base3_ + tree_.nnodes() + l);
+            hsolve(p, W, {HSolveItem{l, X + bl, n, M.rup(x), 0, 0}});
+        } else {
+            const bool tr = W.tready;
+            W.tready = false;   // sequential walk
+            hsolve(p, W, {HSolveItem{l, X + bl, n, M.rup(x), 0, 0}});
+            W.tready = tr;
+        }
         const int evx = ev_base2_ + x, evw = ev_base2_ + tree_.nnodes() + x;
         record(p, evx);
         {   // W12 = trunc(X, m12.V) on its own stream (lowrank.hpp:67-86)
@@ -1098,6 +1136,21 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
         record(p, x);
         cascade_chol(p, M, x, r, P1, M.slabV(t), M.rup(x));
         chol_rec(p, r, M, W);
+        if (chol_tv_ && tv_need_[x]) {   // tV_x = W_r^{-T} V_x once W_r and W12(x) are final (own stream, FIFO)
+            const int nn = tree_.nnodes();
+            record(p, ev_base3_ + x);
+            side_sel_ = tv_idx_;
+            wait(p, ev_base3_ + x);
+            wait(p, ev_base2_ + nn + x);
+            double* tv = W.tslabV(t) + br;
+            copy(p, {CopyItem{W.upV(x), tv, s2, n, n, W.rup(x), 0, 1.0, nullptr}}, s2, KCAP);
+            const bool tr = W.tready;
+            W.tready = tree_.depth - tree_.level[r] >= g_chol_tv_min;
+            hsolve(p, W, {HSolveItem{r, tv, n, W.rup(x), 0, 0}});
+            W.tready = tr;
+            record(p, ev_base3_ + nn + x);
+            side_sel_ = -1;
+        }
         return;
     }
     // b12 = trunc({W11^{-T} m12.U, m12.V})

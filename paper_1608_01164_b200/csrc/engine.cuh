@@ -224,6 +224,10 @@ private:
     int wtr_idx_ = 0;                   // side stream of the deferred W12 truncations
     int ev_base2_ = 0;                  // event slots: x-ready(x) = ev_base2_ + x, w12-done(x) = ev_base2_ + nn + x
     int wtr_last_ev_ = -1;              // latest W12 truncation event (FIFO stream: covers all earlier ones)
+    int tv_idx_ = 0;                    // side stream building the Cholesky's tV bases
+    int ev_base3_ = 0;                  // chol(x) done = ev_base3_ + x, tV_x built = ev_base3_ + nn + x
+    bool chol_tv_ = false;
+    std::vector<char> tv_need_;
     std::vector<double*> xpanels_;      // per-depth untruncated W11^{-T} M12.U panels
     double* leaf_scr_ = nullptr;        // Schur block of a split leaf Cholesky (main stream only)
     std::vector<int> last_leaf_ev_, last_block_ev_;   // latest side-stream event touching a leaf / block
