@@ -662,9 +662,11 @@ void Engine::op_solve_prep(Plan& p, DHodlr& W) {
             maxm = std::max(maxm, std::max(s1, s2));
             double* tv = W.tslabV(t) + tree_.begin[r];
             double* tu = W.tslabU(t) + tree_.begin[l];
-            cp.push_back(CopyItem{W.upV(y), tv, s2, n, n, W.rup(y), 0, 1.0, nullptr});
+            if (!(y < (int)W.tv_built.size() && W.tv_built[y])) {   // tV built by the Cholesky: kept
+                cp.push_back(CopyItem{W.upV(y), tv, s2, n, n, W.rup(y), 0, 1.0, nullptr});
+                hs.push_back(HSolveItem{r, tv, n, W.rup(y), 0, 0});
+            }
             cp.push_back(CopyItem{W.upU(y), tu, s1, n, n, W.rup(y), 0, 1.0, nullptr});
-            hs.push_back(HSolveItem{r, tv, n, W.rup(y), 0, 0});
             hs.push_back(HSolveItem{l, tu, n, W.rup(y), 0, 1});
         }
         copy(p, cp, maxm, KCAP);
@@ -672,6 +674,7 @@ void Engine::op_solve_prep(Plan& p, DHodlr& W) {
         hsolve(p, W, hs);
     }
     W.tready = true;
+    W.tv_built.clear();
 }
 
 void Engine::copy(Plan& p, std::vector<CopyItem> items, int maxm, int maxk) {
@@ -947,6 +950,7 @@ static const bool g_chol_serial = std::getenv("SPG_CHOL_SERIAL") != nullptr;
 void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool defer_trunc) {
     cur_op_ = 6;
     W.tready = false;
+    W.tv_built.clear();
     chol_defer_trunc_ = defer_trunc && !g_chol_serial;
     chol_tv_ = chol_defer_trunc_ && !g_psolve_off && !g_chol_tv_off;
     if (chol_tv_) {   // forward subtree solves inside the factorisation go subtree-parallel
@@ -955,6 +959,7 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
             W.tV = W.tU + W.slab_doubles;
         }
         W.tready = true;
+        W.tv_built.assign(tree_.nnodes(), 0);
         tv_need_.assign(tree_.nnodes(), 0);   // internal nodes inside a subtree-parallel solve
         std::vector<int> in, lv;
         for (int x = 0; x < tree_.nnodes(); ++x) {
@@ -1148,6 +1153,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
             W.tready = tree_.depth - tree_.level[r] >= g_chol_tv_min;
             hsolve(p, W, {HSolveItem{r, tv, n, W.rup(x), 0, 0}});
             W.tready = tr;
+            W.tv_built[x] = 1;
             record(p, ev_base3_ + nn + x);
             side_sel_ = -1;
         }

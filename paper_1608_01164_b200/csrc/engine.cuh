@@ -94,6 +94,7 @@ struct DHodlr {
     double* tU = nullptr;
     double* tV = nullptr;
     bool tready = false;                    // plan-build-time flag: tU / tV are current
+    std::vector<char> tv_built;             // plan-build-time: tV of these nodes built by the Cholesky
     double* tslabU(int lev) const { return tU + (size_t)lev * KCAP * t->n; }
     double* tslabV(int lev) const { return tV + (size_t)lev * KCAP * t->n; }
     long long* d_dinv_off = nullptr;
