@@ -332,6 +332,8 @@ std::unique_ptr<DHodlr> Engine::new_hodlr() {
 }
 
 // ---------------------------------------------------------------- truncation batch
+static const double g_tsqr_segk = std::getenv("SPG_TSQR_SEGK") ? std::atof(std::getenv("SPG_TSQR_SEGK")) : 48.0;
+
 void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     if (tasks.empty()) return;
     Workspace& wsp = side_sel_ >= 0 ? *ws_side_[side_sel_] : *ws_;   // each stream has its own stack
@@ -346,7 +348,7 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
             // sub-block QRs, so seg ~ sqrt(rows * k) balances them (k ~ 48 typical).
             int seg = rows, nseg = 1;
             if (rows > 2 * SB) {
-                seg = std::max(2 * SB, (int)std::ceil(std::sqrt((double)rows * 48.0) / SB) * SB);
+                seg = std::max(2 * SB, (int)std::ceil(std::sqrt((double)rows * g_tsqr_segk) / SB) * SB);
                 nseg = (rows + seg - 1) / seg;
                 if (nseg == 1) seg = rows;
             }
