@@ -75,6 +75,28 @@ __device__ __forceinline__ void dmma_q(double& c0, double& c1, double a, double 
 }
 __constant__ int g_tsqr_v1_dev = 0;   // SPG_TSQR_V1=1: per-column trailing update (A/B checks)
 
+// all-reduce of 8 values across one warp through shared memory (scratch: 32 x 9 doubles):
+// every lane stores its 8 partials, lane L sums value L / 4 over lanes 8 (L % 4) .. +7,
+// two butterfly steps finish each value in its 4 lanes, one shuffle round gathers all 8.
+// Fixed order (deterministic); ~4 dependent shuffle steps instead of 8.
+__device__ __forceinline__ void smem_allreduce8(double (&v)[8], double* scratch, int lane) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) scratch[lane * 9 + c] = v[c];
+    __syncwarp();
+    const int c = lane >> 2, q = lane & 3;
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+        a += scratch[(8 * q + i) * 9 + c];
+        b += scratch[(8 * q + i + 1) * 9 + c];
+    }
+    double t = a + b;
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __shfl_sync(0xffffffffu, t, 4 * k);
+}
+
 // Streaming Householder QR of the rows [r0, r0+nrows) of an implicit matrix with
 // k columns, starting from R = 0:  [0_k; A] = Q [R; 0].  Each 128-row sub-block
 // is folded into R by k reflectors y_j = [e_j; v_j] acting on (R row j, block
@@ -133,7 +155,7 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                         for (int t = 0; t < SB / 32; ++t) s += x[jj][t] * x[c][t];
                         d[c] = s;
                     }
-                    warp_allreduce8(d);
+                    smem_allreduce8(d, sX, lane);   // sX is free during the panel factor
                     const double s2 = d[jj];
                     const double alpha = rowv[jj];
                     double tau = 0.0, scal = 0.0, beta = alpha;
