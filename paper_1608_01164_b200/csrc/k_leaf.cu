@@ -1072,7 +1072,7 @@ constexpr int TRM_RS = 32, TRM_LD = TRM_RS + 4, TRM_THREADS = 256;
 // X(rhs, w) addressing: rhs_t = 1 -> X[rhs + w ldx] (a leaf, rows are right-hand sides);
 // rhs_t = 0 -> X[w + rhs ldx] (a panel, columns are right-hand sides).  The number of
 // right-hand sides is *ncp (device) when given, else nc.
-__global__ void __launch_bounds__(TRM_THREADS) k_leaf_trsm_rows(const TrsmItem* __restrict__ it) {
+__global__ void __launch_bounds__(TRM_THREADS, 2) k_leaf_trsm_rows(const TrsmItem* __restrict__ it) {
     extern __shared__ double smem_trm[];
     const TrsmItem T = it[blockIdx.y];
     const int n = T.n;
@@ -1090,29 +1090,58 @@ __global__ void __launch_bounds__(TRM_THREADS) k_leaf_trsm_rows(const TrsmItem* 
     const long long ldw = T.ldw;
     const long long rs = T.rhs_t ? 1 : T.ldx, ws = T.rhs_t ? T.ldx : 1;   // strides of (rhs, w)
     double* X = T.X + (long long)(r0 + row) * rs;
+    auto load_bf = [&](int a, int c0, double (&bf)[8][2]) {
+        const int k0 = a * 32;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = k0 + 4 * u + gk;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int col = c0 + (ct0 + c) * 8 + gi;
+                bf[u][c] = T.mode == 0 ? T.W[k + (long long)col * ldw] : T.W[col + (long long)k * ldw];
+            }
+        }
+    };
     for (int bi = 0; bi < nblk; ++bi) {
         const int b = T.mode == 0 ? bi : nblk - 1 - bi;
         const int c0 = b * 32;
         double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
         const int a_lo = T.mode == 0 ? 0 : b + 1, a_hi = T.mode == 0 ? b : nblk;
+        // everything this block reads from global memory is requested up front: D_b, X_b and
+        // the W fragments of the first coupling block; later W blocks are fetched one ahead
+        const double* D = T.D + (long long)b * 1024;
+        double dfr[8][2], xv[2][2];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = 4 * u + gk;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int col = (ct0 + c) * 8 + gi;
+                dfr[u][c] = T.mode == 0 ? D[k + 32 * col] : D[col + 32 * k];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) xv[c][v] = rv ? X[(long long)(c0 + (ct0 + c) * 8 + 2 * gk + v) * ws] : 0.0;
+        double bfc[8][2];
+        if (a_lo < a_hi) load_bf(a_lo, c0, bfc);
 #pragma unroll 1
         for (int a = a_lo; a < a_hi; ++a) {
+            double bfn[8][2];
+            if (a + 1 < a_hi) load_bf(a + 1, c0, bfn);
             const int k0 = a * 32;
-            double bf[8][2], af[8];
+            double af[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = k0 + 4 * u + gk;
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int col = c0 + (ct0 + c) * 8 + gi;
-                    bf[u][c] = T.mode == 0 ? T.W[k + (long long)col * ldw] : T.W[col + (long long)k * ldw];
-                }
-                af[u] = sY[(size_t)k * TRM_LD + row];
-            }
+            for (int u = 0; u < 8; ++u) af[u] = sY[(size_t)(k0 + 4 * u + gk) * TRM_LD + row];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
 #pragma unroll
-                for (int c = 0; c < 2; ++c) dmma_leaf(acc[c][0], acc[c][1], af[u], bf[u][c]);
+                for (int c = 0; c < 2; ++c) dmma_leaf(acc[c][0], acc[c][1], af[u], bfc[u][c]);
+            if (a + 1 < a_hi) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) { bfc[u][0] = bfn[u][0]; bfc[u][1] = bfn[u][1]; }
+            }
         }
         // T = X_b - acc
 #pragma unroll
@@ -1120,22 +1149,17 @@ __global__ void __launch_bounds__(TRM_THREADS) k_leaf_trsm_rows(const TrsmItem* 
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
                 const int col = (ct0 + c) * 8 + 2 * gk + v;
-                sT[col * TRM_LD + row] = (rv ? X[(long long)(c0 + col) * ws] : 0.0) - acc[c][v];
+                sT[col * TRM_LD + row] = xv[c][v] - acc[c][v];
             }
         __syncthreads();
         // Y_b = T D_b (mode 0) or T D_b^T (mode 1)
-        const double* D = T.D + (long long)b * 1024;
         double y[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int k = 4 * u + gk;
             const double a = sT[k * TRM_LD + row];
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int col = (ct0 + c) * 8 + gi;
-                const double d = T.mode == 0 ? D[k + 32 * col] : D[col + 32 * k];
-                dmma_leaf(y[c][0], y[c][1], a, d);
-            }
+            for (int c = 0; c < 2; ++c) dmma_leaf(y[c][0], y[c][1], a, dfr[u][c]);
         }
 #pragma unroll
         for (int c = 0; c < 2; ++c)
