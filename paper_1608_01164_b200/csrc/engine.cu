@@ -561,7 +561,7 @@ void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs) {
 static const bool g_psolve_off = std::getenv("SPG_PSOLVE_OFF") != nullptr;
 static const bool g_chol_tv_off = std::getenv("SPG_CHOL_TV_OFF") != nullptr;   // A/B: sequential subtree solves in the Cholesky
 // subtrees of at least this depth are solved subtree-parallel inside the Cholesky (smaller: k_hsolve2)
-static const int g_chol_tv_min = std::getenv("SPG_CHOL_TV_MIN") ? std::atoi(std::getenv("SPG_CHOL_TV_MIN")) : 5;
+static const int g_chol_tv_min = std::getenv("SPG_CHOL_TV_MIN") ? std::atoi(std::getenv("SPG_CHOL_TV_MIN")) : 4;
 
 void Engine::hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items) {
     if (items.empty()) return;
