@@ -752,6 +752,7 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
     double* sInvd = sLc + 32 * 33;              // 1 / L11(j, j)
     double* sS = sInvd + 32;                    // 16 x 17 half-block update
     __shared__ unsigned long long sBar[32];
+    __shared__ unsigned long long sBarC;   // helpers 0-3 -> warp 1: rows 32..63 of the panel updated (h2)
     __shared__ int sFail;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gi = lane >> 2, gk = lane & 3;
@@ -759,6 +760,7 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
     if (tid == 0) {
         sFail = 0;
         for (int j = 0; j < 32; ++j) mbar_init(&sBar[j], 32);   // all 32 lanes of warp 0 arrive
+        mbar_init(&sBarC, 4 * 32);
     }
     if (!C.w_zeroed)
         for (int j = warp; j < n; j += C4_NW)   // W strictly lower = 0 (column j, rows > j)
@@ -879,6 +881,13 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
 #pragma unroll
                 for (int c = 0; c < 32; ++c) D[lane + 32 * c] = t[c];
             }
+            // (c) the first 32 rows of L21 (what the next (a) reads), here while the helpers run
+            // the lookahead: wait for h2 on rows 32..63 (helpers 0-3, first tile each)
+            if (mr > 32) {
+                if (J > 0) mbar_wait(&sBarC, (pi - 1) & 1);
+                __syncwarp();
+                c4_times_d(cur, ldp, sD, 4, 8, 1, gi, gk);
+            }
         } else {
             const int hw = warp - 2;
             if (J + 32 < n && !(dflags & 16)) {   // M[J+32:, J+32:J+64] -> nxt (cp.async, 16 B, coalesced)
@@ -895,8 +904,15 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
                 // (h1) rest of the previous panel's L21: rows 64.. (relative to J-32)
                 if (!(dflags & 4)) c4_times_d(prv, ldp, sDp, 8 + hw, (mr + 32) / 8, C4_HELP, gi, gk);
                 c4_helper_sync();
-                // (h2) cur[32:] -= prv[64:] prv[32:64]^T
-                if (!(dflags & 4)) c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw, mr / 8, C4_HELP, gi, gk);
+                // (h2) cur[32:] -= prv[64:] prv[32:64]^T; helpers 0-3 do rows 32..63 first and signal warp 1
+                if (hw < 4 && mr > 32) {
+                    if (!(dflags & 4)) c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw, 5 + hw, 1, gi, gk);
+                    __syncwarp();
+                    mbar_arrive(&sBarC);
+                    if (!(dflags & 4)) c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw + C4_HELP, mr / 8, C4_HELP, gi, gk);
+                } else if (!(dflags & 4)) {
+                    c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw, mr / 8, C4_HELP, gi, gk);
+                }
                 // (h3) panel J-32 -> W
                 if (!(dflags & 1)) c4_copy_to_w(prv, ldp, C.W, ldw, J - 32, 0, mr + 32, hw, C4_HELP, lane);
             }
@@ -967,24 +983,9 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
                 }
             }
         }
-        __syncthreads();
+        __syncthreads();   // (c) ran inside (b1); one barrier per panel
         C4_TRACE(3);
-        // (c) the first 32 rows of L21 (what the next (a) reads)
-        if (tr && (dflags & 32) && warp == 0) {   // diagnostics: split phase (c) of warp 0
-            const double a0 = cur[32 + gi];
-            const long long t0 = clock64();
-            const double a1 = cur[32 + gi + ldp] + a0;
-            const long long t1 = clock64();
-            double x = 0.0, y = 0.0;
-            dmma_leaf(x, y, a1, a1);
-            dmma_leaf(x, y, a1, x);
-            const long long t2 = clock64() + (long long)(x != 12345.0);
-            if (lane == 0) { tr[pi * 8 + 6] = t1 - t0; tr[pi * 8 + 7] = t2 - t1; }
-            if (x == 1.2345) cur[0] = y;
-        }
-        if (warp < 4 && mr > 32) c4_times_d(cur, ldp, sD, 4 + warp, 5 + warp, 1, gi, gk);
         C4_TRACE(4);
-        __syncthreads();
         C4_TRACE(5);
     }
 #undef C4_TRACE
