@@ -170,7 +170,7 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     }
     ev_base2_ = tree_.nnodes() * (nside + 2) + 4 * nside + 8;
     ev_base3_ = ev_base2_ + 2 * tree_.nnodes();
-    events_.resize((size_t)ev_base3_ + 2 * (size_t)tree_.nnodes());
+    events_.resize((size_t)ev_base3_ + 2 * (size_t)tree_.nnodes() + 2);   // + fork/join of split truncations
     for (auto& e : events_) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (int t = 0; t < std::max(1, tree_.depth); ++t) {
         double* p;
@@ -334,9 +334,39 @@ std::unique_ptr<DHodlr> Engine::new_hodlr() {
 // ---------------------------------------------------------------- truncation batch
 static const double g_tsqr_segk = std::getenv("SPG_TSQR_SEGK") ? std::atof(std::getenv("SPG_TSQR_SEGK")) : 48.0;
 
+// Level-batched truncations mix a few tall tasks (top levels: long TSQR chains with a merge
+// level) with many short ones.  On the main stream outside the Cholesky the tall ones run on
+// a side stream next to the short ones, so their merge / core / apply chain overlaps the
+// short tasks' launches instead of following them.  Both halves take their workspace from
+// the main stack, the tall half's kept until the join.  SPG_TRUNC_SPLIT_OFF=1: one batch.
+static const bool g_trunc_split_off = std::getenv("SPG_TRUNC_SPLIT_OFF") != nullptr;
+static const int g_trunc_tall = std::getenv("SPG_TRUNC_TALL") ? std::atoi(std::getenv("SPG_TRUNC_TALL")) : 2048;
+
 void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     if (tasks.empty()) return;
+    if (side_sel_ < 0 && cur_op_ != 6 && !g_trunc_split_off && tasks.size() >= 2) {
+        std::vector<TTask> tall, flat;
+        for (auto& t : tasks) (std::max(t.p, t.s) > g_trunc_tall ? tall : flat).push_back(t);
+        if (!tall.empty() && !flat.empty()) {
+            const long long mark = ws_->mark();
+            const int evf = ev_base3_ + 2 * tree_.nnodes(), evj = evf + 1;
+            record(p, evf);
+            side_sel_ = 0;
+            wait(p, evf);
+            trunc_batch(p, tall, *ws_, false);   // workspace held until the join
+            record(p, evj);
+            side_sel_ = -1;
+            trunc_batch(p, flat, *ws_, true);
+            wait(p, evj);
+            ws_->release(mark);
+            return;
+        }
+    }
     Workspace& wsp = side_sel_ >= 0 ? *ws_side_[side_sel_] : *ws_;   // each stream has its own stack
+    trunc_batch(p, tasks, wsp, true);
+}
+
+void Engine::trunc_batch(Plan& p, std::vector<TTask> tasks, Workspace& wsp, bool release) {
     const long long mark = wsp.mark();
     std::vector<int3> it0, itm;
     for (size_t i = 0; i < tasks.size(); ++i) {
@@ -380,7 +410,7 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
         for (const auto& t : tasks) prof_rows_ = std::max(prof_rows_, std::max(t.p, t.s));
     }
     push_timed(p, PC_TRUNC, [b, ws, eps, status](cudaStream_t st) { launch_truncate(b, ws, eps, status, st); });
-    wsp.release(mark);
+    if (release) wsp.release(mark);
 }
 
 // ---------------------------------------------------------------- GEMM batch

@@ -160,6 +160,7 @@ public:
     // ---- plan builders (append launches to `p`) ------------------------------
     // truncation batch (lowrank.hpp:67-86); tasks' workspace is assigned here
     void trunc(Plan& p, std::vector<TTask> tasks);
+    void trunc_batch(Plan& p, std::vector<TTask> tasks, Workspace& wsp, bool release);
     void gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>& caps);
     // Y = H|_sub X (trans: H|_sub^T X) for each request (apply_rec/applyT_rec, hodlr.hpp:202-249)
     struct ApplyReq { const DHodlr* H; int root; int trans; const double* X; const int* ncp; double* Y; };
