@@ -414,6 +414,8 @@ void Engine::trunc_batch(Plan& p, std::vector<TTask> tasks, Workspace& wsp, bool
 }
 
 // ---------------------------------------------------------------- GEMM batch
+static const int g_gemm_fill = std::getenv("SPG_GEMM_FILL") ? std::atoi(std::getenv("SPG_GEMM_FILL")) : 2;     // CTAs per SM targeted by split-K
+static const int g_gemm_minkt = std::getenv("SPG_GEMM_MINKT") ? std::atoi(std::getenv("SPG_GEMM_MINKT")) : 4;   // k-tiles per split, at least
 static const bool g_gemm_split_v1 = std::getenv("SPG_GEMM_SPLIT_V1") != nullptr;   // A/B: split-K only for K >= 2048
 
 void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>& caps) {
@@ -431,7 +433,8 @@ void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>&
             base += t;
             ktiles += t * ((caps[i].z + 15) / 16);
         }
-    const long long chunk = std::max<long long>(8, (ktiles + 2 * 148 - 1) / std::max<long long>(2 * 148, base));
+    const long long fillc = (long long)g_gemm_fill * 148;
+    const long long chunk = std::max<long long>(g_gemm_minkt, (ktiles + fillc - 1) / std::max<long long>(fillc, base));
     for (size_t i = 0; i < items.size(); ++i) {
         GemmItem& g = items[i];
         const int mM = caps[i].x, mN = caps[i].y, mK = caps[i].z;
