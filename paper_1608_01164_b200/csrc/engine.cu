@@ -592,6 +592,7 @@ void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs) {
 }
 
 static const bool g_psolve_off = std::getenv("SPG_PSOLVE_OFF") != nullptr;
+static const int g_psolve_min = std::getenv("SPG_PSOLVE_MIN") ? std::atoi(std::getenv("SPG_PSOLVE_MIN")) : 2;   // smallest subtree depth solved subtree-parallel
 static const bool g_chol_tv_off = std::getenv("SPG_CHOL_TV_OFF") != nullptr;   // A/B: sequential subtree solves in the Cholesky
 // subtrees of at least this depth are solved subtree-parallel inside the Cholesky (smaller: k_hsolve2)
 static const int g_chol_tv_min = std::getenv("SPG_CHOL_TV_MIN") ? std::atoi(std::getenv("SPG_CHOL_TV_MIN")) : 4;
@@ -602,7 +603,7 @@ void Engine::hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items) {
         std::vector<HSolveItem> big, small;
         for (const auto& it : items) {
             const int dep = tree_.depth - tree_.level[it.root];   // levels below the root
-            (dep >= 2 ? big : small).push_back(it);
+            (dep >= g_psolve_min ? big : small).push_back(it);
         }
         if (!big.empty()) psolve(p, W, big);
         if (small.empty()) return;
