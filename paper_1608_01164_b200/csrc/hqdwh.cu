@@ -449,7 +449,7 @@ std::unique_ptr<HqdwhState> make_state(int n, int b, int n_min, double eps, doub
     st->X = E.new_hodlr(); st->Z = E.new_hodlr(); st->W = E.new_hodlr(); st->Y = E.new_hodlr();
     st->V = E.new_hodlr(); st->WK = E.new_hodlr(); st->P = E.new_hodlr();
     const int wbl = 3 * b + 1;
-    const size_t tmp_doubles = (size_t)n * std::max(wbl, 4 * b + 4) + 8 * (size_t)n + 128;
+    const size_t tmp_doubles = (size_t)n * std::max(wbl, 4 * b + 4) + 8 * (size_t)n + 128 + 165000;   // + Hager chunk maps (k_seq.cu)
     SPG_CUDA(cudaMalloc(&st->d_bands, sizeof(double) * band_len(n, b)));
     SPG_CUDA(cudaMalloc(&st->d_tmp, sizeof(double) * tmp_doubles));
     SPG_CUDA(cudaMalloc(&st->d_rdiag, sizeof(double) * (size_t)(2 * b + 1) * n));

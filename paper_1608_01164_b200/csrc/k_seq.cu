@@ -5,7 +5,9 @@
 //     (estimate_l0 / hager_norm1 / BandedLu, estimates.hpp:40-80, banded_lu.hpp:16-93)
 //   * Givens reduction of [s A; I] -> R (reduce_banded = reduce_tridiag for b = 1,
 //     fast_qr.hpp:83-232)
+#include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -286,7 +288,7 @@ __device__ __forceinline__ void eb_cpa(void* dst, const void* src, int bytes) {
 
 __global__ void __launch_bounds__(64) k_est_l0_band(int n, int b, const double* __restrict__ bands,
                                                    const double* alpha_p, double* lu, int* piv, double* vecs,
-                                                   double* out, unsigned* status) {
+                                                   double* out, unsigned* status, int chunked) {
     __shared__ double sM[2][EB_B + 2];
     __shared__ int sP[2];
     __shared__ double sRed[2];
@@ -411,11 +413,12 @@ __global__ void __launch_bounds__(64) k_est_l0_band(int n, int b, const double* 
     }
     __syncthreads();
     if (tid == 0) g_seq_trace[6] = clock64();
+    if (chunked && tid == 0) vecs[5 * (size_t)n] = sSing ? 1.0 : 0.0;   // ctl[0] of the chunked Hager launches
     if (sSing) {
         if (tid == 0) { atomicOr(status, ST_SINGULAR); out[0] = 0.0; }
         return;
     }
-    if (warp != 0) return;
+    if (chunked || warp != 0) return;
     // ---- Hager (estimates.hpp:40-68) with the BandedLu solves on warp 0
     const int nch = (n + EB_CH - 1) / EB_CH;
     // chunk q = columns [32q, 32q + 32) of lu (+ invd, piv, an optional vector) into slot q % 3
@@ -576,7 +579,325 @@ __global__ void __launch_bounds__(64) k_est_l0_band(int n, int b, const double* 
     if (lane == 0) { out[0] = n1 / (sqrt((double)n) * (n1 * est)); g_seq_trace[7] = clock64(); }
 }
 
+// ------------------------------------------------------------ Hager for 2 <= b <= 16, chunk-parallel solves
+// hager_norm1 (estimates.hpp:40-68) over the BandedLu factor of k_est_l0_band (banded_lu.hpp:
+// 16-93). Each of the four triangular sweeps (L forward with the interchanges, U backward,
+// U^T forward, L^T backward with the interchanges) touches a sliding window of W = b or 2b
+// entries, so a chunk of its steps is an affine map of the W window entries it inherits
+// from the chunk processed before it. Phase 1: warp q runs chunk q once per basis vector
+// (lane m = 0: inherited window zero; lane m > 0: unit vector m - 1), which gives the map's
+// offset and columns. Phase 2: warp 0 chains the P maps from the known first window.
+// Phase 3: warp q re-runs chunk q on the true inherited window and writes the results.
+// The sweep is the reference's step order; only the inherited windows are formed through the
+// maps (rounding-level differences in the estimate, which only steers the QDWH schedule).
+constexpr int HG_RMAX = 2 * EB_B + 1;
+
+struct HgF {
+    const double* lu;
+    const double* invd;
+    const int* piv;
+    int n, b2, wd;
+    __device__ __forceinline__ double at(int r, int c) const { return lu[(long long)c * wd + (r - c + b2)]; }
+};
+
+// One chunk of sweep MODE (0 L fwd, 1 U bwd, 2 U^T fwd, 3 L^T bwd) over steps [s, e), called by
+// all 32 lanes together. m >= 0: basis run (m = 0 with v outside the window, m > 0 unit window
+// entry m - 1); m < 0: true run from window st[], results into out. Lanes with !valid run along
+// (they feed the shuffles) and write nothing. Lane l prefetches coefficient l + 1 of the step
+// 8 ahead into a register ring, so no L2 latency sits on the step chain.
+template <int MODE, int HG_R>
+__device__ __forceinline__ void hg_chunk(const HgF& F, int W, int s, int e, const double* __restrict__ v, int m, bool valid,
+                         const double* st, double* out, double* stout) {
+    const int n = F.n, lane = threadIdx.x & 31, len = e - s;
+    constexpr bool fwd = MODE == 0 || MODE == 2;
+    const bool use_v = valid && m <= 0;
+    const bool wr = valid && out != nullptr;
+    auto orig = [&](int i) -> double { return (use_v && i >= 0 && i < n) ? v[i] : 0.0; };
+    auto win = [&](int i) -> double { return !valid ? 0.0 : (m < 0 ? st[i] : (m > 0 && i == m - 1 ? 1.0 : 0.0)); };
+    auto kof = [&](int t) -> int { return fwd ? s + t : e - 1 - t; };
+    auto coef = [&](int k) -> double {   // coefficient lane + 1 of step k (0 outside the band)
+        const int i = lane + 1;
+        if (i > W) return 0.0;
+        if (MODE == 0 || MODE == 3) return k + i < n ? F.at(k + i, k) : 0.0;
+        if (MODE == 1) return k - i >= 0 ? F.at(k - i, k) : 0.0;
+        return k + i < n ? F.at(k, k + i) : 0.0;
+    };
+    auto aux = [&](int k) -> double { return (MODE == 0 || MODE == 3) ? (double)(F.piv[k] - k) : F.invd[k]; };
+    auto ovn = [&](int k) -> double {   // element entering the window after step k
+        return MODE == 1 ? orig(k - 1 - W) : (MODE == 3 ? orig(k - 1) : orig(k + 1 + W));
+    };
+    double reg[HG_R];
+#pragma unroll
+    for (int i = 0; i < HG_R; ++i) reg[i] = 0.0;
+    if (MODE == 3) {
+        reg[0] = orig(e - 1);
+#pragma unroll
+        for (int i = 1; i < HG_R; ++i) reg[i] = i <= W ? win(i - 1) : 0.0;
+    } else {
+#pragma unroll
+        for (int i = 0; i < HG_R; ++i) reg[i] = i < W ? win(i) : (i == W ? orig(MODE == 1 ? e - 1 - W : s + W) : 0.0);
+    }
+    constexpr int D = 4;
+    double rc[D], ra[D], ro[D];
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+        rc[u] = 0.0; ra[u] = 0.0; ro[u] = 0.0;
+        if (u < len) { const int k = kof(u); rc[u] = coef(k); ra[u] = aux(k); ro[u] = ovn(k); }
+    }
+    for (int t0 = 0; t0 < len; t0 += D) {
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+            const int t = t0 + u;
+            if (t < len) {
+                const int k = kof(t);
+                const double cu = rc[u], au = ra[u], ou = ro[u];
+                if (t + D < len) { const int kn = kof(t + D); rc[u] = coef(kn); ra[u] = aux(kn); ro[u] = ovn(kn); }
+                if (MODE == 3) {
+                    double ps[4] = {0.0, 0.0, 0.0, 0.0};   // four interleaved partial sums: short FMA chains
+#pragma unroll
+                    for (int i = 1; i < HG_R; ++i)
+                        if (i <= W) ps[i & 3] += __shfl_sync(0xffffffffu, cu, i - 1) * reg[i];
+                    reg[0] -= (ps[0] + ps[1]) + (ps[2] + ps[3]);
+                }
+                if (MODE == 0 || MODE == 3) {
+                    const int po = (int)au;
+                    double top = reg[0];
+#pragma unroll
+                    for (int i = 1; i <= EB_B; ++i) { const double ri = reg[i]; reg[i] = i == po ? top : ri; top = i == po ? ri : top; }
+                    reg[0] = top;
+                }
+                if (MODE == 3) {
+                    if (t + 1 < len) {   // x[k + W] is final: no later step reaches it
+                        double lv = 0.0;
+#pragma unroll
+                        for (int i = 0; i < HG_R; ++i) lv = i == W ? reg[i] : lv;
+                        if (wr && k + W < n) out[k + W] = lv;
+#pragma unroll
+                        for (int i = HG_R - 1; i > 0; --i) reg[i] = i <= W ? reg[i - 1] : reg[i];
+                        reg[0] = ou;
+                    }
+                } else {
+                    const double xk = MODE == 0 ? reg[0] : reg[0] * au;
+                    if (wr) out[k] = xk;
+#pragma unroll
+                    for (int i = 1; i < HG_R; ++i)
+                        if (i <= W) reg[i] -= __shfl_sync(0xffffffffu, cu, i - 1) * xk;
+#pragma unroll
+                    for (int i = 0; i < HG_R - 1; ++i) reg[i] = i < W ? reg[i + 1] : reg[i];
+#pragma unroll
+                    for (int i = 0; i < HG_R; ++i) reg[i] = i == W ? ou : reg[i];
+                }
+            }
+        }
+    }
+    if (MODE == 3 && wr) {
+#pragma unroll
+        for (int i = 0; i < HG_R; ++i)
+            if ((i == W || s == 0) && i <= W && s + i < n) out[s + i] = reg[i];
+    }
+    if (valid && stout) {
+#pragma unroll
+        for (int i = 0; i < HG_R; ++i)
+            if (i < W) stout[i] = reg[i];
+    }
+}
+
+// ---- the sweep as three launches over P chunks (one warp per chunk, one chunk per SM)
+// control block ctl = vecs + 5n: [0] singular (k_est_l0_band), [1] done, [2] est, [3] n1;
+// then the chunk maps T (P x HG_RMAX x 32) and the inherited windows Sg (P x 32)
+struct HgArgs {
+    HgF F;
+    int b, P, L;
+    double* ctl;
+    double* T;
+    double* Sg;
+};
+__device__ __forceinline__ bool hg_skip(const double* ctl) { return ctl[0] != 0.0 || ctl[1] != 0.0; }
+__device__ __forceinline__ int hg_W(int mode, int b) { return (mode == 1 || mode == 2) ? 2 * b : b; }
+
+template <int MODE, int HG_R>
+__global__ void __launch_bounds__(32) k_hg_map(HgArgs A, const double* __restrict__ v) {   // phase 1
+    if (hg_skip(A.ctl)) return;
+    const int q = blockIdx.x, n = A.F.n, W = hg_W(MODE, A.b);
+    if (q >= A.P - 1) return;
+    const int c = (MODE == 0 || MODE == 2) ? q : A.P - 1 - q;
+    const int s = c * A.L, e = min(n, (c + 1) * A.L);
+    for (int m0 = 0; m0 <= W; m0 += 32) {
+        const int m = m0 + (int)threadIdx.x;
+        hg_chunk<MODE, HG_R>(A.F, W, s, e, v, m, m <= W, nullptr, nullptr,
+                             A.T + ((size_t)q * HG_RMAX + min(m, W)) * (2 * EB_B));
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(32) k_hg_chain(HgArgs A, const double* __restrict__ v) {   // phase 2
+    if (hg_skip(A.ctl)) return;
+    const int lane = threadIdx.x, n = A.F.n, W = hg_W(MODE, A.b);
+    double st = 0.0;   // lane j: entry j of the window inherited by the chunk processed t-th
+    if (lane < W) st = MODE == 3 ? 0.0 : (MODE == 1 ? (n - 1 - lane >= 0 ? v[n - 1 - lane] : 0.0) : (lane < n ? v[lane] : 0.0));
+    A.Sg[lane] = st;
+    for (int t = 0; t + 1 < A.P; ++t) {
+        const double* Tq = A.T + (size_t)t * HG_RMAX * (2 * EB_B);
+        double a = Tq[lane];
+        for (int mm = 0; mm < W; ++mm) a += Tq[(mm + 1) * (2 * EB_B) + lane] * __shfl_sync(0xffffffffu, st, mm);
+        st = lane < W ? a : 0.0;
+        A.Sg[(t + 1) * 32 + lane] = st;
+    }
+}
+
+template <int MODE, int HG_R>
+__global__ void __launch_bounds__(32) k_hg_apply(HgArgs A, const double* __restrict__ v, double* out) {   // phase 3
+    if (hg_skip(A.ctl)) return;
+    const int q = blockIdx.x, n = A.F.n, W = hg_W(MODE, A.b), lane = threadIdx.x;
+    if (q >= A.P) return;
+    const int c = (MODE == 0 || MODE == 2) ? q : A.P - 1 - q;
+    const int s = c * A.L, e = min(n, (c + 1) * A.L);
+    hg_chunk<MODE, HG_R>(A.F, W, s, e, v, lane == 0 ? -1 : 1, lane == 0, A.Sg + (size_t)q * 32, out, nullptr);
+}
+
+__device__ double hg_bsum(double a, double* red) {   // 1024-thread block sum, same order in every call
+    a = wsum32(a);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    double r = 0.0;
+    for (int w = 0; w < 32; ++w) r += red[w];
+    return r;
+}
+
+__global__ void __launch_bounds__(1024) k_hg_init(int n, int b, const double* __restrict__ bands, const double* alpha_p,
+                                                  double* vecs, double* ctl) {
+    __shared__ double red[32];
+    if (ctl[0] != 0.0) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    double mx = 0.0;   // norm1 (banded.hpp:94-106)
+    for (int i = tid; i < n; i += 1024) {
+        double cs = fabs(bands[i]);
+        for (int d = 1; d <= b; ++d) {
+            const double* dg = bands + boff(n, d);
+            if (i + d < n) cs += fabs(dg[i]);
+            if (i - d >= 0) cs += fabs(dg[i - d]);
+        }
+        mx = fmax(mx, cs);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    double* x = vecs + n;
+    for (int i = tid; i < n; i += 1024) x[i] = 1.0 / n;
+    if (tid == 0) {
+        double m = 0.0;
+        for (int w = 0; w < 32; ++w) m = fmax(m, red[w]);
+        ctl[1] = 0.0; ctl[2] = 0.0; ctl[3] = m / *alpha_p;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_hg_after_solve(int n, int it, double* vecs, double* ctl) {
+    __shared__ double red[32];
+    if (hg_skip(ctl)) return;
+    const double* y = vecs + 2 * (size_t)n;
+    double* z = vecs + 3 * (size_t)n;
+    double e = 0.0;
+    for (int i = threadIdx.x; i < n; i += 1024) e += fabs(y[i]);
+    e = hg_bsum(e, red);
+    if (it > 0 && e <= ctl[2]) {   // every thread has read ctl[2] before the barrier below
+        __syncthreads();
+        if (threadIdx.x == 0) ctl[1] = 1.0;
+        return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) ctl[2] = e;
+    for (int i = threadIdx.x; i < n; i += 1024) z[i] = y[i] >= 0.0 ? 1.0 : -1.0;
+}
+
+__global__ void __launch_bounds__(1024) k_hg_after_solve_t(int n, double* vecs, double* ctl) {
+    __shared__ double red[32];
+    __shared__ double sz[32];
+    __shared__ int sj[32];
+    if (hg_skip(ctl)) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    double* x = vecs + n;
+    const double* y = vecs + 2 * (size_t)n;
+    double zmax = 0.0, ztx = 0.0;
+    int jm = 0x7fffffff;
+    for (int i = tid; i < n; i += 1024) {
+        const double av = fabs(y[i]);
+        if (av > zmax) { zmax = av; jm = i; }
+        ztx += y[i] * x[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oz = __shfl_xor_sync(0xffffffffu, zmax, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, jm, o);
+        if (oz > zmax || (oz == zmax && oj < jm)) { zmax = oz; jm = oj; }
+    }
+    if (lane == 0) { sz[tid >> 5] = zmax; sj[tid >> 5] = jm; }
+    ztx = hg_bsum(ztx, red);
+    zmax = 0.0;
+    jm = 0x7fffffff;
+    for (int w = 0; w < 32; ++w)
+        if (sz[w] > zmax || (sz[w] == zmax && sj[w] < jm)) { zmax = sz[w]; jm = sj[w]; }
+    if (jm == 0x7fffffff) jm = 0;
+    if (zmax <= ztx) {
+        if (tid == 0) ctl[1] = 1.0;
+        return;
+    }
+    __syncthreads();   // every thread has read x for ztx
+    for (int i = tid; i < n; i += 1024) x[i] = i == jm ? 1.0 : 0.0;
+}
+
+__global__ void k_hg_final(int n, const double* ctl, double* out) {
+    if (ctl[0] != 0.0) return;
+    const double n1 = ctl[3], est = ctl[2];
+    out[0] = n1 / (sqrt((double)n) * (n1 * est));
+}
+
+constexpr int HG_PMAX = 148;
+template <int HG_R>
+static void launch_hager_chunked(int n, int b, const double* bands, const double* alpha, const double* lu, const int* piv,
+                                 double* vecs, double* out, cudaStream_t st) {
+    HgArgs A;
+    A.b = b;
+    A.F = HgF{lu, vecs, piv, n, 2 * b, 3 * b + 1};
+    A.ctl = vecs + 5 * (size_t)n;
+    A.T = A.ctl + 8;
+    A.Sg = A.T + (size_t)HG_PMAX * HG_RMAX * (2 * EB_B);
+    // chunks of at least 2W + 1 steps (an inherited window never reaches past the chunk before)
+    // and at least 128 (the chain of phase 2 stays short against the chunk sweeps)
+    int P = std::min(HG_PMAX, n / std::max(4 * b + 1, 128));
+    if (P < 1) P = 1;
+    A.L = (n + P - 1) / P;
+    A.P = (n + A.L - 1) / A.L;
+    double* x = vecs + n;
+    double* y = vecs + 2 * (size_t)n;
+    double* z = vecs + 3 * (size_t)n;
+    double* t1 = vecs + 4 * (size_t)n;
+    k_hg_init<<<1, 1024, 0, st>>>(n, b, bands, alpha, vecs, A.ctl);
+    auto sweep = [&](auto mode_tag, const double* v, double* o) {
+        constexpr int M = decltype(mode_tag)::value;
+        if (A.P > 1) {
+            k_hg_map<M, HG_R><<<A.P - 1, 32, 0, st>>>(A, v);
+            k_hg_chain<M><<<1, 32, 0, st>>>(A, v);
+        } else {
+            k_hg_chain<M><<<1, 32, 0, st>>>(A, v);
+        }
+        k_hg_apply<M, HG_R><<<A.P, 32, 0, st>>>(A, v, o);
+    };
+    for (int it = 0; it < 5; ++it) {   // hager_norm1 (estimates.hpp:40-68); kernels after a break exit at once
+        sweep(std::integral_constant<int, 0>{}, x, t1);   // BandedLu::solve: L, then U
+        sweep(std::integral_constant<int, 1>{}, t1, y);
+        k_hg_after_solve<<<1, 1024, 0, st>>>(n, it, vecs, A.ctl);
+        sweep(std::integral_constant<int, 2>{}, z, t1);   // BandedLu::solve_transposed: U^T, then L^T
+        sweep(std::integral_constant<int, 3>{}, t1, y);
+        k_hg_after_solve_t<<<1, 1024, 0, st>>>(n, vecs, A.ctl);
+    }
+    k_hg_final<<<1, 1, 0, st>>>(n, A.ctl, out);
+    SPG_LAUNCH_CHECK();
+}
+
 static const bool g_l0_window = std::getenv("SPG_L0_WINDOW") != nullptr;   // A/B: the windowed single-warp kernel
+static const bool g_hager_seq = std::getenv("SPG_HAGER_BAND_SEQ") != nullptr;   // A/B: Hager solves on one warp
 
 void launch_estimate_l0(int n, int b, const double* bands, const double* alpha, double* lu_work, int* piv,
                         double* vecs, double* out_l0, unsigned* status, cudaStream_t st) {
@@ -585,8 +906,12 @@ void launch_estimate_l0(int n, int b, const double* bands, const double* alpha, 
         return;
     }
     if (b <= EB_B && !g_l0_window) {   // (caller provides >= 5 n doubles at vecs)
-        k_est_l0_band<<<1, 64, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status);
+        k_est_l0_band<<<1, 64, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status, g_hager_seq ? 0 : 1);
         SPG_LAUNCH_CHECK();
+        if (!g_hager_seq) {
+            if (b <= 8) launch_hager_chunked<17>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, st);
+            else launch_hager_chunked<33>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, st);
+        }
         return;
     }
     k_est_l0_w<<<1, 32, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status);

@@ -1,4 +1,5 @@
-"""A/B of the banded l0 estimate: register-resident kernel vs the windowed one (SPG_L0_WINDOW)."""
+"""A/B of the banded l0 estimate against a variant selected by env AB_ENV (default SPG_L0_WINDOW:
+the windowed kernel; SPG_HAGER_BAND_SEQ: the single-warp Hager solves)."""
 import os
 import subprocess
 import sys
@@ -25,7 +26,7 @@ ra = subprocess.run([sys.executable, __file__, "child", *names], capture_output=
 print(ra.stderr[-2000:])
 a = ra.stdout.split("\n")
 b = subprocess.run([sys.executable, __file__, "child", *names], capture_output=True, text=True,
-                   env={**os.environ, "SPG_L0_WINDOW": "1"}).stdout.split("\n")
+                   env={**os.environ, os.environ.get("AB_ENV", "SPG_L0_WINDOW"): "1"}).stdout.split("\n")
 for x, y in zip(a, b):
     if not x:
         continue

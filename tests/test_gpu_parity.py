@@ -321,3 +321,17 @@ def test_cpp_dropin_runs(root):
     r = subprocess.run([out, "/tmp/spg_npd_bands.txt"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout
+
+
+# chunk-parallel Hager solves of the banded l0 estimate (k_seq.cu k_hg_*): several chunks,
+# ragged last chunk, every window width, interchanges; vs the restated estimate_l0
+# (estimates.hpp:40-80) on the same alpha
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,b,seed", [(3000, 2, 5), (2778, 12, 6), (5000, 16, 7), (1290, 5, 8), (700, 9, 9)])
+def test_banded_l0_chunked_vs_restatement(restate, n, b, seed):
+    A = S.dimer_chain(n, 1.0, 0.8, 0.0, seed, b=b, s=0.05 / (2 * b + 1))
+    r = S.hqdwh(A, 128, 1e-10)
+    l0 = restate.estimate_l0(A.bands, r.alpha)
+    assert abs(r.l0 - l0) <= 1e-12 * l0
+    assert round(r.P.trace()) == n // 2
+    r.close()
