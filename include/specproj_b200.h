@@ -74,6 +74,16 @@ typedef struct spg_info {
     /* CUDA graph of the Cholesky-based iteration (replayed iterations-1 times) */
     int graph_used;
     long long graph_nodes;
+    /* per-phase work counters, summed over iterations; phase index 0 setup, 1 first
+     * iterate, 2 multiply, 3 Cholesky, 4 solve, 5 solveT, 6 axpby + symmetrize:
+     *   ph_trunc_bytes : recompression algorithmic bytes 8 (p+s)(k_in+k_out)
+     *   ph_qr_flops    : Householder QR of both truncation factors, 4 m k^2 - 4/3 k^3 each
+     *                    (m = max, k = min of rows and k_in; dense_factor.hpp:34-101)
+     *   ph_core_flops  : truncation core product and basis products, 2 k_u k_v k_in +
+     *                    2 (p k_u + s k_v) k_out (lowrank.hpp:78-83; Jacobi sweeps not counted)
+     *   ph_gemm_flops  : batched GEMM items, 2 M N K
+     *   ph_leaf_flops  : leaf Cholesky, s^3 / 3 per leaf                              */
+    double ph_trunc_bytes[8], ph_qr_flops[8], ph_core_flops[8], ph_gemm_flops[8], ph_leaf_flops[8];
 } spg_info;
 
 /* Runs the hQDWH projector on device 0 (current device).  `bands` is host
@@ -132,6 +142,17 @@ int spg_micro_kernel(int which, int n, int reps, double* out, int nout);
 int spg_measure_dmma_tflops(double* out);
 /* compiled capacities */
 int spg_kcap(void);
+/* frees every cached projector plan (engine, HODLR storage, CUDA graphs) of every
+ * device; returns how many were freed.  Plans are otherwise kept (at most 2) for
+ * repeated calls of the same shape. */
+int spg_release_plan_cache(void);
+
+/* R of the stacked QR of [A; I] for banded symmetric A (`bands` as above, no scaling):
+ * method 1 = the Givens sweep of reduce_tridiag / reduce_banded (fast_qr.hpp:83-232),
+ * method 0 = the band Cholesky of A^2 + I (b <= 16); the two constructions the first
+ * iterate selects between by c0.  rdiag[d*n + i] = R(i, i+d), d = 0..2b
+ * (zero past the end).  Diagnostics / parity tests. */
+int spg_stacked_qr_r(int n, int b, const double* bands, int method, double* rdiag);
 
 /* ---- component-level entry points (parity tests of each HODLR operation) --- */
 typedef struct spg_ctx spg_ctx;
@@ -143,7 +164,10 @@ int spg_ctx_download(spg_ctx* c, int slot, int* ranks, double* data);
 /* op codes: 1 multiply(dst = a*b), 2 axpby(dst = alpha a + beta b), 3 symmetrize(dst in place),
  *           4 cholesky(dst = chol(a)), 5 solve_upper_right(dst W = a, W = b),
  *           6 solve_upperT_right(dst W^T = a), 7 scale_shift(dst = alpha dst + beta I),
- *           8 from_banded(dst, bands in `bands`, b = band) */
+ *           8 multiply, upper blocks and leaves only (dst.lower left at rank 0; the
+ *             product the QDWH iteration feeds to the Cholesky),
+ *           9 cholesky as the QDWH iteration runs it (W12 truncation deferred, Schur
+ *             update from the untruncated pair) */
 int spg_ctx_op(spg_ctx* c, int op, int dst, int a, int b, double alpha, double beta);
 int spg_ctx_from_banded(spg_ctx* c, int dst, int b, const double* bands);
 /* single truncate (lowrank.hpp:67-86) on device: U p x k, V s x k row-major in,

@@ -19,6 +19,8 @@ from . import hodlr_np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libspecproj_ref.so")
+# memory-patched variant (oracle/patch_memory.py; bitwise equal, frees assemble_q's aux columns)
+REF_PATCHED_SO = os.path.join(HERE, "_ref", "libspecproj_ref_patched.so")
 RESTATE_SO = os.path.join(HERE, "_build", "librestate.so")
 
 _dp = C.POINTER(C.c_double)
@@ -46,8 +48,8 @@ def unpack_bands(packed, n, b):
     return out
 
 
-def ref_available():
-    return os.path.exists(REF_SO)
+def ref_available(patched=False):
+    return os.path.exists(REF_PATCHED_SO if patched else REF_SO)
 
 
 def restate_available():
@@ -105,6 +107,9 @@ class RefLib:
             "ref_result_l0": ([vp], C.c_double),
             "ref_result_diag": ([vp, _dp], None),
             "ref_result_hodlr": ([vp, C.c_int], vp),
+            "ref_is_patched": ([], C.c_int),
+            "ref_make_dimer_chain": ([C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                                      C.c_ulonglong, _dp], C.c_int),
             "ref_synth_banded": ([C.c_int, C.c_int, C.c_double, C.c_ulonglong, _dp], C.c_int),
             "ref_write_sbm": ([C.c_int, C.c_int, _dp, C.c_char_p], C.c_int),
             "ref_read_sbm": ([C.c_char_p, C.POINTER(C.c_int), C.c_void_p], C.c_int),
@@ -170,6 +175,21 @@ class RefLib:
         if self.L.ref_read_sbm(path.encode(), nb.ctypes.data_as(C.POINTER(C.c_int)), out.ctypes.data_as(C.c_void_p)):
             raise RefError(self.err())
         return unpack_bands(out, n, b)
+
+    def dimer_chain(self, n, t1, t2, eps_dis, seed, b=1, s=0.0):
+        """SURVEY.md §8d dimer chain generated on the oracle side (no product library)."""
+        out = np.zeros((b + 1) * n - b * (b + 1) // 2)
+        if self.L.ref_make_dimer_chain(n, b, t1, t2, eps_dis, s, seed, _d(out)):
+            raise RefError("ref_make_dimer_chain: invalid arguments")
+        return unpack_bands(out, n, b)
+
+    def config_bands(self, c, seed_offset=0):
+        """bands of a BASELINE config dict (paper_1608_01164_b200.configs.CONFIGS entry)"""
+        return self.dimer_chain(c["n"], c["t1"], c["t2"], c["eps_dis"], c["seed"] + seed_offset, b=c["b"], s=c["s"])
+
+    @property
+    def patched(self):
+        return bool(self.L.ref_is_patched())
 
     def synth_banded(self, n, b, gap, seed):
         """synth.hpp:106-137 with SpectrumSpec::uniform_two_sided(n, gap) (the reference tests' inputs)."""

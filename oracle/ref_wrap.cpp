@@ -16,7 +16,9 @@
 
 #include <chrono>
 #include <cstring>
+#include <algorithm>
 #include <exception>
+#include <random>
 #include <string>
 #include <vector>
 #include <xmmintrin.h>
@@ -274,6 +276,40 @@ int ref_read_sbm(const char* path, int* nb, double* bands) {   // bands may be n
         }
         return 0;
     } catch (const std::exception& e) { return classify(e); }
+}
+
+// 1 when this library was built against the memory-patched fast_qr.hpp (oracle/patch_memory.py)
+int ref_is_patched() {
+#ifdef REF_PATCHED
+    return 1;
+#else
+    return 0;
+#endif
+}
+
+// BASELINE dimer chains, generated on the oracle side so the reference arm
+// never loads the product library: bond i is t1 for even i and t2 for odd i, diagonal
+// eps_dis * U(-1,1), then an optional band perturbation s * U(-1,1) for d = 0..b
+// (std::mt19937_64 + uniform_real_distribution<double>(-1, 1), diagonal drawn first).
+// No FMA contraction, so the bands are bitwise those of the product's spg_make_dimer_chain.
+__attribute__((optimize("fp-contract=off")))
+int ref_make_dimer_chain(int n, int b, double t1, double t2, double eps_dis, double s,
+                         unsigned long long seed, double* bands) {
+    if (n < 2 || b < 1 || b >= n) return REF_INVALID;
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    const std::size_t len = static_cast<std::size_t>(b + 1) * n - static_cast<std::size_t>(b) * (b + 1) / 2;
+    std::fill(bands, bands + len, 0.0);
+    for (int i = 0; i < n; ++i) bands[i] = eps_dis * dist(rng);
+    for (int i = 0; i + 1 < n; ++i) bands[n + i] = (i % 2 == 0) ? t1 : t2;
+    if (s != 0.0) {
+        std::size_t off = 0;
+        for (int d = 0; d <= b; ++d) {
+            for (int i = 0; i + d < n; ++i) bands[off + i] += s * dist(rng);
+            off += n - d;
+        }
+    }
+    return REF_OK;
 }
 
 int ref_synth_banded(int n, int b, double gap, unsigned long long seed, double* bands) {

@@ -83,7 +83,11 @@ class _Info(C.Structure):
                 ("prof_ms_hsolve", C.c_double), ("prof_ms_leaf", C.c_double),
                 ("prof_batches_trunc", C.c_longlong), ("prof_batches_gemm", C.c_longlong),
                 ("prof_batches_hsolve", C.c_longlong), ("prof_batches_leaf", C.c_longlong),
-                ("graph_used", C.c_int), ("graph_nodes", C.c_longlong)]
+                ("graph_used", C.c_int), ("graph_nodes", C.c_longlong),
+                ("ph_trunc_bytes", C.c_double * 8), ("ph_qr_flops", C.c_double * 8), ("ph_core_flops", C.c_double * 8),
+                ("ph_gemm_flops", C.c_double * 8), ("ph_leaf_flops", C.c_double * 8)]
+
+PHASES = ("setup", "first", "multiply", "cholesky", "solve", "solveT", "axpby_sym")
 
 
 class _Diag(C.Structure):
@@ -100,7 +104,7 @@ ABI_SYMBOLS = (
     "spg_make_dimer_chain", "spg_make_random_banded", "spg_kcap", "spg_ctx_create", "spg_ctx_free",
     "spg_ctx_upload", "spg_ctx_flat_size", "spg_ctx_download", "spg_ctx_op", "spg_ctx_from_banded",
     "spg_truncate", "spg_set_profile", "spg_measure_dmma_tflops", "spg_micro_kernel", "spg_host_alloc",
-    "spg_host_free", "spg_hqdwh_shifts",
+    "spg_host_free", "spg_hqdwh_shifts", "spg_release_plan_cache", "spg_stacked_qr_r",
 )
 
 
@@ -130,6 +134,8 @@ def load_library(path: str | None = None):
                                   C.c_ulonglong, _dp], C.c_int),
         "spg_make_random_banded": ([C.c_int, C.c_int, C.c_ulonglong, _dp], C.c_int),
         "spg_kcap": ([], C.c_int),
+        "spg_release_plan_cache": ([], C.c_int),
+        "spg_stacked_qr_r": ([C.c_int, C.c_int, _dp, C.c_int, _dp], C.c_int),
         "spg_ctx_create": ([C.c_int, C.c_int, C.c_double, C.c_int], vp),
         "spg_ctx_free": ([vp], None),
         "spg_ctx_upload": ([vp, C.c_int, _ip, _dp], C.c_int),
@@ -491,6 +497,9 @@ def _result_from_handle(h, n, n_min) -> ProjectorResult:
     _raise(L.spg_result_diag(h, diag))
     per = [IterationDiag(d.k, d.l, d.c, d.max_rank, d.memory_bytes, d.wall_ms) for d in diag[:info.iterations]]
     infod = {name: getattr(info, name) for name, _ in _Info._fields_}
+    for name, _ in _Info._fields_:
+        if name.startswith("ph_"):
+            infod[name] = list(infod[name])[:len(PHASES)]
     return ProjectorResult(info.iterations, info.alpha, info.l0, per, infod, h, PartitionTree(n, n_min))
 
 
@@ -552,6 +561,20 @@ def cli_path() -> str:
     return os.path.join(os.path.dirname(_LIB_PATH), "specproj_b200")
 
 
+def stacked_qr_r(A: BandedSymmetric, method: str = "givens") -> np.ndarray:
+    """R of the stacked QR of [A; I] on the device (reduce_tridiag / reduce_banded,
+    fast_qr.hpp:83-232): diagonals (2b+1, n), rd[d, i] = R(i, i+d).  method "givens" is the
+    rotation sweep, "cholesky" the band Cholesky of A^2 + I (equal up to row signs)."""
+    out = np.zeros((2 * A.b + 1) * A.n)
+    _raise(load_library().spg_stacked_qr_r(A.n, A.b, _d(A.packed()), 1 if method == "givens" else 0, _d(out)))
+    return out.reshape(2 * A.b + 1, A.n)
+
+
+def release_plan_cache() -> int:
+    """Frees every cached projector plan (spg_release_plan_cache)."""
+    return int(load_library().spg_release_plan_cache())
+
+
 def set_profile(on: bool = True):
     """Profile mode: bracket every batched launch with CUDA events (per-class device times in info)."""
     load_library().spg_set_profile(1 if on else 0)
@@ -602,7 +625,7 @@ class HodlrContext:
     solve_upper_right, solve_upperT_right, hodlr_scale + add_scaled_identity)."""
 
     OPS = {"multiply": 1, "axpby": 2, "symmetrize": 3, "cholesky": 4, "solve_upper_right": 5,
-           "solve_upperT_right": 6, "scale_shift": 7}
+           "solve_upperT_right": 6, "scale_shift": 7, "multiply_upper": 8, "cholesky_deferred": 9}
 
     def __init__(self, n, n_min, eps, nslots=4):
         L = load_library()

@@ -15,6 +15,9 @@ CONFIGS = {
     "sweep0.99": dict(n=65536, b=1, t1=1.0, t2=0.99, eps_dis=0.002, s=0.0, nmin=256, eps=1e-10, seed=42),
     "sweep0.999": dict(n=65536, b=1, t1=1.0, t2=0.999, eps_dis=2e-4, s=0.0, nmin=256, eps=1e-10, seed=43),
     "large": dict(n=131072, b=16, t1=1.0, t2=0.95, eps_dis=0.0, s=0.02 / 33, nmin=512, eps=1e-8, seed=5),
+    # parity-only stress case (not a BASELINE config): t2 = 0.9999 puts c0 above 1e8, where a
+    # Cholesky-based first iterate would lose accuracy
+    "stress0.9999": dict(n=16384, b=1, t1=1.0, t2=0.9999, eps_dis=2e-5, s=0.0, nmin=256, eps=1e-10, seed=6),
 }
 HEADLINE = "sweep0.999"
 

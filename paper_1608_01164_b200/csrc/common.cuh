@@ -45,6 +45,23 @@ struct CudaError : std::runtime_error {
 // load before the next iteration; issuing cp.async instead keeps all of a thread's
 // copies in flight at once (one memory latency per staging pass, not one per element).
 #ifdef __CUDACC__
+// Work counters of one truncation (SURVEY.md §8d units, per device counter block
+// (double*)(status + 16)): [0] recompression bytes 8 (p+s)(k_in+k_out), [2] tasks,
+// [4] Householder QR flops of both factors (4 m k^2 - 4/3 k^3, m >= k; dense_factor.hpp:34-101),
+// [5] core product R_u R_v^T and basis products Q_u (U_s S), Q_v V_s (lowrank.hpp:78-83).
+__device__ __forceinline__ void count_trunc_work(unsigned* status, int p, int s, int k, int r) {
+    double* ctr = reinterpret_cast<double*>(status + 16);
+    auto qr = [](double m, double kk) {
+        const double a = fmax(m, kk), b = fmin(m, kk);
+        return 4.0 * a * b * b - 4.0 / 3.0 * b * b * b;
+    };
+    const double ku = fmin((double)p, (double)k), kv = fmin((double)s, (double)k);
+    atomicAdd(ctr, 8.0 * (double)(p + s) * (double)(k + r));
+    atomicAdd(ctr + 2, 1.0);
+    atomicAdd(ctr + 4, qr(p, k) + qr(s, k));
+    atomicAdd(ctr + 5, 2.0 * ku * kv * k + 2.0 * ((double)p * ku + (double)s * kv) * r);
+}
+
 __device__ __forceinline__ void cpa8(double* dst, const double* src) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");

@@ -125,6 +125,28 @@ void DHodlr::zero(cudaStream_t st) const {
 }
 
 // ================================================================ small kernels
+__global__ void k_zero_lower_ranks(int* rank, int nnodes) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nnodes) rank[2 * i + 1] = 0;
+}
+void launch_zero_lower_ranks(int* rank, int nnodes, cudaStream_t st) {
+    k_zero_lower_ranks<<<(nnodes + 127) / 128, 128, 0, st>>>(rank, nnodes);
+    SPG_LAUNCH_CHECK();
+}
+
+// per-phase work counters (spg_info::ph_*): a phase's begin marker snapshots the device
+// counter block, its end marker adds the difference to the phase's row of acc
+__global__ void k_phase_mark(const double* counters, double* snap, double* acc, int phase, int end) {
+    const int i = threadIdx.x;
+    if (i >= 8) return;
+    if (!end) snap[phase * 8 + i] = counters[i];
+    else acc[phase * 8 + i] += counters[i] - snap[phase * 8 + i];
+}
+void launch_phase_mark(const double* counters, double* snap, double* acc, int phase, int end, cudaStream_t st) {
+    k_phase_mark<<<1, 32, 0, st>>>(counters, snap, acc, phase, end);
+    SPG_LAUNCH_CHECK();
+}
+
 struct RankOp { int* out; const int* a; const int* b; };
 __global__ void k_rank_op(const RankOp* ops, int nops) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -554,7 +576,7 @@ void Engine::apply(Plan& p, const std::vector<ApplyReq>& reqs) {
 }
 
 // ---------------------------------------------------------------- cascade
-void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs) {
+void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs, bool upper_only) {
     std::vector<TTask> tasks;
     std::vector<LowRankUpd> upd;
     int maxm = 0;
@@ -570,6 +592,7 @@ void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs) {
             up.g[1] = TGroup{c.QU + bl, c.QV + br, tree_.n, tree_.n, c.qrank, 0, c.s, nullptr};
             up.ou = H.upU(y); up.ov = H.upV(y); up.ldou = up.ldov = tree_.n; up.orank = H.rup(y); up.skipg = 1; up.tag = cur_op_ * 100000 + 50000 + y;
             tasks.push_back(up);
+            if (upper_only) continue;
             TTask lo{};
             lo.p = tree_.size[r]; lo.s = tree_.size[l]; lo.ng = 2;
             lo.g[0] = TGroup{H.loU(y), H.loV(y), tree_.n, tree_.n, H.rlo(y), 0, 1.0, nullptr};
@@ -855,7 +878,12 @@ void Engine::op_leaf_dinv(Plan& p, DHodlr& W) {
 // hodlr_multiply (hodlr.hpp:409-451), level-batched in the reference's order:
 // (1) leaf products, (2) all own-term panels, (3) own-term truncations,
 // (4) ancestor products trunc(lr_multiply), (5) cascades nearest ancestor first.
-void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
+// upper_only: C is consumed only by hodlr_cholesky, which reads C's upper blocks and
+// leaves and never C.lower (hodlr.hpp:540-574): the lower own-term
+// panels and truncations and the lower halves of the ancestor cascades are skipped and
+// C.lower is left at rank 0.  Every upper block receives exactly the operands and
+// truncation order of the full product, so the upper blocks and leaves are unchanged.
+void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C, bool upper_only) {
     cur_op_ = 3;
     const int n = tree_.n, D = std::max(tree_.depth, 1);
     // (1) leaves
@@ -890,6 +918,7 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
             const int l = tree_.left[x], r = tree_.right[x];
             rq.push_back(ApplyReq{&A, l, 0, B.slabU(t), B.rup(x), T1 + t * slab});   // A11 b12.U
             rq.push_back(ApplyReq{&B, r, 1, A.slabV(t), A.rup(x), T2 + t * slab});   // B22^T a12.V
+            if (upper_only) continue;
             rq.push_back(ApplyReq{&B, l, 1, A.slabV(t), A.rlo(x), U1 + t * slab});   // B11^T a21.V
             rq.push_back(ApplyReq{&A, r, 0, B.slabU(t), B.rlo(x), U2 + t * slab});   // A22 b21.U
         }
@@ -909,6 +938,7 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
             up.g[1] = TGroup{A.upU(x), T2 + t * slab + br, n, n, A.rup(x), 0, 1.0, nullptr};
             up.ou = C.upU(x); up.ov = C.upV(x); up.ldou = up.ldov = n; up.orank = C.rup(x); up.tag = 300000 + x;
             tasks.push_back(up);
+            if (upper_only) continue;
             TTask lo{};
             lo.p = s2; lo.s = s1; lo.ng = 2; lo.skipg = -1;
             lo.g[0] = TGroup{A.loU(x), U1 + t * slab + bl, n, n, A.rlo(x), 0, 1.0, nullptr};
@@ -917,6 +947,11 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
             tasks.push_back(lo);
         }
         trunc(p, tasks);
+        if (upper_only) {
+            int* rk = C.rank;
+            const int nn = tree_.nnodes();
+            push(p, [rk, nn](cudaStream_t st) { launch_zero_lower_ranks(rk, nn, st); });
+        }
     }
     // (4) ancestor products: Q_l = trunc(a12 b21) on rows l, Q_r = trunc(a21 b12) on rows r
     {
@@ -966,7 +1001,7 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C) {
             cs.push_back(Cascade{tree_.left[x], QU + t * slab, QV + t * slab, qr + 2 * x, 1.0});
             cs.push_back(Cascade{tree_.right[x], QU + t * slab, QV + t * slab, qr + 2 * x + 1, 1.0});
         }
-        cascade(p, C, cs);
+        cascade(p, C, cs, upper_only);
     }
     ws_->release(mark);
 }
@@ -1218,7 +1253,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
             record(p, x);
             cascade_chol(p, M, x, r, P1, W.slabV(t), W.rup(x));
         } else {
-            cascade(p, M, {Cascade{r, P1, W.slabV(t), W.rup(x), 1.0}});
+            cascade(p, M, {Cascade{r, P1, W.slabV(t), W.rup(x), 1.0}}, /*upper_only=*/true);   // M.lower is never read
         }
     }
     chol_rec(p, r, M, W);

@@ -140,10 +140,14 @@ struct Scalars {          // device scalar block
     int* counter;
     unsigned* status;     // status word + overflow diagnostics (16 ints)
     double* counters;     // [0] recompression bytes 8(p+s)(k_in+k_out) [1] GEMM flops 2MNK [2] truncation tasks
+                          // [3] core statistics [4] truncation QR flops [5] core + basis flops (8 doubles)
 };
 
 // kernel classes timed with CUDA events in profile mode
 enum ProfClass { PC_TRUNC = 0, PC_GEMM, PC_HSOLVE, PC_LEAF, PC_NCLS };
+
+void launch_zero_lower_ranks(int* rank, int nnodes, cudaStream_t st);
+void launch_phase_mark(const double* counters, double* snap, double* acc, int phase, int end, cudaStream_t st);
 
 class Engine {
 public:
@@ -167,7 +171,7 @@ public:
     void apply(Plan& p, const std::vector<ApplyReq>& reqs);
     // add_lowrank_into (hodlr.hpp:400-405) of s * QU QV^T into the subtrees (batched, disjoint)
     struct Cascade { int root; const double* QU; const double* QV; const int* qrank; double s; };
-    void cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs);
+    void cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs, bool upper_only = false);
     void hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items);
     // the same solves, subtree-parallel: all leaves at once, then one batched low-rank
     // correction per tree level with the solved coupling bases (needs op_solve_prep(W))
@@ -185,7 +189,7 @@ public:
     void op_leaf_dinv(Plan& p, DHodlr& W);
     // solved coupling bases tU / tV of a finished upper-triangular factor (bottom-up)
     void op_solve_prep(Plan& p, DHodlr& W);
-    void op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C);
+    void op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C, bool upper_only = false);
     // defer_trunc: W12 = trunc(W11^{-T} M12) is taken off the critical path (own stream)
     // and the Schur complement uses the untruncated pair (differs at the eps level)
     void op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool defer_trunc = false);

@@ -302,20 +302,46 @@ struct HqdwhState {
     std::unique_ptr<Engine> eng;
     std::unique_ptr<DHodlr> X, Z, W, Y, V, WK, P;
     double *d_bands = nullptr, *d_tmp = nullptr, *d_rdiag = nullptr, *d_diag = nullptr;
+    double* d_phase = nullptr;   // per-phase counter snapshots [64] and sums [64] (launch_phase_mark)
     int* d_piv = nullptr;
     cudaGraphExec_t g_first = nullptr, g_iter = nullptr;
+    cudaGraph_t gr_first = nullptr, gr_iter = nullptr;   // kept for the event-node updates below
     long long l_first = 0, l_iter = 0, nodes_iter = 0;
+    // phase timing inside the graphs: external event-record nodes (placeholder events
+    // ph_ev[2 * phase + {0, 1}] at capture), re-pointed before every replay to that run's
+    // row of the caller's event table (cudaGraphExecEventRecordNodeSetEvent), so the
+    // per-phase device times of graph replays come without any host synchronisation
+    cudaEvent_t ph_ev[2 * 8] = {};
+    struct EvNode { cudaGraphNode_t node; int phase, end; };
+    std::vector<EvNode> ev_first, ev_iter;
+    // timing events of a call, owned by the state (destroyed with it on every path, reused
+    // by later calls of a cached state instead of ~900 cudaEventCreate per call)
+    std::vector<cudaEvent_t> evpool;
+    size_t evnext = 0;
+    cudaEvent_t take_event() {
+        if (evnext == evpool.size()) {
+            cudaEvent_t e;
+            SPG_CUDA(cudaEventCreate(&e));
+            evpool.push_back(e);
+        }
+        return evpool[evnext++];
+    }
     size_t arena_mark = 0;
     long long leaf_entries = 0;
     ~HqdwhState() {
         if (g_first) cudaGraphExecDestroy(g_first);
         if (g_iter) cudaGraphExecDestroy(g_iter);
-        cudaFree(d_bands); cudaFree(d_tmp); cudaFree(d_rdiag); cudaFree(d_diag); cudaFree(d_piv);
+        if (gr_first) cudaGraphDestroy(gr_first);
+        if (gr_iter) cudaGraphDestroy(gr_iter);
+        for (auto e : ph_ev) if (e) cudaEventDestroy(e);
+        for (auto e : evpool) cudaEventDestroy(e);
+        cudaFree(d_bands); cudaFree(d_tmp); cudaFree(d_rdiag); cudaFree(d_diag); cudaFree(d_piv); cudaFree(d_phase);
         X.reset(); Z.reset(); W.reset(); Y.reset(); V.reset(); WK.reset(); P.reset();
         eng.reset();
     }
-    bool matches(int n_, int b_, int nm_, double e_, double d_) const {
-        return n == n_ && b == b_ && n_min == nm_ && eps == e_ && delta == d_;
+    int device = 0;   // the CUDA device the engine's stream, graphs and buffers belong to
+    bool matches(int n_, int b_, int nm_, double e_, double d_, int dev) const {
+        return n == n_ && b == b_ && n_min == nm_ && eps == e_ && delta == d_ && device == dev;
     }
 };
 
@@ -325,15 +351,38 @@ std::vector<std::unique_ptr<HqdwhState>> g_state_cache;
 constexpr size_t kStateCache = 2;
 const bool g_no_state_cache = std::getenv("SPG_NO_PLAN_CACHE") != nullptr;
 
+int current_device() {
+    int dev = 0;
+    SPG_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
+
 std::unique_ptr<HqdwhState> take_cached_state(int n, int b, int n_min, double eps, double delta) {
+    const int dev = current_device();
     std::lock_guard<std::mutex> lk(g_state_mu);
     for (size_t i = 0; i < g_state_cache.size(); ++i)
-        if (g_state_cache[i]->matches(n, b, n_min, eps, delta)) {
+        if (g_state_cache[i]->matches(n, b, n_min, eps, delta, dev)) {
             auto s = std::move(g_state_cache[i]);
             g_state_cache.erase(g_state_cache.begin() + i);
             return s;
         }
     return nullptr;
+}
+// drops every cached plan (all devices); returns how many were freed
+int drop_cached_states() {
+    std::vector<std::unique_ptr<HqdwhState>> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_state_mu);
+        drop.swap(g_state_cache);
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& s : drop) {   // free each state on its own device
+        cudaSetDevice(s->device);
+        s.reset();
+    }
+    cudaSetDevice(cur);
+    return (int)drop.size();
 }
 }  // namespace
 
@@ -399,7 +448,7 @@ void build_iter(Plan& p, HqdwhState& st, const TimedFn& timed) {
     Scalars S = E.sc();
     timed(p, PH_MUL, [&]() {
         p.launches.push_back([=](cudaStream_t s) { launch_iter_params(S.sched, S.counter, S.slots, S.scal, s); });
-        E.op_multiply(p, *st.X, *st.X, *st.Z);
+        E.op_multiply(p, *st.X, *st.X, *st.Z, /*upper_only=*/true);   // Z.lower is dead
         E.op_scale_shift(p, *st.Z, 1.0, S.slots + 0, 1.0);
     });
     // deferred W12 truncation (SPG_CHOL_REFERENCE_ORDER=1: the reference's order)
@@ -417,11 +466,11 @@ void build_iter(Plan& p, HqdwhState& st, const TimedFn& timed) {
     push_diag(p, st);
 }
 
-cudaGraphExec_t capture(HqdwhState& st, Plan& p, long long& launches, long long* nodes) {
+cudaGraphExec_t capture(HqdwhState& st, Plan& p, long long& launches, long long* nodes, cudaGraph_t& g,
+                        std::vector<HqdwhState::EvNode>& evn) {
     Engine& E = *st.eng;
     cudaStream_t s = E.stream();
     E.arena().commit(s);
-    cudaGraph_t g;
     const long long l0 = g_launches.load();
     SPG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     p.run(s);
@@ -430,18 +479,27 @@ cudaGraphExec_t capture(HqdwhState& st, Plan& p, long long& launches, long long*
     SPG_CUDA(cudaGraphInstantiate(&ge, g, 0));
     launches = g_launches.load() - l0;
     g_launches -= launches;   // counted again at every replay
-    if (nodes) {
-        size_t nn = 0;
-        SPG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
-        *nodes = (long long)nn;
+    size_t nn = 0;
+    SPG_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+    if (nodes) *nodes = (long long)nn;
+    std::vector<cudaGraphNode_t> all(nn);
+    SPG_CUDA(cudaGraphGetNodes(g, all.data(), &nn));
+    for (cudaGraphNode_t nd : all) {   // the phase markers (external event-record nodes)
+        cudaGraphNodeType ty;
+        SPG_CUDA(cudaGraphNodeGetType(nd, &ty));
+        if (ty != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t e;
+        SPG_CUDA(cudaGraphEventRecordNodeGetEvent(nd, &e));
+        for (int i = 0; i < 16; ++i)
+            if (st.ph_ev[i] == e) evn.push_back({nd, i / 2, i % 2});
     }
-    SPG_CUDA(cudaGraphDestroy(g));
     return ge;
 }
 
-std::unique_ptr<HqdwhState> make_state(int n, int b, int n_min, double eps, double delta, bool profile) {
+std::unique_ptr<HqdwhState> make_state_once(int n, int b, int n_min, double eps, double delta, bool profile) {
     auto st = std::make_unique<HqdwhState>();
     st->n = n; st->b = b; st->n_min = n_min; st->eps = eps; st->delta = delta;
+    st->device = current_device();
     st->eng = std::make_unique<Engine>(n, n_min, eps);
     Engine& E = *st->eng;
     E.set_profile(profile);
@@ -455,21 +513,48 @@ std::unique_ptr<HqdwhState> make_state(int n, int b, int n_min, double eps, doub
     SPG_CUDA(cudaMalloc(&st->d_rdiag, sizeof(double) * (size_t)(2 * b + 1) * n));
     SPG_CUDA(cudaMalloc(&st->d_diag, sizeof(double) * 2 * 64));
     SPG_CUDA(cudaMalloc(&st->d_piv, sizeof(int) * n));
+    SPG_CUDA(cudaMalloc(&st->d_phase, sizeof(double) * 128));
     for (int f : E.tree().leaves) st->leaf_entries += (long long)E.tree().size[f] * E.tree().size[f];
     return st;
 }
 
+// allocation failures first evict the cached plans (they may hold GBs each) and retry once
+std::unique_ptr<HqdwhState> make_state(int n, int b, int n_min, double eps, double delta, bool profile) {
+    try {
+        return make_state_once(n, b, n_min, eps, delta, profile);
+    } catch (const CudaError&) {
+        cudaGetLastError();
+        if (drop_cached_states() == 0) throw;
+        return make_state_once(n, b, n_min, eps, delta, profile);
+    }
+}
+
 void build_graphs(HqdwhState& st) {
-    const TimedFn untimed = [](Plan&, int, const std::function<void()>& body) { body(); };
+    for (auto& e : st.ph_ev)
+        if (!e) SPG_CUDA(cudaEventCreate(&e));
+    cudaEvent_t* ph = st.ph_ev;
+    const double* ctr = st.eng->sc().counters;
+    double* dph = st.d_phase;
+    const TimedFn marked = [ph, ctr, dph](Plan& p, int phase, const std::function<void()>& body) {
+        p.launches.push_back([ph, phase, ctr, dph](cudaStream_t s) {
+            SPG_CUDA(cudaEventRecordWithFlags(ph[2 * phase], s, cudaEventRecordExternal));
+            launch_phase_mark(ctr, dph, dph + 64, phase, 0, s);
+        });
+        body();
+        p.launches.push_back([ph, phase, ctr, dph](cudaStream_t s) {
+            launch_phase_mark(ctr, dph, dph + 64, phase, 1, s);
+            SPG_CUDA(cudaEventRecordWithFlags(ph[2 * phase + 1], s, cudaEventRecordExternal));
+        });
+    };
     {
         Plan p;
-        build_first(p, st, untimed);
-        st.g_first = capture(st, p, st.l_first, nullptr);
+        build_first(p, st, marked);
+        st.g_first = capture(st, p, st.l_first, nullptr, st.gr_first, st.ev_first);
     }
     {
         Plan p;
-        build_iter(p, st, untimed);
-        st.g_iter = capture(st, p, st.l_iter, &st.nodes_iter);
+        build_iter(p, st, marked);
+        st.g_iter = capture(st, p, st.l_iter, &st.nodes_iter, st.gr_iter, st.ev_iter);
     }
     st.arena_mark = st.eng->arena().mark();
     st.graphs = true;
@@ -500,8 +585,8 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     const double h_alloc = hms();
 
     // ---- timing instrumentation: per-run event tables, no host sync inside the loop
-    std::vector<cudaEvent_t> evs;
-    auto mkev = [&]() { cudaEvent_t e; SPG_CUDA(cudaEventCreate(&e)); evs.push_back(e); return e; };
+    stt.evnext = 0;
+    auto mkev = [&]() { return stt.take_event(); };
     const int nruns = 64;                     // one row per projector phase-run (k <= 60)
     const int nmarks = PH_NPH;
     std::vector<cudaEvent_t> evtab((size_t)nruns * nmarks * 2);
@@ -509,6 +594,8 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     std::vector<int> used((size_t)nruns * nmarks, 0);
     int cur_run = 0;
     int* cur_run_p = &cur_run;
+    const double* ctr_dev = S.counters;
+    double* dph = stt.d_phase;
     const TimedFn timed = [&](Plan& p, int phase, const std::function<void()>& body) {
         cudaEvent_t* tab = evtab.data();
         int* up = used.data();
@@ -516,12 +603,21 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
             const int r = *cur_run_p;
             up[r * nmarks + phase] = 1;
             SPG_CUDA(cudaEventRecord(tab[(r * nmarks + phase) * 2], s));
+            launch_phase_mark(ctr_dev, dph, dph + 64, phase, 0, s);
         });
         body();
         p.launches.push_back([=](cudaStream_t s) {
             const int r = *cur_run_p;
+            launch_phase_mark(ctr_dev, dph, dph + 64, phase, 1, s);
             SPG_CUDA(cudaEventRecord(tab[(r * nmarks + phase) * 2 + 1], s));
         });
+    };
+    // graph replay r: its phase markers record into row r of the event table
+    auto point_events = [&](cudaGraphExec_t ge, const std::vector<HqdwhState::EvNode>& evn, int r) {
+        for (const auto& en : evn) {
+            used[r * nmarks + en.phase] = 1;
+            SPG_CUDA(cudaGraphExecEventRecordNodeSetEvent(ge, en.node, evtab[(r * nmarks + en.phase) * 2 + en.end]));
+        }
     };
     auto commit_run = [&](Plan& p) {
         E.arena().commit(st);
@@ -540,7 +636,8 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
             p.launches.push_back([=](cudaStream_t s) {
                 SPG_CUDA(cudaMemsetAsync(S.status, 0, 14 * sizeof(unsigned), s));
                 SPG_CUDA(cudaMemsetAsync(S.counter, 0, sizeof(int), s));
-                SPG_CUDA(cudaMemsetAsync(S.counters, 0, 4 * sizeof(double), s));
+                SPG_CUDA(cudaMemsetAsync(S.counters, 0, 8 * sizeof(double), s));
+                SPG_CUDA(cudaMemsetAsync(dph, 0, 128 * sizeof(double), s));
                 SPG_CUDA(cudaMemcpyAsync(d_bands, bands_host, sizeof(double) * blen, cudaMemcpyHostToDevice, s));
                 launch_estimate_2norm(n, b, d_bands, d_tmp, s);            // d_tmp[0] = alpha
                 SPG_CUDA(cudaMemcpyAsync(S.scal, d_tmp, sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -594,6 +691,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         it_ev.push_back(e0);
         SPG_CUDA(cudaEventRecord(e0, st));
         if (stt.graphs) {
+            point_events(stt.g_first, stt.ev_first, 0);
             SPG_CUDA(cudaGraphLaunch(stt.g_first, st));
             g_launches += stt.l_first;
         } else if (use_graph) {
@@ -634,6 +732,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
             it_ev.push_back(e0);
             SPG_CUDA(cudaEventRecord(e0, st));
             if (stt.graphs) {
+                point_events(stt.g_iter, stt.ev_iter, k);
                 SPG_CUDA(cudaGraphLaunch(stt.g_iter, st));
                 g_launches += stt.l_iter;
             } else {
@@ -709,13 +808,25 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     }
     I.launches = g_launches.load() - launches0;
     {
-        double ctr[4];
+        double ctr[8];
         SPG_CUDA(cudaMemcpy(ctr, S.counters, sizeof(ctr), cudaMemcpyDeviceToHost));
         if (std::getenv("SPG_CORE_STATS"))
             std::fprintf(stderr, "core tasks %.0f, with k_in > 64: %.0f\n", ctr[2], ctr[3]);
         I.trunc_bytes = ctr[0];
         I.gemm_flops = ctr[1];
         I.trunc_tasks = (long long)ctr[2];
+        double phc[128];
+        SPG_CUDA(cudaMemcpy(phc, stt.d_phase, sizeof(phc), cudaMemcpyDeviceToHost));
+        double leaf3 = 0.0;
+        for (int f : E.tree().leaves) leaf3 += std::pow((double)E.tree().size[f], 3) / 3.0;
+        for (int ph = 0; ph < PH_NPH && ph < 8; ++ph) {
+            const double* a = phc + 64 + 8 * ph;
+            I.ph_trunc_bytes[ph] = a[0];
+            I.ph_gemm_flops[ph] = a[1];
+            I.ph_qr_flops[ph] = a[4];
+            I.ph_core_flops[ph] = a[5];
+        }
+        I.ph_leaf_flops[PH_CHOL] = std::max(count - 1, 0) * leaf3;
         if (E.profile()) {
             double pm[PC_NCLS];
             long long pb[PC_NCLS];
@@ -749,7 +860,6 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         SPG_CUDA(cudaStreamSynchronize(st));
         I.trace = hp[8];
     }
-    for (auto e : evs) cudaEventDestroy(e);
     R->state = std::move(state);
     return R.release();
 }
@@ -800,6 +910,37 @@ int spg_measure_dmma_tflops(double* out) {
     });
 }
 int spg_kcap(void) { return KCAP; }
+
+int spg_release_plan_cache(void) { return drop_cached_states(); }
+
+int spg_stacked_qr_r(int n, int b, const double* bands, int method, double* rdiag) {
+    return guarded([&]() {
+        ensure_device();
+        if (n < 2 || b < 1 || b >= n) throw StatusError(SPG_INVALID_ARGUMENT, "spg_stacked_qr_r: n >= 2, 1 <= b < n");
+        if (method == 0 && b > 16) throw StatusError(SPG_INVALID_ARGUMENT, "spg_stacked_qr_r: band Cholesky needs b <= 16");
+        double *db, *dw, *dr, *ds;
+        unsigned* dst;
+        const long long blen = band_len(n, b);
+        SPG_CUDA(cudaMalloc(&db, sizeof(double) * blen));
+        SPG_CUDA(cudaMalloc(&dw, sizeof(double) * (size_t)n * (4 * b + 4)));
+        SPG_CUDA(cudaMalloc(&dr, sizeof(double) * (size_t)n * (2 * b + 1)));
+        SPG_CUDA(cudaMalloc(&ds, sizeof(double) * 8));
+        SPG_CUDA(cudaMalloc(&dst, sizeof(unsigned) * 16));
+        // slots[0] = c0 selects the construction (launch_givens_reduce), slots[5] = scale 1
+        double slots[8] = {method == 1 ? 1e308 : 0.0, 0, 0, 0, 0, 1.0, 0, 0};
+        SPG_CUDA(cudaMemcpy(db, bands, sizeof(double) * blen, cudaMemcpyHostToDevice));
+        SPG_CUDA(cudaMemcpy(ds, slots, sizeof(slots), cudaMemcpyHostToDevice));
+        SPG_CUDA(cudaMemset(dst, 0, sizeof(unsigned) * 16));
+        SPG_CUDA(cudaMemset(dr, 0, sizeof(double) * (size_t)n * (2 * b + 1)));
+        launch_givens_reduce(n, b, db, ds, dw, dr, nullptr, dst);
+        SPG_CUDA(cudaDeviceSynchronize());
+        SPG_CUDA(cudaMemcpy(rdiag, dr, sizeof(double) * (size_t)n * (2 * b + 1), cudaMemcpyDeviceToHost));
+        unsigned stw = 0;
+        SPG_CUDA(cudaMemcpy(&stw, dst, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        cudaFree(db); cudaFree(dw); cudaFree(dr); cudaFree(ds); cudaFree(dst);
+        if (stw & ST_NPD) throw StatusError(SPG_NOT_POSITIVE_DEFINITE, "band Cholesky: non-positive pivot");
+    });
+}
 
 int spg_host_alloc(long long bytes, void** out) {
     *out = nullptr;
@@ -1038,9 +1179,11 @@ int spg_ctx_op(spg_ctx* c, int op, int dst, int a, int b, double alpha, double b
         DHodlr& D = *c->slots.at(dst);
         switch (op) {
             case 1: E.op_multiply(p, *c->slots.at(a), *c->slots.at(b), D); break;
+            case 8: E.op_multiply(p, *c->slots.at(a), *c->slots.at(b), D, /*upper_only=*/true); break;
             case 2: E.op_axpby(p, alpha, nullptr, *c->slots.at(a), beta, nullptr, *c->slots.at(b), D); break;
             case 3: E.op_symmetrize(p, D); break;
             case 4: E.op_cholesky(p, *c->slots.at(a), D, *c->work); break;
+            case 9: E.op_cholesky(p, *c->slots.at(a), D, *c->work, /*defer_trunc=*/true); break;
             case 5:
                 E.op_leaf_dinv(p, *c->slots.at(b));   // uploaded factors carry no block inverses yet
                 E.op_solve_upper_right(p, *c->slots.at(a), *c->slots.at(b), D, *c->work);

@@ -342,9 +342,7 @@ __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double*
         sR = r;
         hdr[0] = k; hdr[1] = r;
         if (rp > 0 && !(sSig[sOrd[0]] == sSig[sOrd[0]])) atomicOr(status, ST_NONFINITE);
-        double* ctr = reinterpret_cast<double*>(status + 16);   // algorithmic bytes 8 (p+s)(k_in+k_out)
-        atomicAdd(ctr, 8.0 * (double)(t.p + t.s) * (double)(k + r));
-        atomicAdd(ctr + 2, 1.0);
+        count_trunc_work(status, t.p, t.s, k, r);   // SURVEY.md §8d work units
     }
     __syncthreads();
     const int r = sR;
@@ -737,9 +735,7 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         hdr[0] = k; hdr[1] = r;
         core_hist(k, rp, nsweeps, r);
         if (rp > 0 && !(sSig[sOrd3[0]] == sSig[sOrd3[0]])) atomicOr(status, ST_NONFINITE);
-        double* ctr = reinterpret_cast<double*>(status + 16);
-        atomicAdd(ctr, 8.0 * (double)(t.p + t.s) * (double)(k + r));
-        atomicAdd(ctr + 2, 1.0);
+        count_trunc_work(status, t.p, t.s, k, r);   // SURVEY.md §8d work units
     }
     __syncthreads();
     const int r = sR3;

@@ -534,13 +534,39 @@ __device__ __forceinline__ void givens_cs_t(double f, double g, double& c, doubl
     s = g * ir;
 }
 
+// make_givens (givens.hpp:27-36) without the scaling: r = sign(f) sqrt(f^2 + g^2) from one
+// refined reciprocal square root (c = |f| / |r|, s = sign(f) g / |r|) -- one MUFU seed and
+// two Newton steps on the dependency chain instead of a reciprocal, a square root and a
+// second reciprocal.  Within an ulp or two of make_givens; outside [1e-290, 1e290] for
+// f^2 + g^2 (never met by the first-iterate sweep: its pivots stay >= 1) it falls back to
+// the scaled form.
+__device__ __forceinline__ void givens_fast(double f, double g, double& c, double& s, double& r) {
+    if (g == 0.0) { c = 1.0; s = 0.0; r = f; return; }
+    if (f == 0.0) { c = 0.0; s = 1.0; r = g; return; }
+    const double ss = fma(f, f, g * g);
+    if (!(ss > 1e-290 && ss < 1e290)) {
+        givens_cs_t(f, g, c, s);
+        r = c * f + s * g;
+        return;
+    }
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(ss));
+    y = fma(0.5 * y, fma(-ss * y, y, 1.0), y);
+    y = fma(0.5 * y, fma(-ss * y, y, 1.0), y);
+    const double sy = f < 0.0 ? -y : y;
+    c = fabs(f) * y;
+    s = g * sy;
+    r = ss * sy;
+}
+
 // reduce_tridiag: per row t the rotations alpha_{t,t} (rowN_t against aux_t = 1),
 // beta_t (R_tt against rowN_t, carrying R_{t,t+1} into rowN_{t+1}) and gamma_t
 // (row t against the original row t+1, filling R_{t,t+2}); row t of R is final
 // after gamma_t.  Same rotations and arithmetic as the band kernel (k_seq.cu).
 __global__ void __launch_bounds__(32) k_givens_tri(int n, const double* __restrict__ bands, const double* slots,
-                                                  double* __restrict__ rdiag) {
+                                                  double* __restrict__ rdiag, double c0_max) {
     __shared__ __align__(16) double sbuf[PST * PNA * PCH];
+    if (!(slots[0] > c0_max)) return;   // R from the band Cholesky instead (launch_givens_reduce)
     const int lane = threadIdx.x;
     const double sA = slots[5];
     const double* dg = bands;
@@ -548,35 +574,32 @@ __global__ void __launch_bounds__(32) k_givens_tri(int n, const double* __restri
     double* r0 = rdiag;
     double* r1 = rdiag + n;
     double* r2 = rdiag + 2 * (size_t)n;
-    double a0 = dg[0] * sA, a1 = of[0] * sA, a2 = 0.0;
+    double a0 = dg[0] * sA, a1 = of[0] * sA;
     double rn = 1.0;   // rowN_t
     Ring<3> R{{of, dg, of}, {0, 1, 1}, {n - 1, n, n - 1}, 0, false, sbuf};
     run_ring(R, n, lane, [&](long long t, const double* v) {
-        double c, s;
-        if (t > 0) {   // alpha_{t,t}
-            givens_cs_t(rn, 1.0, c, s);
-            rn = c * rn + s * 1.0;
+        double c, s, r;
+        if (t > 0) {   // alpha_{t,t}: rowN_t against aux_t = 1
+            givens_fast(rn, 1.0, c, s, r);
+            rn = r;
         }
-        double rn1 = 0.0;
-        givens_cs_t(a0, rn, c, s);   // beta_t
-        a0 = c * a0 + s * rn;
+        givens_fast(a0, rn, c, s, r);   // beta_t
+        a0 = r;
         if (t + 1 < n) {
             const double x = a1;
-            a1 = c * x + s * 0.0;
-            rn1 = -s * x + c * 0.0;
+            a1 = c * x;
+            const double rn1 = -s * x;   // carried into rowN_{t+1}
             const double b0 = v[0] * sA, b1 = v[1] * sA, b2 = v[2] * sA;   // original row t+1
-            givens_cs_t(a0, b0, c, s);                                     // gamma_{t,t+1}
-            const double n0 = c * a0 + s * b0;
+            givens_fast(a0, b0, c, s, r);                                  // gamma_{t,t+1}
             const double n1 = c * a1 + s * b1;
             const double q1 = -s * a1 + c * b1;
-            double n2 = 0.0, q2 = b2;
-            if (t + 2 < n) { n2 = c * a2 + s * b2; q2 = -s * a2 + c * b2; }
-            if (lane == 0) { r0[t] = n0; r1[t] = n1; r2[t] = n2; }
-            a0 = q1; a1 = q2; a2 = 0.0;
+            const double n2 = t + 2 < n ? s * b2 : 0.0, q2 = t + 2 < n ? c * b2 : b2;
+            if (lane == 0) { r0[t] = r; r1[t] = n1; r2[t] = n2; }
+            a0 = q1; a1 = q2;
+            rn = rn1;
         } else {
             if (lane == 0) { r0[t] = a0; r1[t] = 0.0; r2[t] = 0.0; }
         }
-        rn = rn1;
     });
 }
 
@@ -591,8 +614,8 @@ void launch_est_l0_tri(int n, const double* bands, const double* alpha, double* 
     }
 }
 
-void launch_givens_tri(int n, const double* bands, const double* slots, double* rdiag, cudaStream_t st) {
-    k_givens_tri<<<1, 32, 0, st>>>(n, bands, slots, rdiag);
+void launch_givens_tri(int n, const double* bands, const double* slots, double* rdiag, cudaStream_t st, double c0_max) {
+    k_givens_tri<<<1, 32, 0, st>>>(n, bands, slots, rdiag, c0_max);
     SPG_LAUNCH_CHECK();
 }
 

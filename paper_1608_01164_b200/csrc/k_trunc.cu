@@ -552,9 +552,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_core(const TTask* __restrict__ t
         hdr[0] = k; hdr[1] = r;
         if (!(sSig[sPerm[0]] == sSig[sPerm[0]])) atomicOr(status, ST_NONFINITE);
         // algorithmic recompression traffic 8 (p + s)(k_in + k_out)
-        double* ctr = reinterpret_cast<double*>(status + 16);
-        atomicAdd(ctr, 8.0 * (double)(t.p + t.s) * (double)(k + r));
-        atomicAdd(ctr + 2, 1.0);
+        count_trunc_work(status, t.p, t.s, k, r);   // SURVEY.md §8d work units
     }
     __syncthreads();
     const int r = sR_;

@@ -181,7 +181,8 @@ void launch_from_band(DevTree t, DevHodlrView H, int mode, int b, const double* 
 // b = 1 specialisations (k_tri.cu): work >= 9 n doubles
 void launch_est_l0_tri(int n, const double* bands, const double* alpha, double* work, double* out_l0,
                        unsigned* status, cudaStream_t st);
-void launch_givens_tri(int n, const double* bands, const double* slots, double* rdiag, cudaStream_t st);
+// c0_max: the kernel runs only when the first-iterate c0 (slots[0]) exceeds it (launch_givens_reduce)
+void launch_givens_tri(int n, const double* bands, const double* slots, double* rdiag, cudaStream_t st, double c0_max);
 // work: n*(3b+1) + 2n + n*max(b-1,1) doubles; slots[5] = sqrt(c0)/alpha
 void launch_givens_reduce(int n, int b, const double* bands, const double* slots, double* work, double* rdiag,
                           cudaStream_t st, unsigned* status);

@@ -138,6 +138,41 @@ def test_ops_vs_restatement(n, nmin):
     ctx.close()
 
 
+@pytest.mark.parametrize("n,nmin", [(300, 40), (1024, 64)])
+def test_multiply_upper_only_and_deferred_cholesky(n, nmin):
+    """The two production variants of the iteration: Z = X X with the dead
+    lower blocks skipped (op 8) gives bitwise the upper blocks and leaves of the full
+    product, and the same Cholesky factor; the deferred-W12 Cholesky (op 9) matches the
+    reference-order factor (hodlr.hpp:540-574) at the truncation level."""
+    eps = 1e-10
+    bands, Xn = _random_hodlr(n, nmin, n + 1)
+    ctx = S.HodlrContext(n, nmin, eps, 6)
+    ctx.from_banded(0, S.BandedSymmetric(n, 2, bands))
+    ctx.op("symmetrize", 0)
+    ctx.op("multiply", 1, 0, 0)
+    ctx.op("multiply_upper", 2, 0, 0)
+    Zf, Zu = ctx.download(1), ctx.download(2)
+    for i, (U, V) in Zf.upper.items():
+        assert np.array_equal(Zu.upper[i][0], U) and np.array_equal(Zu.upper[i][1], V)
+        assert Zu.lower[i][0].shape[1] == 0
+    for i, D in Zf.dense.items():
+        assert np.array_equal(Zu.dense[i], D)
+    for slot in (1, 2):
+        ctx.op("scale_shift", slot, alpha=20.0, beta=1.0)
+    ctx.op("cholesky", 3, 1)
+    ctx.op("cholesky", 4, 2)
+    W1, W2 = ctx.download(3).to_flat(), ctx.download(4).to_flat()
+    assert np.array_equal(W1[0], W2[0]) and np.array_equal(W1[1], W2[1])
+    ctx.op("cholesky_deferred", 5, 2)
+    Wd = ctx.download(5).to_dense()
+    Wr = ctx.download(3).to_dense()
+    Zd = ctx.download(1).to_dense()
+    assert np.all(np.tril(Wd, -1) == 0.0)
+    assert np.linalg.norm(Wd - Wr, 2) <= 10 * eps * np.linalg.norm(Wr, 2)
+    assert np.linalg.norm(Wd.T @ Wd - Zd, 2) <= 1e-8 * np.linalg.norm(Zd, 2)    # test_hodlr.cpp:235-245 bound
+    ctx.close()
+
+
 def assert_exact_mirror(Hm):
     # hodlr_symmetrize keeps lower = upper^T as exact factor mirrors (hodlr.hpp:357-361)
     for i, (U, V) in Hm.upper.items():
@@ -335,3 +370,128 @@ def test_banded_l0_chunked_vs_restatement(restate, n, b, seed):
     assert abs(r.l0 - l0) <= 1e-12 * l0
     assert round(r.P.trace()) == n // 2
     r.close()
+
+
+# ------------------------------------------------------------------ first iterate (fast_qr.hpp)
+@pytest.mark.parametrize("name", ["reduce_n64_b1", "reduce_n50_b3", "reduce_n33_b2"])
+def test_stacked_qr_r_vs_reference_kat(golden_dir, name):
+    """R of the stacked QR of [A; I] (reduce_tridiag / reduce_banded, fast_qr.hpp:83-232):
+    the device Givens sweep against the reference's R (kat.npz, written by the reference),
+    and the band Cholesky of A^2 + I against it up to row signs."""
+    g = load(golden_dir, "kat")
+    bands = g[name + "_bands"]
+    b = int(name.split("_b")[1])
+    n = int(name.split("_n")[1].split("_")[0])
+    A = S.BandedSymmetric.from_packed(n, b, bands)
+    Rref = g[name + "_R"].reshape(2 * b + 1, n)
+    Rg = S.stacked_qr_r(A, "givens")
+    scale = np.abs(Rref).max()
+    assert np.abs(Rg - Rref).max() <= 1e-13 * scale
+    Rc = S.stacked_qr_r(A, "cholesky")
+    sgn = np.sign(Rref[0])                          # row signs of the Givens R
+    Rs = np.zeros_like(Rref)
+    for d in range(2 * b + 1):
+        Rs[d, :n - d] = Rref[d, :n - d] * sgn[:n - d]
+    assert np.abs(Rc - Rs).max() <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("n,b", [(3000, 1), (2000, 5), (1500, 16)])
+def test_stacked_qr_r_vs_reference(reflib, n, b):
+    A = S.dimer_chain(n, 1.0, 0.9, 0.01, 31 + b, b=b, s=0.02 / (2 * b + 1) if b > 1 else 0.0).scaled(300.0)
+    rd = np.zeros((2 * b + 1) * n)
+    reflib.L.ref_reduce(n, b, R._d(A.packed()), R._d(rd))
+    Rref = rd.reshape(2 * b + 1, n)
+    assert np.abs(S.stacked_qr_r(A, "givens") - Rref).max() <= 1e-12 * np.abs(Rref).max()
+
+
+# (n, b, t2, n_min): c0 > 1e6 (Givens sweep: b = 1 and b = 3) and c0 < 1e6 (band Cholesky)
+FIRST_CASES = [(4096, 1, 0.999, 256), (2048, 1, 0.8, 128), (2048, 3, 0.9999, 128), (2048, 8, 0.8, 128),
+               (2048, 16, 0.95, 128)]
+
+
+@pytest.mark.parametrize("n,b,t2,nmin", FIRST_CASES)
+def test_first_iterate_vs_reference(reflib, n, b, t2, nmin):
+    """The first (QR-based) iterate against the reference's: hqdwh stopped after k = 0 (delta
+    between |1 - l0| and |1 - l1|, qdwh.hpp:209) gives U = X1 on both sides; the product
+    Q1 Q2^T (q1q2t, fast_qr.hpp:509-514) is recovered from X1 and compared with
+    ref_first_iterate_m, which runs fast_stacked_qr + q1q2t on the same scaled input."""
+    eps = 1e-10
+    s = 0.02 / (2 * b + 1) if b > 1 else 0.0
+    A = S.dimer_chain(n, 1.0, t2, 0.2 * (1 - t2) if b == 1 else 0.0, 70 + b, b=b, s=s)
+    r0 = S.hqdwh(A, nmin, eps)
+    l0, l1 = r0.l0, r0.per_iteration[0].l
+    delta = 0.5 * (abs(1 - min(l0, 1 - 1e-12)) + abs(1 - l1))
+    r = S.hqdwh(A, nmin, eps, delta)
+    assert r.iterations == 1
+    ref = reflib.hqdwh(A.bands, nmin, eps, delta)
+    assert ref["iterations"] == 1
+    Ug = r.U.to_dense()
+    Ur = reflib.to_dense(ref["U"], n)
+    assert np.linalg.norm(Ug - Ur, 2) <= 100 * eps
+    c0 = r.per_iteration[0].c
+    a0, b0, _ = S.qdwh_params(min(l0, 1 - 1e-12))
+    X0 = A.to_dense() / r.alpha
+    Mg = (Ug - (b0 / c0) * X0) * np.sqrt(c0) / (a0 - b0 / c0)
+    hm = reflib.L.ref_first_iterate_m(n, b, R._d(A.scaled(np.sqrt(c0) / r.alpha).packed()), nmin, eps)
+    Mr = reflib.to_dense(hm, n)
+    reflib.L.ref_hodlr_free(hm)
+    reflib.L.ref_result_free(ref["handle"])
+    assert np.linalg.norm(Mg - Mr, 2) <= 100 * eps, (c0, np.linalg.norm(Mg - Mr, 2))
+
+
+# ------------------------------------------------------------------ BASELINE sizes (north_star gate)
+HALKO = 10.0 * np.sqrt(2.0 / np.pi)
+
+
+@pytest.mark.parametrize("cfg", ["sweep0.999", "banded", "stress0.9999"])
+def test_baseline_config_vs_reference_probes(golden_dir, cfg):
+    """BASELINE config 4 (headline, n = 65536, t2 = 0.999), config 3 (banded b = 8, n = 32768)
+    and the c0 > 1e8 stress case against the reference's P applied to 16 Gaussian probes
+    (tests/golden/probe_<cfg>.npz, written by oracle/run_ref.py from oracle/_ref; bitwise
+    the same on this container and on the GPU box host).  ||P - P_ref||_2 is bounded by
+    10 sqrt(2/pi) max_i ||(P - P_ref) w_i|| with probability >= 1 - 1e-16 (Halko, Martinsson
+    & Tropp 2011, Lemma 4.1); the gate is north_star's 100 * eps.  Power-iteration norms of
+    the same comparison at every BASELINE config: profiles/parity_r02.json."""
+    from paper_1608_01164_b200.configs import CONFIGS, make_input
+    c = CONFIGS[cfg]
+    g = load(golden_dir, "probe_" + cfg)
+    n, eps = c["n"], c["eps"]
+    r = S.hqdwh(make_input(c), c["nmin"], eps)
+    assert r.iterations == int(g["iterations"])
+    tr = r.info["trace"]
+    assert round(tr) == n // 2 and abs(tr - float(g["trace"])) < 1e-8
+    Om = np.random.default_rng(int(g["seed"])).standard_normal((n, g["PrefOm"].shape[1]))
+    E = r.apply(Om) - g["PrefOm"]
+    assert HALKO * np.linalg.norm(E, axis=0).max() <= 100 * eps
+    idem = power_norm(lambda x: r.apply(r.apply(x)) - r.apply(x), n, iters=30)
+    assert idem <= 100 * eps
+    r.close()
+
+
+@pytest.mark.parametrize("cfg", ["pr1", "smallgap"])
+def test_baseline_config_vs_reference_dense(reflib, cfg):
+    """Configs 1 and 2 (n <= 16384): dense ||P - P_ref||_2 and ||P^2 - P||_2 (north_star:
+    checked densely for n <= 16384), the reference run here through oracle/_ref."""
+    from paper_1608_01164_b200.configs import CONFIGS, make_input
+    c = CONFIGS[cfg]
+    n, eps = c["n"], c["eps"]
+    A = make_input(c)
+    r = S.hqdwh(A, c["nmin"], eps)
+    ref = reflib.hqdwh(A.bands, c["nmin"], eps)
+    assert r.iterations == ref["iterations"]
+    Pg = r.P.to_dense()
+    Pr = reflib.to_dense(ref["P"], n)
+    reflib.L.ref_result_free(ref["handle"])
+    r.close()
+    from scipy.sparse.linalg import LinearOperator, eigsh
+    D = Pg - Pr
+    del Pr
+    assert np.abs(Pg - Pg.T).max() < 1e-12
+    # 2-norms of the dense symmetric differences by Lanczos (largest |eigenvalue|)
+    nd = abs(eigsh(D, k=1, which="LM", tol=1e-4, return_eigenvectors=False)[0])
+    del D
+    idem = LinearOperator((n, n), matvec=lambda x: Pg @ (Pg @ x) - Pg @ x, dtype=np.float64)
+    ni = abs(eigsh(idem, k=1, which="LM", tol=1e-4, return_eigenvectors=False)[0])
+    assert nd <= 100 * eps, nd
+    assert ni <= 100 * eps, ni
+    assert round(np.trace(Pg)) == n // 2
