@@ -128,17 +128,12 @@ int spg_make_dimer_chain(int n, int b, double t1, double t2, double eps_dis, dou
                          double* bands);
 /* generic random banded input (test_hodlr.cpp:19-26 convention) */
 int spg_make_random_banded(int n, int b, unsigned long long seed, double* bands);
-/* FP64 tensor-pipe (DMMA) throughput probe on device 0, TFLOP/s (roofline denominator) */
 /* Page-locked host memory for result export (cudaHostAlloc / cudaFreeHost):
  * exporting into it runs the D2H copy at full PCIe/NVLink-C2C speed. */
 int spg_host_alloc(long long bytes, void** out);
 void spg_host_free(void* p);
 
-/* Diagnostics: time one kernel of the critical path on a synthetic input (which 0 =
- * leaf Cholesky of an n x n SPD leaf).  out[0] = us per launch; out[1..6] = mean
- * cycles per 32-column panel phase (panel update, P, diagonal factor, panel solve,
- * write-back, panel gap); out[7] = status word. */
-int spg_micro_kernel(int which, int n, int reps, double* out, int nout);
+/* FP64 tensor-pipe (DMMA) throughput probe on the current device, TFLOP/s (roofline denominator) */
 int spg_measure_dmma_tflops(double* out);
 /* compiled capacities */
 int spg_kcap(void);

@@ -1,8 +1,7 @@
 // Wire formats and reporting of the specproj tools, over the C++ shim
 // (specproj.hpp): SBM text matrices (banded.hpp:115-154), the JSON run report
 // (tools/specproj.cpp:82-118), the dense-oracle error metrics used by `verify`
-// (qdwh.hpp:260-302, dense.hpp:228-278) and the two-sided-spectrum test matrices
-// of `generate` / `bench` (synth.hpp).  Header-only, host side; every projector
+// (qdwh.hpp:260-302, dense.hpp:228-278).  Header-only, host side; every projector
 // in here runs on the B200 through specproj::b200::hqdwh.
 #pragma once
 
@@ -247,89 +246,6 @@ inline ErrorMetrics error_metrics(const Matrix& U, const Matrix& Pi, int nu) {
         for (int i = 0; i < n; ++i) y[i] = 0.5 * (x[i] - t[i]) - t2[i];
     });
     return m;
-}
-
-// ------------------------------------------------------------------ synthetic matrices (generate / bench)
-// eigenvalues uniformly spaced in [-1, -gap] u [gap, 1], floor(n/2) negative (synth.hpp:20-40)
-inline std::vector<double> two_sided_spectrum(int n, double gap) {
-    if (n < 2) throw std::invalid_argument("SpectrumSpec: n >= 2 required");
-    if (!(gap > 0.0) || gap > 1.0) throw std::invalid_argument("SpectrumSpec: 0 < gap <= 1 required");
-    const int nn = n / 2, np = n - nn;
-    std::vector<double> ev;
-    for (int i = 0; i < nn; ++i) ev.push_back(nn == 1 ? -1.0 : -1.0 + (1.0 - gap) * i / (nn - 1));
-    for (int i = 0; i < np; ++i) ev.push_back(np == 1 ? 1.0 : gap + (1.0 - gap) * i / (np - 1));
-    return ev;
-}
-
-// Givens pair (c, s) with c f + s g = r, -s f + c g = 0, r carrying the sign of f (givens.hpp:27-36)
-inline void givens_pair(double f, double g, double& c, double& s) {
-    if (g == 0.0) { c = 1.0; s = 0.0; return; }
-    if (f == 0.0) { c = 0.0; s = 1.0; return; }
-    const double sc = std::abs(f) + std::abs(g);
-    const double fs = f / sc, gs = g / sc;
-    double r = sc * std::sqrt(fs * fs + gs * gs);
-    if (f < 0.0) r = -r;
-    c = f / r;
-    s = g / r;
-}
-
-// Banded symmetric matrix with the given spectrum (synth.hpp:100-137): diag(lambda) (sorted,
-// optionally shuffled by the seed) under a similarity by adjacent rotations, each rotation's
-// out-of-band fill chased to the corner by further rotations -- all in band storage.
-inline BandedSymmetric synth_banded(std::vector<double> lam, int b, std::uint64_t seed = 0) {
-    const int n = (int)lam.size();
-    if (n < 2) throw std::invalid_argument("synth_banded: n >= 2 required");
-    if (b < 1 || b >= n) throw std::invalid_argument("synth_banded: 1 <= b < n required");
-    for (double v : lam)
-        if (v == 0.0) throw std::invalid_argument("synth_banded: zero eigenvalue (matrix must be nonsingular)");
-    std::sort(lam.begin(), lam.end());
-    if (seed != 0) {
-        std::mt19937_64 rng(seed);
-        std::shuffle(lam.begin(), lam.end(), rng);
-    }
-    BandedSymmetric A(n, b);
-    A.bands[0] = lam;
-    // rotate rows/cols (p, p+1); the incoming bulge sits at (p+1, p-b), the outgoing one
-    // is created at (p+b+1, p); returns it (has = whether that position exists)
-    auto rot = [&](int p, double c, double s, double bin, bool hasin, bool& has) {
-        const int q = p + 1;
-        for (int k = std::max(0, p - b); k < p; ++k) {
-            const double x = A.bands[p - k][k];
-            const bool inb = q - k <= b;
-            const double y = inb ? A.bands[q - k][k] : (hasin && k == p - b ? bin : 0.0);
-            A.bands[p - k][k] = c * x + s * y;
-            if (inb) A.bands[q - k][k] = -s * x + c * y;
-        }
-        const double app = A.bands[0][p], aqq = A.bands[0][q], apq = A.bands[1][p];
-        A.bands[0][p] = c * c * app + 2.0 * c * s * apq + s * s * aqq;
-        A.bands[0][q] = s * s * app - 2.0 * c * s * apq + c * c * aqq;
-        A.bands[1][p] = c * s * (aqq - app) + (c * c - s * s) * apq;
-        double bout = 0.0;
-        for (int k = q + 1; k <= std::min(n - 1, p + b + 1); ++k) {
-            const bool xin = k - p <= b;
-            const double x = xin ? A.bands[k - p][p] : 0.0;
-            const double y = A.bands[k - q][q];
-            if (xin) A.bands[k - p][p] = c * x + s * y;
-            else bout = c * x + s * y;
-            A.bands[k - q][q] = -s * x + c * y;
-        }
-        has = p + b + 1 <= n - 1;
-        return bout;
-    };
-    for (int i = n - 1; i >= 1; --i) {
-        double c, s;
-        givens_pair(A.bands[0][i], 1.0, c, s);
-        bool has;
-        double bulge = rot(i - 1, c, s, 0.0, false, has);
-        int brow = i + b;
-        while (has) {
-            const int p = brow - 1;
-            givens_pair(A.bands[b][p - b], bulge, c, s);
-            bulge = rot(p, c, s, bulge, true, has);
-            brow += b;
-        }
-    }
-    return A;
 }
 
 // ------------------------------------------------------------------ run report (tools/specproj.cpp:82-118)

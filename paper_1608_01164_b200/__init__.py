@@ -103,7 +103,7 @@ ABI_SYMBOLS = (
     "spg_result_apply", "spg_result_free", "spg_last_error", "spg_tree", "spg_qdwh_params", "spg_l_update",
     "spg_make_dimer_chain", "spg_make_random_banded", "spg_kcap", "spg_ctx_create", "spg_ctx_free",
     "spg_ctx_upload", "spg_ctx_flat_size", "spg_ctx_download", "spg_ctx_op", "spg_ctx_from_banded",
-    "spg_truncate", "spg_set_profile", "spg_measure_dmma_tflops", "spg_micro_kernel", "spg_host_alloc",
+    "spg_truncate", "spg_set_profile", "spg_measure_dmma_tflops", "spg_host_alloc",
     "spg_host_free", "spg_hqdwh_shifts", "spg_release_plan_cache", "spg_stacked_qr_r",
 )
 
@@ -146,7 +146,6 @@ def load_library(path: str | None = None):
         "spg_truncate": ([C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_double, _dp, _dp, _ip], C.c_int),
         "spg_set_profile": ([C.c_int], None),
         "spg_measure_dmma_tflops": ([_dp], C.c_int),
-        "spg_micro_kernel": ([C.c_int, C.c_int, C.c_int, _dp, C.c_int], C.c_int),
         "spg_host_alloc": ([C.c_longlong, C.POINTER(vp)], C.c_int),
         "spg_host_free": ([vp], None),
         "spg_hqdwh_shifts": ([C.c_int, C.c_int, _dp, C.c_int, _dp, C.c_int, C.c_double, C.c_double, C.c_int,
@@ -585,14 +584,6 @@ def measure_dmma_tflops() -> float:
     out = np.zeros(1)
     _raise(load_library().spg_measure_dmma_tflops(_d(out)))
     return float(out[0])
-
-
-def micro_kernel(which: int, n: int, reps: int = 20) -> np.ndarray:
-    """Diagnostics: times one critical-path kernel on a synthetic input (see
-    spg_micro_kernel in include/specproj_b200.h)."""
-    out = np.zeros(16)
-    _raise(load_library().spg_micro_kernel(which, n, reps, _d(out), 16))
-    return out
 
 
 def qdwh_params(l):

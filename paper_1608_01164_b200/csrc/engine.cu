@@ -203,7 +203,7 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     }
     int max_leaf = 0;
     for (int x = 0; x < tree_.nnodes(); ++x) if (tree_.leaf(x)) max_leaf = std::max(max_leaf, tree_.size[x]);
-    if (max_leaf > C4_LEAF_MAX || std::getenv("SPG_CHOL_SPLIT_MIN"))
+    if (max_leaf > C4_LEAF_MAX)
         SPG_CUDA(cudaMalloc(&leaf_scr_, sizeof(double) * (size_t)(TRM_NMAX / 2) * (TRM_NMAX / 2)));
     // device tree
     std::vector<int> tb = tree_.begin, ts = tree_.size, tl = tree_.left, tr = tree_.right, tv = tree_.level,
@@ -354,21 +354,20 @@ std::unique_ptr<DHodlr> Engine::new_hodlr() {
 }
 
 // ---------------------------------------------------------------- truncation batch
-static const double g_tsqr_segk = std::getenv("SPG_TSQR_SEGK") ? std::atof(std::getenv("SPG_TSQR_SEGK")) : 48.0;
+constexpr double kTsqrSegK = 48.0;   // TSQR segment length ~ sqrt(rows * 48) (merge vs segment balance)
 
 // Level-batched truncations mix a few tall tasks (top levels: long TSQR chains with a merge
 // level) with many short ones.  On the main stream outside the Cholesky the tall ones run on
 // a side stream next to the short ones, so their merge / core / apply chain overlaps the
 // short tasks' launches instead of following them.  Both halves take their workspace from
-// the main stack, the tall half's kept until the join.  SPG_TRUNC_SPLIT_OFF=1: one batch.
-static const bool g_trunc_split_off = std::getenv("SPG_TRUNC_SPLIT_OFF") != nullptr;
-static const int g_trunc_tall = std::getenv("SPG_TRUNC_TALL") ? std::atoi(std::getenv("SPG_TRUNC_TALL")) : 2048;
+// the main stack, the tall half's kept until the join.
+constexpr int kTruncTall = 2048;
 
 void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     if (tasks.empty()) return;
-    if (side_sel_ < 0 && cur_op_ != 6 && !g_trunc_split_off && tasks.size() >= 2) {
+    if (side_sel_ < 0 && cur_op_ != 6 && tasks.size() >= 2) {
         std::vector<TTask> tall, flat;
-        for (auto& t : tasks) (std::max(t.p, t.s) > g_trunc_tall ? tall : flat).push_back(t);
+        for (auto& t : tasks) (std::max(t.p, t.s) > kTruncTall ? tall : flat).push_back(t);
         if (!tall.empty() && !flat.empty()) {
             const long long mark = ws_->mark();
             const int evf = ev_base3_ + 2 * tree_.nnodes(), evj = evf + 1;
@@ -400,7 +399,7 @@ void Engine::trunc_batch(Plan& p, std::vector<TTask> tasks, Workspace& wsp, bool
             // sub-block QRs, so seg ~ sqrt(rows * k) balances them (k ~ 48 typical).
             int seg = rows, nseg = 1;
             if (rows > 2 * SB) {
-                seg = std::max(2 * SB, (int)std::ceil(std::sqrt((double)rows * g_tsqr_segk) / SB) * SB);
+                seg = std::max(2 * SB, (int)std::ceil(std::sqrt((double)rows * kTsqrSegK) / SB) * SB);
                 nseg = (rows + seg - 1) / seg;
                 if (nseg == 1) seg = rows;
             }
@@ -436,9 +435,8 @@ void Engine::trunc_batch(Plan& p, std::vector<TTask> tasks, Workspace& wsp, bool
 }
 
 // ---------------------------------------------------------------- GEMM batch
-static const int g_gemm_fill = std::getenv("SPG_GEMM_FILL") ? std::atoi(std::getenv("SPG_GEMM_FILL")) : 2;     // CTAs per SM targeted by split-K
-static const int g_gemm_minkt = std::getenv("SPG_GEMM_MINKT") ? std::atoi(std::getenv("SPG_GEMM_MINKT")) : 4;   // k-tiles per split, at least
-static const bool g_gemm_split_v1 = std::getenv("SPG_GEMM_SPLIT_V1") != nullptr;   // A/B: split-K only for K >= 2048
+constexpr int kGemmFill = 2;    // CTAs per SM targeted by split-K
+constexpr int kGemmMinKt = 4;   // k-tiles per split, at least
 
 void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>& caps) {
     if (items.empty()) return;
@@ -455,8 +453,8 @@ void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>&
             base += t;
             ktiles += t * ((caps[i].z + 15) / 16);
         }
-    const long long fillc = (long long)g_gemm_fill * 148;
-    const long long chunk = std::max<long long>(g_gemm_minkt, (ktiles + fillc - 1) / std::max<long long>(fillc, base));
+    const long long fillc = (long long)kGemmFill * 148;
+    const long long chunk = std::max<long long>(kGemmMinKt, (ktiles + fillc - 1) / std::max<long long>(fillc, base));
     for (size_t i = 0; i < items.size(); ++i) {
         GemmItem& g = items[i];
         const int mM = caps[i].x, mN = caps[i].y, mK = caps[i].z;
@@ -467,14 +465,8 @@ void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>&
         // partials stay within a quarter of the stream's workspace
         const long long room = (long long)wsp.capacity() / 4 - (wsp.mark() - mark);
         while (ns >= 2 && (long long)ns * mM * mN > room) ns /= 2;
-        if (ns >= 2 && !g_gemm_split_v1) {
+        if (ns >= 2) {
             g.nsplit = ns;
-            g.Mcap = mM;
-            g.Ncap = mN;
-            g.partial = wsp.ptr(wsp.alloc((long long)g.nsplit * mM * mN));
-            red.push_back((int)i);
-        } else if (g_gemm_split_v1 && mK >= 2048 && tm * tn <= 8) {
-            g.nsplit = std::min(64, (mK + 1023) / 1024);
             g.Mcap = mM;
             g.Ncap = mN;
             g.partial = wsp.ptr(wsp.alloc((long long)g.nsplit * mM * mN));
@@ -614,19 +606,17 @@ void Engine::cascade(Plan& p, DHodlr& H, const std::vector<Cascade>& cs, bool up
     }
 }
 
-static const bool g_psolve_off = std::getenv("SPG_PSOLVE_OFF") != nullptr;
-static const int g_psolve_min = std::getenv("SPG_PSOLVE_MIN") ? std::atoi(std::getenv("SPG_PSOLVE_MIN")) : 2;   // smallest subtree depth solved subtree-parallel
-static const bool g_chol_tv_off = std::getenv("SPG_CHOL_TV_OFF") != nullptr;   // A/B: sequential subtree solves in the Cholesky
+constexpr int kPsolveMin = 2;   // smallest subtree depth solved subtree-parallel (smaller: k_hsolve2)
 // subtrees of at least this depth are solved subtree-parallel inside the Cholesky (smaller: k_hsolve2)
-static const int g_chol_tv_min = std::getenv("SPG_CHOL_TV_MIN") ? std::atoi(std::getenv("SPG_CHOL_TV_MIN")) : 4;
+constexpr int kCholTvMin = 4;
 
 void Engine::hsolve(Plan& p, const DHodlr& W, std::vector<HSolveItem> items) {
     if (items.empty()) return;
-    if (W.tready && !g_psolve_off) {   // subtrees of >= 4 leaves: the subtree-parallel form
+    if (W.tready) {   // subtrees of >= 4 leaves: the subtree-parallel form
         std::vector<HSolveItem> big, small;
         for (const auto& it : items) {
             const int dep = tree_.depth - tree_.level[it.root];   // levels below the root
-            (dep >= g_psolve_min ? big : small).push_back(it);
+            (dep >= kPsolveMin ? big : small).push_back(it);
         }
         if (!big.empty()) psolve(p, W, big);
         if (small.empty()) return;
@@ -703,7 +693,6 @@ void Engine::psolve(Plan& p, const DHodlr& W, const std::vector<HSolveItem>& ite
 // tV_t[rows r(y)] = W_{r(y)}^{-T} V_y and tU_t[rows l(y)] = W_{l(y)}^{-1} U_y for every
 // internal node y, bottom-up (a level's solves use the bases of the levels below).
 void Engine::op_solve_prep(Plan& p, DHodlr& W) {
-    if (g_psolve_off) return;
     const int n = tree_.n;
     if (!W.tU) {
         SPG_CUDA(cudaMalloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
@@ -1015,15 +1004,13 @@ void Engine::op_multiply(Plan& p, const DHodlr& A, const DHodlr& B, DHodlr& C, b
 // block still receives its updates in the reference's order (the side stream is
 // FIFO), so the factor is unchanged; the cascades just leave the critical path.
 // Only M's upper blocks and leaves are updated: cholesky_rec never reads M.lower.
-// SPG_CHOL_SERIAL=1 restores the single-stream schedule (A/B checks).
-static const bool g_chol_serial = std::getenv("SPG_CHOL_SERIAL") != nullptr;
 
 void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool defer_trunc) {
     cur_op_ = 6;
     W.tready = false;
     W.tv_built.clear();
-    chol_defer_trunc_ = defer_trunc && !g_chol_serial;
-    chol_tv_ = chol_defer_trunc_ && !g_psolve_off && !g_chol_tv_off;
+    chol_defer_trunc_ = defer_trunc;
+    chol_tv_ = chol_defer_trunc_;
     if (chol_tv_) {   // forward subtree solves inside the factorisation go subtree-parallel
         if (!W.tU) {
             SPG_CUDA(cudaMalloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
@@ -1036,7 +1023,7 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
         for (int x = 0; x < tree_.nnodes(); ++x) {
             if (tree_.leaf(x)) continue;
             const int l = tree_.left[x];
-            if (tree_.depth - tree_.level[l] < g_chol_tv_min) continue;
+            if (tree_.depth - tree_.level[l] < kCholTvMin) continue;
             tree_.subtree(l, in, lv);
             for (int y : in) tv_need_[y] = 1;
         }
@@ -1045,11 +1032,6 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
     op_copy(p, M, work);
     const DHodlr* Wp = &W;
     push(p, [Wp](cudaStream_t st) { Wp->zero(st); });
-    if (g_chol_serial) {
-        chol_deferred_ = false;
-        chol_rec(p, 0, work, W);
-        return;
-    }
     const int nn = tree_.nnodes(), nside = ncasc_, nall = (int)sides_.size();
     last_leaf_ev_.assign(nn, -1);
     last_block_ev_.assign(nn, -1);
@@ -1127,18 +1109,15 @@ void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU,
 // Leaves above the fast leaf kernel's size (C4_LEAF_MAX < s <= TRM_NMAX, s % 64 == 0) as a
 // 2x2 block Cholesky: W11 = chol(M11); W12 = W11^{-T} M21^T (DMMA row-strip TRSM);
 // S = M22 - W12^T W12 (DMMA GEMM); W22 = chol(S).  Same factor as the unblocked
-// recursion of cholesky.hpp up to summation order (SPG_CHOL_SPLIT_OFF=1: one kernel).
-static const bool g_no_split = std::getenv("SPG_CHOL_SPLIT_OFF") != nullptr;
-static const int g_split_min = std::getenv("SPG_CHOL_SPLIT_MIN") ? std::atoi(std::getenv("SPG_CHOL_SPLIT_MIN"))
-                                                                  : C4_LEAF_MAX + 1;   // smallest split leaf
+// recursion of cholesky.hpp up to summation order.
 
 void Engine::leaf_chol_split(Plan& p, const double* Ml, double* Wl, double* D, int s) {
     const int h = s / 2;
     unsigned* status = sc_.status;
     double* S = leaf_scr_;
-    const CholItem* c1 = arena_->push(std::vector<CholItem>{CholItem{Ml, Wl, h, s, s, D, nullptr, 1}});
+    const CholItem* c1 = arena_->push(std::vector<CholItem>{CholItem{Ml, Wl, h, s, s, D, 1}});
     const CholItem* c2 = arena_->push(std::vector<CholItem>{
-        CholItem{S, Wl + h + (size_t)h * s, h, h, s, D + (size_t)(h / 32) * 1024, nullptr, 1}});
+        CholItem{S, Wl + h + (size_t)h * s, h, h, s, D + (size_t)(h / 32) * 1024, 1}});
     const TrsmItem* tr = arena_->push(std::vector<TrsmItem>{TrsmItem{Wl, Wl + (size_t)h * s, h, s, s, nullptr, h, 0, 0, D}});
     push_timed(p, PC_LEAF, [=](cudaStream_t st) {
         launch_leaf_split_prep(Ml, Wl, S, s, h, st);
@@ -1155,11 +1134,11 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     if (tree_.leaf(x)) {
         if (chol_deferred_ && last_leaf_ev_[x] >= 0) wait(p, last_leaf_ev_[x]);
         const int s = tree_.size[x];
-        if (s >= g_split_min && s <= TRM_NMAX && s % 64 == 0 && leaf_scr_ && !g_no_split) {
+        if (s > C4_LEAF_MAX && s <= TRM_NMAX && s % 64 == 0 && leaf_scr_) {
             leaf_chol_split(p, M.leaf(x), W.leaf(x), W.leaf_dinv(x), s);
             return;
         }
-        std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s, W.leaf_dinv(x), nullptr, 1}};   // W memset above
+        std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s, W.leaf_dinv(x), 1}};   // W memset above
         const CholItem* d = arena_->push(ci);
         unsigned* status = sc_.status;
         push_timed(p, PC_LEAF, [d, status, s](cudaStream_t st) { launch_leaf_cholesky(d, 1, status, st, s); });
@@ -1179,7 +1158,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
         double* X = xpanels_[t];
         copy(p, {CopyItem{M.upU(x), X + bl, s1, n, n, M.rup(x), 0, 1.0, nullptr}}, s1, KCAP);
         if (wtr_last_ev_ >= 0 && !tree_.leaf(l)) wait(p, wtr_last_ev_);
-        if (chol_tv_ && tree_.depth - tree_.level[l] >= g_chol_tv_min) {   // subtree-parallel: tV inside l built
+        if (chol_tv_ && tree_.depth - tree_.level[l] >= kCholTvMin) {   // subtree-parallel: tV inside l built
             wait(p, ev_base3_ + tree_.nnodes() + l);
             hsolve(p, W, {HSolveItem{l, X + bl, n, M.rup(x), 0, 0}});
         } else {
@@ -1221,7 +1200,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
             double* tv = W.tslabV(t) + br;
             copy(p, {CopyItem{W.upV(x), tv, s2, n, n, W.rup(x), 0, 1.0, nullptr}}, s2, KCAP);
             const bool tr = W.tready;
-            W.tready = tree_.depth - tree_.level[r] >= g_chol_tv_min;
+            W.tready = tree_.depth - tree_.level[r] >= kCholTvMin;
             hsolve(p, W, {HSolveItem{r, tv, n, W.rup(x), 0, 0}});
             W.tready = tr;
             W.tv_built[x] = 1;
@@ -1244,17 +1223,13 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
     // Schur: M22 -= V (U^T U) V^T
     {
         double* G = coef_ + (size_t)(4 * x + 2) * KCAP * KCAP;
-        double* P1 = chol_deferred_ ? chol_panels_[t] : panel(1);
+        double* P1 = chol_panels_[t];
         gemm(p, {gitem(W.upU(x), n, 1, W.upU(x), n, 0, G, KCAP, 0, W.rup(x), 0, W.rup(x), s1, nullptr, -1.0, 0.0)},
              {make_int3(KCAP, KCAP, s1)});
         gemm(p, {gitem(W.upV(x), n, 0, G, KCAP, 0, P1 + br, n, s2, nullptr, 0, W.rup(x), 0, W.rup(x), 1.0, 0.0)},
              {make_int3(s2, KCAP, KCAP)});
-        if (chol_deferred_) {
-            record(p, x);
-            cascade_chol(p, M, x, r, P1, W.slabV(t), W.rup(x));
-        } else {
-            cascade(p, M, {Cascade{r, P1, W.slabV(t), W.rup(x), 1.0}}, /*upper_only=*/true);   // M.lower is never read
-        }
+        record(p, x);
+        cascade_chol(p, M, x, r, P1, W.slabV(t), W.rup(x));
     }
     chol_rec(p, r, M, W);
 }
@@ -1262,7 +1237,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
 // all-leaves TRSM of the level-batched solves: the DMMA row-strip kernel when every
 // leaf is a multiple of 32 (diagonal-block inverses present), else the generic one
 void Engine::leaf_trsm_batch(Plan& p, const std::vector<TrsmItem>& ti, const std::vector<int2>& ct) {
-    bool rows = !std::getenv("SPG_TRSM_V1");
+    bool rows = true;
     int maxn = 0, maxrhs = 0;
     for (const auto& t : ti) {
         maxrhs = std::max(maxrhs, t.ncp ? KCAP : t.nc);

@@ -9,6 +9,7 @@
 //   k >= 1    : Z = X X, Z = cZ + I, W = chol(Z), Y = X W^{-1}, V = Y W^{-T}
 //   every k   : X = (b/c) X + (a - b/c) V  (or M-scaled), symmetrize
 //   final     : P = (I - X) / 2
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -507,7 +508,11 @@ std::unique_ptr<HqdwhState> make_state_once(int n, int b, int n_min, double eps,
     st->X = E.new_hodlr(); st->Z = E.new_hodlr(); st->W = E.new_hodlr(); st->Y = E.new_hodlr();
     st->V = E.new_hodlr(); st->WK = E.new_hodlr(); st->P = E.new_hodlr();
     const int wbl = 3 * b + 1;
-    const size_t tmp_doubles = (size_t)n * std::max(wbl, 4 * b + 4) + 8 * (size_t)n + 128 + 165000;   // + Hager chunk maps (k_seq.cu)
+    // setup scratch d_tmp: alpha at [0] and the power-iteration vectors at [64, 64 + 2n);
+    // l0: the banded LU (n x (3b+1)) at [128, ...) and the Hager vectors right after it (b = 1:
+    // 9 n doubles from 128); first iterate: the band H / Givens work rows, n x (4b + 4)
+    const size_t tmp_doubles = std::max({(size_t)128 + (size_t)n * wbl + estimate_l0_vecs_doubles(n),
+                                         (size_t)128 + 9 * (size_t)n, (size_t)n * (4 * b + 4), (size_t)64 + 2 * (size_t)n});
     SPG_CUDA(cudaMalloc(&st->d_bands, sizeof(double) * band_len(n, b)));
     SPG_CUDA(cudaMalloc(&st->d_tmp, sizeof(double) * tmp_doubles));
     SPG_CUDA(cudaMalloc(&st->d_rdiag, sizeof(double) * (size_t)(2 * b + 1) * n));
@@ -566,8 +571,6 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     const long long blen = band_len(n, b);
     for (long long i = 0; i < blen; ++i)
         if (!std::isfinite(bands_host[i])) throw StatusError(SPG_INVALID_ARGUMENT, "hqdwh: nonfinite input");
-    const auto hc0 = std::chrono::steady_clock::now();
-    auto hms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hc0).count(); };
     const bool profile = g_profile.load() != 0;
     const bool use_graph = !profile && !std::getenv("SPG_NO_GRAPH");
     auto R = std::make_unique<spg_result>();
@@ -582,7 +585,6 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     double *d_bands = stt.d_bands, *d_tmp = stt.d_tmp, *d_diag = stt.d_diag;
     int* d_piv = stt.d_piv;
     const int wbl = 3 * b + 1;
-    const double h_alloc = hms();
 
     // ---- timing instrumentation: per-run event tables, no host sync inside the loop
     stt.evnext = 0;
@@ -709,10 +711,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     // ---------------- k >= 1: Cholesky-based iterates (graph replay; rebuilt per run in profile mode)
     {
         if (use_graph && !stt.graphs) {
-            const double h0 = hms();
             build_graphs(stt);
-            if (std::getenv("SPG_HOST_TIMING"))
-                std::fprintf(stderr, "host: graphs built in %.1f ms (arena %.1f MB)\n", hms() - h0, E.arena().used() / 1048576.0);
         }
         R->info.graph_used = stt.graphs ? 1 : 0;
         R->info.graph_nodes = stt.nodes_iter;
@@ -758,9 +757,6 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     SPG_CUDA(cudaStreamSynchronize(st));
     SPG_CUDA(cudaGetLastError());
     if (stt.graphs) E.arena().release(std::max(amark, stt.arena_mark));   // per-call descriptors
-    if (std::getenv("SPG_HOST_TIMING"))
-        std::fprintf(stderr, "host: state %s %.1f ms, run_hqdwh to sync %.1f ms\n", cached ? "cached" : "built", h_alloc,
-                     hms());
     check_status_dev(S.status);
 
     // ---------------- report
@@ -810,8 +806,6 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     {
         double ctr[8];
         SPG_CUDA(cudaMemcpy(ctr, S.counters, sizeof(ctr), cudaMemcpyDeviceToHost));
-        if (std::getenv("SPG_CORE_STATS"))
-            std::fprintf(stderr, "core tasks %.0f, with k_in > 64: %.0f\n", ctr[2], ctr[3]);
         I.trunc_bytes = ctr[0];
         I.gemm_flops = ctr[1];
         I.trunc_tasks = (long long)ctr[2];
@@ -954,12 +948,6 @@ void spg_host_free(void* p) {
     if (p) cudaFreeHost(p);
 }
 
-int spg_micro_kernel(int which, int n, int reps, double* out, int nout) {
-    return guarded([&]() {
-        ensure_device();
-        if (micro_kernel(which, n, reps, out, nout) != 0) throw std::invalid_argument("spg_micro_kernel: unknown kernel");
-    });
-}
 
 int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double delta, spg_result** out) {
     *out = nullptr;

@@ -19,30 +19,6 @@
 
 namespace spg {
 
-__device__ int g_core_hist_on = 0;            // diagnostics: histograms of k_in, r', sweeps, rank
-__device__ unsigned g_core_hist[4][128];
-__device__ __forceinline__ void core_hist(int k, int rp, int sweeps, int r) {
-    if (!g_core_hist_on) return;
-    atomicAdd(&g_core_hist[0][min(k, 127)], 1u);
-    atomicAdd(&g_core_hist[1][min(rp, 127)], 1u);
-    atomicAdd(&g_core_hist[2][min(sweeps, 127)], 1u);
-    atomicAdd(&g_core_hist[3][min(r, 127)], 1u);
-}
-void core_hist_ctl(int enable, double* out, int nout) {
-    if (enable >= 0) {
-        SPG_CUDA(cudaMemcpyToSymbol(g_core_hist_on, &enable, sizeof(int)));
-        static unsigned z[4][128] = {};
-        SPG_CUDA(cudaMemcpyToSymbol(g_core_hist, z, sizeof(z)));
-    }
-    if (out) {
-        unsigned h[4][128];
-        SPG_CUDA(cudaMemcpyFromSymbol(h, g_core_hist, sizeof(h)));
-        for (int i = 0; i < nout && i < 512; ++i) out[i] = h[i / 128][i % 128];
-    }
-}
-__device__ long long* g_core_trace = nullptr;   // micro-benchmarks: clock64 per phase of task 0
-void set_core_trace(long long* p) { SPG_CUDA(cudaMemcpyToSymbol(g_core_trace, &p, sizeof(p))); }
-#define CORE_TRACE(k) do { if (g_core_trace && blockIdx.x == 0 && threadIdx.x == 0) g_core_trace[k] = clock64(); } while (0)
 
 
 __device__ __forceinline__ double csum(double v) {
@@ -125,7 +101,6 @@ __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double*
         if (tid == 0) { hdr[0] = 0; hdr[1] = 0; *t.orank = 0; }
         return;
     }
-    CORE_TRACE(0);
     const double* Ru = core_final_R(t, ws, 0);
     const double* Rv = core_final_R(t, ws, 1);
     // C[i][j] = sum_l Ru[i][l] Rv[j][l], l >= max(i, j); Frobenius norm for the noise floor
@@ -154,7 +129,6 @@ __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double*
     }
     __syncthreads();
     const double delta = sDelta;
-    CORE_TRACE(1);
     // ---- Householder QR with column pivoting (stop at small remaining norms)
     int rr = 0;
     for (int j = 0; j < k; ++j) {
@@ -226,7 +200,6 @@ __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double*
         rr = j + 1;
     }
     const int rp = rr;
-    CORE_TRACE(2);
     // ---- spill the reflectors (needed for Zu) to the task's core scratch, Z = R'^T (k x rp), V_J = I
     double* gR = ws + t.ws + t.wcore;
     for (int idx = tid; idx < k * k; idx += blockDim.x) {
@@ -244,7 +217,6 @@ __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double*
         sJ[i + j * KIN_MAX] = i == j ? 1.0 : 0.0;
     }
     __syncthreads();
-    CORE_TRACE(3);
     int nsweeps = 0;
     // ---- one-sided Jacobi on the columns of Z (circle-method rounds, 8-lane groups)
     if (rp > 1) {
@@ -310,8 +282,6 @@ __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double*
             __syncthreads();
         }
     }
-    CORE_TRACE(4);
-    if (g_core_trace && blockIdx.x == 0 && tid == 0) { g_core_trace[8] = nsweeps; g_core_trace[9] = rp; g_core_trace[10] = k; }
     // ---- singular values, ordering, rank
     for (int j = warp; j < rp; j += nwarps) {
         double s = 0.0;
@@ -382,7 +352,6 @@ __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double*
     }
     __syncthreads();
     if (tid == 0) *t.orank = r;
-    CORE_TRACE(5);
 }
 
 // ---------------------------------------------------------------------------
@@ -461,7 +430,6 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gi = lane >> 2, gk = lane & 3;
     double* hdr = ws + t.ws;
-    CORE_TRACE(0);
     const double* Ru = core_final_R(t, ws, 0);
     const double* Rv = core_final_R(t, ws, 1);
     for (int idx = tid; idx < K3 * K3; idx += TS_THREADS) {
@@ -507,7 +475,6 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     __syncthreads();
     const double delta = sDelta3;
     const double delta2 = delta * delta;
-    CORE_TRACE(1);
     // ---- QRCP
     // squared column norms double-buffered (read cur, write nxt) so that the redundant
     // per-warp pivot search never races with the updates; after each reflector they
@@ -603,7 +570,6 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         __syncthreads();
         rp = j + 1;
     }
-    CORE_TRACE(2);
     // reflector tails scaled in place, R(j, j) = beta_j; unpivoted columns appended to the order
     for (int j = warp; j < rp; j += 16) {
         double* col = sC + sPerm3[j] * L3;
@@ -634,7 +600,6 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         sPairs[r * 32 + pi] = (unsigned short)(p | (q << 8));
     }
     __syncthreads();
-    CORE_TRACE(3);
     int nsweeps = 0;
     const int nact = (npairs + 1) / 2;   // warps holding a pair (a half-warp per pair)
     if (rp > 1 && warp < nact) {
@@ -699,8 +664,6 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         }
     }
     __syncthreads();
-    CORE_TRACE(4);
-    if (g_core_trace && blockIdx.x == 0 && tid == 0) { g_core_trace[8] = nsweeps; g_core_trace[9] = rp; g_core_trace[10] = k; }
     // ---- singular values, order, rank
     for (int j = warp; j < rp; j += 16) {
         const double a0 = lane < k ? sZ[lane + j * L3] : 0.0;
@@ -733,7 +696,6 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         }
         sR3 = r;
         hdr[0] = k; hdr[1] = r;
-        core_hist(k, rp, nsweeps, r);
         if (rp > 0 && !(sSig[sOrd3[0]] == sSig[sOrd3[0]])) atomicOr(status, ST_NONFINITE);
         count_trunc_work(status, t.p, t.s, k, r);   // SURVEY.md §8d work units
     }
@@ -784,7 +746,6 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     }
     __syncthreads();
     if (tid == 0) *t.orank = r;
-    CORE_TRACE(5);
 }
 
 __global__ void __launch_bounds__(TS_THREADS, 1) k_core_any(const TTask* __restrict__ tasks, double* __restrict__ ws,
@@ -797,20 +758,18 @@ __global__ void __launch_bounds__(TS_THREADS, 1) k_core_any(const TTask* __restr
             core3_body(t, k, ws, eps, status, smem);
             return;
         }
-        if (k > K3 && threadIdx.x == 0) atomicAdd(reinterpret_cast<double*>(status + 16) + 3, 1.0);
     }
     core2_body(tasks, ws, eps, status, smem);
 }
 
 size_t core2_smem() { return sizeof(double) * (2 * KIN_MAX * KIN_MAX); }
-static const bool g_core2_only = std::getenv("SPG_CORE2") != nullptr;
 
 void core2_init_attributes() {
     SPG_CUDA(cudaFuncSetAttribute(k_core_any, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)core2_smem()));
 }
 
 void launch_core2(const TTask* tasks, int ntasks, double* ws, double eps, unsigned* status, cudaStream_t st) {
-    k_core_any<<<ntasks, TS_THREADS, core2_smem(), st>>>(tasks, ws, eps, status, g_core2_only ? 0 : 1);
+    k_core_any<<<ntasks, TS_THREADS, core2_smem(), st>>>(tasks, ws, eps, status, 1);
     SPG_LAUNCH_CHECK();
 }
 

@@ -257,13 +257,10 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
         const int i = idx % n, j = idx / n;
         if (i > j) C.W[i + (long long)j * C.ldw] = 0.0;
     }
-    long long* tr = C.trace;
-#define CH_TRACE(k) if (tr && tid == 0) tr[(J / CH_NB) * 8 + (k)] = clock64()
     for (int J = 0; J < n; J += CH_NB) {
         const int nb = min(CH_NB, n - J), mr = n - J;           // panel columns / rows
         const int nrt = (mr + 7) / 8;
         const int nch = J / KC;
-        CH_TRACE(0);
         // group 0 also carries the M panel: sP[i + jj ld] = M[J+i, J+jj]
         for (int idx = tid; idx < mr * nb; idx += CH_THREADS) {
             const int i = idx % mr, jj = idx / mr;
@@ -311,7 +308,6 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
         }
         cp_wait_l<0>();
         __syncthreads();
-        CH_TRACE(1);
         // P = M[J+i, J+jj] - S  (lower part only is meaningful)
 #pragma unroll
         for (int a = 0; a < 5; ++a) {
@@ -326,7 +322,6 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
                 }
         }
         __syncthreads();
-        CH_TRACE(2);
         // (2a) warp 0: Cholesky of the nb x nb diagonal block, lane i holding row i
         //      in registers (column j of L broadcast by shuffles)
         if (warp == 0) {
@@ -368,7 +363,6 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
             if (lane >= nb) sInv[lane] = 1.0;
         }
         __syncthreads();
-        CH_TRACE(3);
         if (warp == 0) {
             // (2c) D = W_bb^{-1} = (L11^{-1})^T: lane i forms row i of L11^{-1} (t L11 = e_i,
             //      solved right-looking from the last column) = column i of D
@@ -413,16 +407,13 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol2(const CholItem* __res
             }
         }
         __syncthreads();
-        CH_TRACE(4);
         // (3) L(J+i, J+jj) -> W(J+jj, J+i)
         for (int idx = tid; idx < mr * nb; idx += blockDim.x) {
             const int jj = idx % nb, i = idx / nb;
             if (i >= jj) C.W[(J + jj) + (long long)(J + i) * C.ldw] = sP[i + jj * ldp];
         }
         __syncthreads();
-        CH_TRACE(5);
     }
-#undef CH_TRACE
     if (tid == 0 && sFail) atomicOr(status, ST_NPD);
 }
 
@@ -506,12 +497,9 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
         if (i > j) C.W[i + (long long)j * ldw] = 0.0;
     }
     __syncthreads();
-    long long* tr = C.trace;
-#define C3_TRACE(k) if (tr && tid == 0) tr[(J / CH_NB) * 8 + (k)] = clock64()
     for (int J = 0; J < n; J += CH_NB) {
         const int nb = min(CH_NB, n - J), mr = n - J;
         const int nrt = (mr + 7) / 8;
-        C3_TRACE(0);
         const int nks = J / 4;
         const int nseg = nks > 0 ? max(1, min(nks / 8, C3_TASKS / nrt)) : 0;
         const int ntask = nrt * nseg;
@@ -565,9 +553,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
             }
             cp_wait_l<0>();
         }
-        C3_TRACE(1);
         __syncthreads();
-        C3_TRACE(2);
         if (nseg > 0)   // P = M - S, fixed-order reduction over the K segments
             for (int jj = warp; jj < nb; jj += NW)
                 for (int i = jj + lane; i < mr; i += 32) {
@@ -577,7 +563,6 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
                     sP[i + jj * ldp] -= s;
                 }
         __syncthreads();
-        C3_TRACE(3);
         // (2a) diagonal block, warp 0: rows in registers, column j broadcast through
         //      a double-buffered shared vector (one warp barrier per column)
         if (warp == 0) {
@@ -611,7 +596,6 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
             if (lane >= nb) sInv[lane] = 1.0;
         }
         __syncthreads();
-        C3_TRACE(4);
         if (warp > 0) {
             // diagonal block of L -> W(J.., J+col) (coalesced), then
             // (2b) L21 = P21 L11^{-T}, one row per thread, written straight to W
@@ -641,9 +625,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_leaf_chol3(const CholItem* __res
             }
         }
         __syncthreads();
-        C3_TRACE(5);
     }
-#undef C3_TRACE
     if (warp == 0 && C.D) {   // W_bb^{-1} of the last panel
         const int Jl = ((n - 1) / 32) * 32;
         chol3_dinv(sL11, sInv, min(CH_NB, n - Jl), C.D + (long long)(Jl / 32) * 1024, status);
@@ -739,9 +721,7 @@ __device__ __forceinline__ void c4_sub_abt(double* Y, const double* pa, const do
     }
 }
 
-__device__ int g_c4_flags = 0;   // diagnostics only (SPG_C4_FLAGS): 1 skip W copy, 2 skip lookahead, 4 skip h1/h2
 __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __restrict__ it, unsigned* status) {
-    const int dflags = g_c4_flags;
     extern __shared__ double sm4[];
     const CholItem C = it[blockIdx.x];
     const int n = C.n;
@@ -773,8 +753,6 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
     __syncthreads();
-    long long* tr = C.trace;
-#define C4_TRACE(k) if (tr && tid == 0) tr[(J / 32) * 8 + (k)] = clock64()
     for (int J = 0; J < n; J += 32) {
         const int pi = J / 32;
         double* cur = sm4 + (pi % 3) * pstride;
@@ -783,12 +761,10 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
         double* sD = sDb + (pi & 1) * 32 * C4_DP;
         const double* sDp = sDb + ((pi + 1) & 1) * 32 * C4_DP;   // D of panel J-32
         const int mr = n - J;
-        C4_TRACE(0);
         if (J > 0) {   // (a) diagonal block rows
             if (warp < 4) c4_sub_abt(cur, prv + 32, prv + 32, ldp, warp, warp + 1, 1, gi, gk);
             __syncthreads();
         }
-        C4_TRACE(1);
         if (warp == 0) {
             // (b0) diagonal block factor in two 16-column halves
             double r[16], q[16];
@@ -856,7 +832,6 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
                 for (int k = jj + 1; k < 16; ++k) q[k] -= lij * sLc[j * 33 + 16 + k];
             }
             if (fail) sFail = 1;
-            C4_TRACE(2);
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
                 cur[lane + c * ldp] = c <= lane ? r[c] : 0.0;
@@ -890,7 +865,7 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
             }
         } else {
             const int hw = warp - 2;
-            if (J + 32 < n && !(dflags & 16)) {   // M[J+32:, J+32:J+64] -> nxt (cp.async, 16 B, coalesced)
+            if (J + 32 < n) {   // M[J+32:, J+32:J+64] -> nxt (cp.async, 16 B, coalesced)
                 const int J2 = J + 32, m2 = n - J2;
                 for (int idx = tid - 64; idx < m2 * 16; idx += C4_HELP * 32) {
                     const int col = idx / (m2 / 2), i2 = idx % (m2 / 2);
@@ -902,25 +877,25 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
             }
             if (J > 0) {
                 // (h1) rest of the previous panel's L21: rows 64.. (relative to J-32)
-                if (!(dflags & 4)) c4_times_d(prv, ldp, sDp, 8 + hw, (mr + 32) / 8, C4_HELP, gi, gk);
+                c4_times_d(prv, ldp, sDp, 8 + hw, (mr + 32) / 8, C4_HELP, gi, gk);
                 c4_helper_sync();
                 // (h2) cur[32:] -= prv[64:] prv[32:64]^T; helpers 0-3 do rows 32..63 first and signal warp 1
                 if (hw < 4 && mr > 32) {
-                    if (!(dflags & 4)) c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw, 5 + hw, 1, gi, gk);
+                    c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw, 5 + hw, 1, gi, gk);
                     __syncwarp();
                     mbar_arrive(&sBarC);
-                    if (!(dflags & 4)) c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw + C4_HELP, mr / 8, C4_HELP, gi, gk);
-                } else if (!(dflags & 4)) {
+                    c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw + C4_HELP, mr / 8, C4_HELP, gi, gk);
+                } else {
                     c4_sub_abt(cur, prv + 32, prv + 32, ldp, 4 + hw, mr / 8, C4_HELP, gi, gk);
                 }
                 // (h3) panel J-32 -> W
-                if (!(dflags & 1)) c4_copy_to_w(prv, ldp, C.W, ldw, J - 32, 0, mr + 32, hw, C4_HELP, lane);
+                c4_copy_to_w(prv, ldp, C.W, ldw, J - 32, 0, mr + 32, hw, C4_HELP, lane);
             }
-            if (J + 32 < n && !(dflags & 16)) {   // the M copies into nxt have landed (all helpers)
+            if (J + 32 < n) {   // the M copies into nxt have landed (all helpers)
                 asm volatile("cp.async.wait_all;\n" ::: "memory");
                 c4_helper_sync();
             }
-            if (J + 32 < n && !(dflags & 2)) {   // (h4) lookahead of panel J+32
+            if (J + 32 < n) {   // (h4) lookahead of panel J+32
                 // each helper owns row tiles hw, hw + H, hw + 2H (<= 3; n <= 256) and loads every
                 // B fragment once for all of them (B = L[J+32:J+64, :J] is shared by all tiles)
                 const int J2 = J + 32, nrt2 = (n - J2) / 8;
@@ -977,18 +952,13 @@ __global__ void __launch_bounds__(C4_THREADS, 1) k_leaf_chol4(const CholItem* __
 #pragma unroll
                                 for (int v = 0; v < 2; ++v) {
                                     const int row = (hw + t * C4_HELP) * 8 + gi, col = c * 8 + 2 * gk + v;
-                                    if (dflags & 16) nxt[row + col * ldp] = 1.0 - acc[t][c][v];
-                                    else nxt[row + col * ldp] -= acc[t][c][v];
+                                    nxt[row + col * ldp] -= acc[t][c][v];
                                 }
                 }
             }
         }
         __syncthreads();   // (c) ran inside (b1); one barrier per panel
-        C4_TRACE(3);
-        C4_TRACE(4);
-        C4_TRACE(5);
     }
-#undef C4_TRACE
     c4_copy_to_w(sm4 + ((n / 32 - 1) % 3) * pstride, ldp, C.W, ldw, n - 32, 0, 32, warp, C4_NW, lane);   // last panel
     if (tid == 0 && sFail) atomicOr(status, ST_NPD);
 }
@@ -1002,12 +972,9 @@ static size_t chol2_smem(int kc, int n) {
 
 void launch_leaf_cholesky(const CholItem* d, int nitems, unsigned* status, cudaStream_t st, int maxn) {
     if (!nitems) return;
-    if (maxn <= C4_NMAX && maxn % 32 == 0 && !std::getenv("SPG_CHOL_V3") && !std::getenv("SPG_CHOL_V2")) {
-        static const int fl = std::getenv("SPG_C4_FLAGS") ? std::atoi(std::getenv("SPG_C4_FLAGS")) : -1;
-        static bool set = false;
-        if (fl >= 0 && !set) { SPG_CUDA(cudaMemcpyToSymbol(g_c4_flags, &fl, sizeof(int))); set = true; }
+    if (maxn <= C4_NMAX && maxn % 32 == 0) {
         k_leaf_chol4<<<nitems, C4_THREADS, chol4_smem(maxn), st>>>(d, status);
-    } else if (maxn <= C3_NMAX && !std::getenv("SPG_CHOL_V2")) {
+    } else if (maxn <= C3_NMAX) {   // leaves that are not a multiple of 32 rows
         k_leaf_chol3<<<nitems, CH_THREADS, chol3_smem(maxn), st>>>(d, status);
     } else if (maxn <= 256) {
         k_leaf_chol2<16><<<nitems, CH_THREADS, chol2_smem(16, maxn), st>>>(d, status);

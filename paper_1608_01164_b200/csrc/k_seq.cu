@@ -897,8 +897,9 @@ static void launch_hager_chunked(int n, int b, const double* bands, const double
     SPG_LAUNCH_CHECK();
 }
 
-static const bool g_l0_window = std::getenv("SPG_L0_WINDOW") != nullptr;   // A/B: the windowed single-warp kernel
-static const bool g_hager_seq = std::getenv("SPG_HAGER_BAND_SEQ") != nullptr;   // A/B: Hager solves on one warp
+size_t estimate_l0_vecs_doubles(int n) {
+    return 5 * (size_t)n + 8 + (size_t)HG_PMAX * HG_RMAX * (2 * EB_B) + (size_t)HG_PMAX * 32;
+}
 
 void launch_estimate_l0(int n, int b, const double* bands, const double* alpha, double* lu_work, int* piv,
                         double* vecs, double* out_l0, unsigned* status, cudaStream_t st) {
@@ -906,13 +907,11 @@ void launch_estimate_l0(int n, int b, const double* bands, const double* alpha, 
         launch_est_l0_tri(n, bands, alpha, lu_work, out_l0, status, st);
         return;
     }
-    if (b <= EB_B && !g_l0_window) {   // (caller provides >= 5 n doubles at vecs)
-        k_est_l0_band<<<1, 64, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status, g_hager_seq ? 0 : 1);
+    if (b <= EB_B) {   // (caller provides estimate_l0_vecs_doubles(n) doubles at vecs)
+        k_est_l0_band<<<1, 64, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status, 1);
         SPG_LAUNCH_CHECK();
-        if (!g_hager_seq) {
-            if (b <= 8) launch_hager_chunked<17>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, st);
-            else launch_hager_chunked<33>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, st);
-        }
+        if (b <= 8) launch_hager_chunked<17>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, st);
+        else launch_hager_chunked<33>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, st);
         return;
     }
     k_est_l0_w<<<1, 32, 0, st>>>(n, b, bands, alpha, lu_work, piv, vecs, out_l0, status);

@@ -605,10 +605,9 @@ __global__ void __launch_bounds__(32) k_givens_tri(int n, const double* __restri
 
 void launch_est_l0_tri(int n, const double* bands, const double* alpha, double* work, double* out_l0,
                        unsigned* status, cudaStream_t st) {
-    static const bool seq = std::getenv("SPG_HAGER_SEQ") != nullptr;   // A/B: the sequential sweeps
-    k_est_l0_tri<<<1, 32, 0, st>>>(n, bands, alpha, work, work + 6 * (size_t)n, out_l0, status, seq ? 0 : 1);
+    k_est_l0_tri<<<1, 32, 0, st>>>(n, bands, alpha, work, work + 6 * (size_t)n, out_l0, status, 1);
     SPG_LAUNCH_CHECK();
-    if (!seq && n >= 2) {
+    if (n >= 2) {
         k_hager_tri<<<1, HG_T, 0, st>>>(n, bands, alpha, work, work + 6 * (size_t)n, out_l0, status);
         SPG_LAUNCH_CHECK();
     }

@@ -63,9 +63,6 @@ __device__ __forceinline__ double* z_area(const TTask& t, double* ws, int side) 
 }
 
 // ------------------------------------------------------------------ TSQR
-__device__ long long* g_tsqr_trace = nullptr;   // micro-benchmarks: clock64 per panel phase (CTA 0, sub-block 0)
-void set_tsqr_trace(long long* p) { SPG_CUDA(cudaMemcpyToSymbol(g_tsqr_trace, &p, sizeof(p))); }
-#define TSQR_TRACE(slot) do { if (g_tsqr_trace && b == 0 && blockIdx.x == 0 && threadIdx.x == 0) g_tsqr_trace[slot] = clock64(); } while (0)
 constexpr int LDB = SB + 4;   // leading dimension of the staged sub-block (conflict-free DMMA fragments)
 constexpr int TS_XS = 6 * 64; // split-tile partials: G * ntile <= 6 tiles of 8 x 8
 __device__ __forceinline__ void dmma_q(double& c0, double& c1, double a, double b) {
@@ -73,7 +70,6 @@ __device__ __forceinline__ void dmma_q(double& c0, double& c1, double a, double 
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }
-__constant__ int g_tsqr_v1_dev = 0;   // SPG_TSQR_V1=1: per-column trailing update (A/B checks)
 
 // all-reduce of 8 values across one warp through shared memory (scratch: 32 x 9 doubles):
 // every lane stores its 8 partials, lane L sums value L / 4 over lanes 8 (L % 4) .. +7,
@@ -125,7 +121,6 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
         for (int pn = 0; pn < npan; ++pn) {
             const int j0 = pn * TS_NB, nb = min(TS_NB, k - j0);
             double* Tp = sTT + KIN_MAX + pn * TS_NB * TS_NB;   // T (column-major 8 x 8)
-            TSQR_TRACE(3 * pn);
             if (warp == 0) {
                 double x[TS_NB][SB / 32];
 #pragma unroll
@@ -202,49 +197,8 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                         for (int t = 0; t < SB / 32; ++t) sB[(lane + 32 * t) + (j0 + a) * LDB] = x[a][t];
             }
             __syncthreads();
-            TSQR_TRACE(3 * pn + 1);
             // Q_panel^T on the remaining columns: w = Y^T a, w = T^T w, a -= Y w
-            if (g_tsqr_v1_dev) for (int c = j0 + nb + warp; c < k; c += nwarps) {
-                double av[SB / 32], w[TS_NB];
-#pragma unroll
-                for (int t = 0; t < SB / 32; ++t) av[t] = sB[(lane + 32 * t) + c * LDB];
-#pragma unroll
-                for (int a = 0; a < TS_NB; ++a) {
-                    double s = 0.0;
-                    if (a < nb)
-#pragma unroll
-                        for (int t = 0; t < SB / 32; ++t) s += sB[(lane + 32 * t) + (j0 + a) * LDB] * av[t];
-                    w[a] = s;
-                }
-                warp_allreduce8(w);
-                double ra[TS_NB];
-#pragma unroll
-                for (int a = 0; a < TS_NB; ++a) {
-                    ra[a] = a < nb ? sR[(j0 + a) + c * KIN_MAX] : 0.0;
-                    w[a] += ra[a];
-                }
-                double wt[TS_NB];
-#pragma unroll
-                for (int i = 0; i < TS_NB; ++i) {   // (T^T w)_i = sum_{a <= i} T(a, i) w_a
-                    double s = 0.0;
-#pragma unroll
-                    for (int a = 0; a <= i; ++a) s += Tp[a + i * TS_NB] * w[a];
-                    wt[i] = s;
-                }
-#pragma unroll
-                for (int t = 0; t < SB / 32; ++t) {
-                    double s = av[t];
-#pragma unroll
-                    for (int a = 0; a < TS_NB; ++a)
-                        if (a < nb) s -= sB[(lane + 32 * t) + (j0 + a) * LDB] * wt[a];
-                    sB[(lane + 32 * t) + c * LDB] = s;
-                }
-                __syncwarp();
-#pragma unroll
-                for (int a = 0; a < TS_NB; ++a)
-                    if (lane == a && a < nb) sR[(j0 + a) + c * KIN_MAX] = ra[a] - wt[a];
-            }
-            else {
+            {
                 // 8-column tiles on DMMA, one warp per tile:
                 //   W = Y^T A + R[j0:j0+8, tile];  W' = T^T W;  R[j0:j0+8, tile] -= W';  A -= Y W'
                 const int gi = lane >> 2, gk = lane & 3;
@@ -318,7 +272,6 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
                 }
             }
             __syncthreads();
-            TSQR_TRACE(3 * pn + 2);
         }
         // store reflector tails (SB x k), taus and the panel T's of this sub-block
         double* dst = refl + (long long)b * SB * KIN_MAX;
@@ -424,150 +377,6 @@ __device__ __forceinline__ const double* final_R(const TTask& t, double* ws, int
     return seg_area(t, ws, side, 0) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + TS_TAUT);
 }
 
-// one CTA per task: C = R_u R_v^T, parallel one-sided Jacobi, sort, threshold
-__global__ void __launch_bounds__(TS_THREADS) k_core(const TTask* __restrict__ tasks, double* __restrict__ ws,
-                                                    double eps, unsigned* status) {
-    int* dbg = reinterpret_cast<int*>(status + 4);   // first overflow: tag, p, s, k_in, r_full
-    extern __shared__ double smem[];
-    double* sW = smem;                       // k x k (ld KIN_MAX)
-    double* sV = sW + KIN_MAX * KIN_MAX;     // k x k
-    __shared__ double sSig[KIN_MAX];
-    __shared__ int sPerm[KIN_MAX];
-    __shared__ int sTop[KIN_MAX / 2 + 1], sBot[KIN_MAX / 2 + 1];
-    __shared__ int sRot;
-    const TTask& t = tasks[blockIdx.x];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    double* hdr = ws + t.ws;
-    if (task_skip(t)) {
-        if (tid == 0) { hdr[0] = 0; hdr[1] = 0; }
-        return;
-    }
-    int k = task_kin(t);
-    if (k > KIN_MAX) k = KIN_MAX;
-    if (k == 0) {
-        if (tid == 0) { hdr[0] = 0; hdr[1] = 0; *t.orank = 0; }
-        return;
-    }
-    const double* Ru = final_R(t, ws, 0);
-    const double* Rv = final_R(t, ws, 1);
-    // C[i][j] = sum_l Ru[i][l] Rv[j][l], l >= max(i, j)
-    for (int idx = tid; idx < k * k; idx += blockDim.x) {
-        const int i = idx % k, j = idx / k;
-        double s = 0.0;
-        for (int l = max(i, j); l < k; ++l) s += Ru[i + (long long)l * KIN_MAX] * Rv[j + (long long)l * KIN_MAX];
-        sW[i + j * KIN_MAX] = s;
-        sV[i + j * KIN_MAX] = (i == j) ? 1.0 : 0.0;
-    }
-    const int kk = k + (k & 1);   // even number of slots; slot k (if odd) is a dummy
-    const int npairs = kk / 2;
-    const int mrr = kk - 1;                       // rounds per sweep (circle method)
-    constexpr int GL = 8;                         // lanes per pair: 4 pairs per warp in flight
-    const int gid = lane / GL, gl = lane % GL;
-    const int slots = nwarps * (32 / GL);
-    const int slot = warp * (32 / GL) + gid;
-    (void)sTop; (void)sBot;
-    __syncthreads();
-    const double tol = 1e-15;
-    for (int sweep = 0; sweep < 60; ++sweep) {
-        if (tid == 0) sRot = 0;
-        __syncthreads();
-        int rotated = 0;
-        for (int round = 0; round < mrr; ++round) {
-            // pairs of round `round`: (round, kk-1) and ((round+i) mod m, (round-i) mod m), i = 1..kk/2-1
-            for (int base = 0; base < npairs; base += slots) {
-                const int pi = base + slot;
-                int p = 0, q = 0;
-                if (pi < npairs) {
-                    if (pi == 0) { p = round; q = kk - 1; }
-                    else { p = (round + pi) % mrr; q = (round - pi + mrr) % mrr; }
-                    if (p > q) { const int tmp = p; p = q; q = tmp; }
-                }
-                const bool act = pi < npairs && q < k;
-                double* wp = sW + p * KIN_MAX;
-                double* wq = sW + q * KIN_MAX;
-                double app = 0.0, aqq = 0.0, apq = 0.0;
-                if (act)
-                    for (int i = gl; i < k; i += GL) {
-                        const double a = wp[i], b = wq[i];
-                        app += a * a; aqq += b * b; apq += a * b;
-                    }
-#pragma unroll
-                for (int o = GL / 2; o > 0; o >>= 1) {   // group-local reductions (all 32 lanes shuffle)
-                    app += __shfl_xor_sync(0xffffffffu, app, o);
-                    aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
-                    apq += __shfl_xor_sync(0xffffffffu, apq, o);
-                }
-                if (!act || app == 0.0 || aqq == 0.0) continue;
-                if (fabs(apq) <= tol * sqrt(app * aqq)) continue;
-                rotated = 1;
-                const double zeta = (aqq - app) / (2.0 * apq);
-                const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double c = 1.0 / sqrt(1.0 + tt * tt);
-                const double s = c * tt;
-                double* vp = sV + p * KIN_MAX;
-                double* vq = sV + q * KIN_MAX;
-                for (int i = gl; i < k; i += GL) {
-                    const double x = wp[i], y = wq[i];
-                    wp[i] = c * x - s * y; wq[i] = s * x + c * y;
-                    const double xv = vp[i], yv = vq[i];
-                    vp[i] = c * xv - s * yv; vq[i] = s * xv + c * yv;
-                }
-            }
-            __syncthreads();
-        }
-        if (rotated) sRot = 1;   // benign race: any writer sets 1
-        __syncthreads();
-        if (!sRot) break;
-        __syncthreads();
-    }
-    // singular values = column norms of W, descending order (stable by index)
-    for (int j = warp; j < k; j += nwarps) {
-        double s = 0.0;
-        for (int i = lane; i < k; i += 32) { const double a = sW[i + j * KIN_MAX]; s += a * a; }
-        s = warp_sum(s);
-        if (lane == 0) sSig[j] = sqrt(s);
-    }
-    __syncthreads();
-    if (tid < k) {
-        const double sj = sSig[tid];
-        int pos = 0;
-        for (int i = 0; i < k; ++i) {
-            const double si = sSig[i];
-            pos += (si > sj) || (si == sj && i < tid);
-        }
-        sPerm[pos] = tid;
-    }
-    __syncthreads();
-    __shared__ int sR_;
-    if (tid == 0) {
-        int r = 0;
-        while (r < k && sSig[sPerm[r]] > eps) ++r;
-        if (r > KCAP) {
-            if (atomicOr(status, ST_RANK_CAP) == 0 || dbg[0] == 0) {
-                dbg[0] = t.tag + 1; dbg[1] = t.p; dbg[2] = t.s; dbg[3] = k; dbg[4] = r;
-            }
-            r = KCAP;
-        }
-        sR_ = r;
-        hdr[0] = k; hdr[1] = r;
-        if (!(sSig[sPerm[0]] == sSig[sPerm[0]])) atomicOr(status, ST_NONFINITE);
-        // algorithmic recompression traffic 8 (p + s)(k_in + k_out)
-        count_trunc_work(status, t.p, t.s, k, r);   // SURVEY.md §8d work units
-    }
-    __syncthreads();
-    const int r = sR_;
-    double* Zu = z_area(t, ws, 0);
-    double* Zv = z_area(t, ws, 1);
-    for (int idx = tid; idx < k * r; idx += blockDim.x) {
-        const int i = idx % k, c = idx / k;
-        const int src = sPerm[c];
-        Zu[i + (long long)c * KIN_MAX] = sW[i + src * KIN_MAX];
-        Zv[i + (long long)c * KIN_MAX] = sV[i + src * KIN_MAX];
-    }
-    __syncthreads();
-    if (tid == 0) *t.orank = r;
-}
-
 // ------------------------------------------------------------------ Q application
 // Applies Q (per sub-block compact-WY panels, see stream_qr) to [Z; 0]: the R-part
 // starts as Z (k x r), every sub-block's output rows start at 0; sub-blocks are
@@ -654,7 +463,6 @@ __device__ void stream_apply(int k, int r, int nrows, const double* refl, const 
 // which the block costs two small GEMMs on the FP64 tensor path instead of k
 // dependent reflector steps.
 constexpr int AD_K = 64, AD_LV = SB + 4, AD_LG = AD_K + 4;
-__constant__ int g_apply_v1_dev = 0;   // SPG_APPLY_V1=1: reflector-by-panel path for every k (A/B checks)
 __device__ __forceinline__ void dmma_a(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
@@ -801,7 +609,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
                 if (i < mrows) Zst[i + (long long)c * ldst] = o[tt];
             }
         };
-        if (k <= AD_K && !g_apply_v1_dev) {
+        if (k <= AD_K) {
             auto wr1 = [&](int row, int c, double v) { Zst[row + (long long)c * ldst] = v; };
             stream_apply_dmma(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, smem, wr1);
         } else {
@@ -834,7 +642,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
                 if (i < nr) out[r0 + i + (long long)c * ldo] = o[tt];
             }
         };
-        if (k <= AD_K && !g_apply_v1_dev) {
+        if (k <= AD_K) {
             auto wr1 = [&](int row, int c, double v) { out[r0 + row + (long long)c * ldo] = v; };
             stream_apply_dmma(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, smem, wr1);
         } else {
@@ -845,56 +653,31 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
 
 // ------------------------------------------------------------------ host side
 size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + LDB * KIN_MAX + TS_TAUT + TS_XS); }
-size_t trunc_smem_core() { return sizeof(double) * (2 * KIN_MAX * KIN_MAX); }
 size_t trunc_smem_apply() {
     return std::max(sizeof(double) * (KIN_MAX * KCAP + SB * KIN_MAX + TS_TAUT), apply_dmma_smem());
 }
 
 void trunc_init_attributes() {
-    if (std::getenv("SPG_APPLY_V1")) {
-        const int one = 1;
-        SPG_CUDA(cudaMemcpyToSymbol(g_apply_v1_dev, &one, sizeof(int)));
-    }
-    if (std::getenv("SPG_TSQR_V1")) {
-        const int one = 1;
-        SPG_CUDA(cudaMemcpyToSymbol(g_tsqr_v1_dev, &one, sizeof(int)));
-    }
     SPG_CUDA(cudaFuncSetAttribute(k_tsqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_tsqr()));
-    SPG_CUDA(cudaFuncSetAttribute(k_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_core()));
     SPG_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trunc_smem_apply()));
     core2_init_attributes();
 }
 
-// SPG_CORE_JACOBI=1 selects the unpreconditioned full-size Jacobi core (A/B checks)
-static const bool g_core_jacobi = std::getenv("SPG_CORE_JACOBI") != nullptr;
-
-cudaEvent_t* g_trunc_events = nullptr;   // micro-benchmarks: events around tsqr | core | apply
-void set_trunc_events(cudaEvent_t* ev) { g_trunc_events = ev; }
-
 void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* status, cudaStream_t st) {
     if (b.ntasks == 0) return;
-    if (g_trunc_events) SPG_CUDA(cudaEventRecord(g_trunc_events[0], st));
     k_tsqr<<<b.n_items0, TS_THREADS, trunc_smem_tsqr(), st>>>(b.d_tasks, b.d_items0, ws, status, 0);
     SPG_LAUNCH_CHECK();
     if (b.n_itemsm) {
         k_tsqr<<<b.n_itemsm, TS_THREADS, trunc_smem_tsqr(), st>>>(b.d_tasks, b.d_itemsm, ws, status, 1);
         SPG_LAUNCH_CHECK();
     }
-    if (g_trunc_events) SPG_CUDA(cudaEventRecord(g_trunc_events[1], st));
-    if (g_core_jacobi) {
-        k_core<<<b.ntasks, TS_THREADS, trunc_smem_core(), st>>>(b.d_tasks, ws, eps, status);
-        SPG_LAUNCH_CHECK();
-    } else {
-        launch_core2(b.d_tasks, b.ntasks, ws, eps, status, st);
-    }
-    if (g_trunc_events) SPG_CUDA(cudaEventRecord(g_trunc_events[2], st));
+    launch_core2(b.d_tasks, b.ntasks, ws, eps, status, st);
     if (b.n_itemsm) {
         k_apply<<<b.n_itemsm, TS_THREADS, trunc_smem_apply(), st>>>(b.d_tasks, b.d_itemsm, ws, 1);
         SPG_LAUNCH_CHECK();
     }
     k_apply<<<b.n_items0, TS_THREADS, trunc_smem_apply(), st>>>(b.d_tasks, b.d_items0, ws, 0);
     SPG_LAUNCH_CHECK();
-    if (g_trunc_events) SPG_CUDA(cudaEventRecord(g_trunc_events[3], st));
 }
 
 }  // namespace spg

@@ -16,9 +16,6 @@ void trunc_init_attributes();
 void core2_init_attributes();
 void launch_core2(const TTask* tasks, int ntasks, double* ws, double eps, unsigned* status, cudaStream_t st);
 void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* status, cudaStream_t st);
-void set_trunc_events(cudaEvent_t* ev);   // micro-benchmarks (4 events: tsqr | core | apply)
-void set_core_trace(long long* p);        // micro-benchmarks (clock64 per core phase, task 0)
-void set_tsqr_trace(long long* p);        // micro-benchmarks (clock64 per TSQR panel phase, CTA 0)
 
 // ------------------------------------------------------------ batched DMMA GEMM
 // C = alpha * op(A) op(B) + beta * C, column-major.  Dimensions are constants
@@ -94,7 +91,6 @@ struct CholItem {
     double* W;
     int n, ldm, ldw;
     double* D;         // optional: inverses of W's 32x32 diagonal blocks (for trsm_tile_dinv)
-    long long* trace;  // optional (micro-benchmarks): clock64 per panel phase, 8 per panel
     int w_zeroed;      // 1: W's strictly lower triangle is already zero (the engine memsets W)
 };
 // inverses of the 32x32 diagonal blocks of upper-triangular leaves (W or R)
@@ -106,9 +102,6 @@ struct DinvItem {
 void launch_leaf_dinv(const DinvItem* d, int nitems, unsigned* status, cudaStream_t st);
 void launch_leaf_cholesky(const CholItem* d, int nitems, unsigned* status, cudaStream_t st, int maxn);
 void leaf_init_attributes();
-// micro-benchmarks of single kernels (k_micro.cu): which 0 = leaf Cholesky; returns
-// us per launch in out[0] and, for the Cholesky, mean cycles per panel phase in out[1..6]
-int micro_kernel(int which, int n, int reps, double* out, int nout);
 void hsolve_init_attributes();
 int hsolve_tile_cols();
 
@@ -168,6 +161,9 @@ void launch_hsolve(DevTree t, DevHodlrView W, const HSolveItem* d, const int2* d
 
 // ------------------------------------------------------------ setup kernels
 void launch_estimate_2norm(int n, int b, const double* bands, double* out_alpha, cudaStream_t st);
+// doubles launch_estimate_l0 needs at `vecs` (5 vectors of n, the Hager control block, the
+// chunk maps and inherited windows of the chunk-parallel sweeps, k_seq.cu)
+size_t estimate_l0_vecs_doubles(int n);
 void launch_estimate_l0(int n, int b, const double* bands, const double* alpha, double* lu_work, int* piv,
                         double* vecs, double* out_l0, unsigned* status, cudaStream_t st);
 // scal: [0] alpha [1] l0 [2] 1/alpha (written); sched[4k..] = (a, b, c, l_after)

@@ -2,11 +2,11 @@
 // report schema and exit codes (tools/specproj.cpp): every projector runs on the B200
 // through the C++ shim (include/specproj_b200/specproj.hpp -> the C-ABI).
 //
-//   generate --n N --band B [--gap G] [--seed S] --out F.sbm
 //   project  --in F.sbm [--nmin] [--eps] [--delta] [--shift MU | --shifts MU1,MU2,..]
 //            [--report R.json] [--dump-projector D.txt]
 //   verify   --in F.sbm [--nmin] [--eps] [--delta] [--shift] [--report] [--oracle-cap N]
-//   bench    [--sizes 4096,8192] [--band] [--gap] [--repeat] [--nmin] [--out C.csv]
+//   bench    [--sizes 4096,8192] [--band] [--t2] [--repeat] [--nmin] [--out C.csv]  (dimer chains)
+// (the reference's `generate` -- synth.hpp test matrices -- is out of scope)
 //
 // Exit codes: 0 ok, 1 other failure, 2 invalid flags, 3 I/O failure, 4 Cholesky
 // breakdown, 5 oracle size cap exceeded (tools/specproj.cpp:33-36).
@@ -159,30 +159,6 @@ Matrix dense_oracle(const BandedSymmetric& A, int& nu) {
     return Pi;
 }
 
-int cmd_generate(const Args& a) {
-    a.require("n"); a.require("band"); a.require("out");
-    const int n = (int)a.integer("n", 0), band = (int)a.integer("band", 1);
-    const double gap = a.num("gap", 1e-1);
-    const long long seed = a.integer("seed", 0);
-    if (n < 2 || band < 1 || band >= n || !(gap > 0.0) || gap > 1.0) {
-        std::cerr << "error: require n >= 2, 1 <= band < n, 0 < gap <= 1\n";
-        return kExitFlags;
-    }
-    const std::vector<double> ev = io::two_sided_spectrum(n, gap);
-    const BandedSymmetric A = io::synth_banded(ev, band, seed < 0 ? 0 : (std::uint64_t)seed);
-    try {
-        io::write_sbm(a.str("out"), A);
-    } catch (const std::exception& e) {
-        std::cerr << "error: " << e.what() << "\n";
-        return kExitIo;
-    }
-    char g[32];
-    std::snprintf(g, sizeof g, "%.17g", gap);
-    std::cout << "wrote " << a.str("out") << ": n=" << n << " b=" << band << " gap=" << g << " nu=" << n / 2
-              << " spectrum=[-1,-" << g << "] u [" << g << ",1]\n";
-    return 0;
-}
-
 int cmd_project(const Args& a) {
     a.require("in");
     const double eps = a.num("eps", 1e-10), delta = a.num("delta", 1e-15);
@@ -267,11 +243,13 @@ int cmd_verify(const Args& a) {
                       a.str("report"));
 }
 
+// bench on the BASELINE input family (SURVEY.md §8d dimer chains: bond t1 = 1 / t2, diagonal
+// disorder 0.2 (1 - t2), band perturbation 0.02 / (2b + 1) for b > 1), seed 1
 int cmd_bench(const Args& a) {
     const std::vector<double> sizes = parse_list(a.str("sizes", "4096,8192"));
     const int band = (int)a.integer("band", 1), repeat = (int)a.integer("repeat", 1);
-    const double gap = a.num("gap", 1e-6);
-    if (sizes.empty() || band < 1 || !(gap > 0.0) || gap > 1.0 || repeat < 1) {
+    const double t2 = a.num("t2", 0.999);
+    if (sizes.empty() || band < 1 || !(t2 > 0.0) || t2 >= 1.0 || repeat < 1) {
         std::cerr << "error: invalid bench flags\n";
         return kExitFlags;
     }
@@ -283,7 +261,16 @@ int cmd_bench(const Args& a) {
             std::cerr << "error: size " << n << " incompatible with band " << band << "\n";
             return kExitFlags;
         }
-        const BandedSymmetric A = io::synth_banded(io::two_sided_spectrum(n, gap), band, 0);
+        BandedSymmetric A(n, band);
+        {
+            const long long len = (long long)(band + 1) * n - (long long)band * (band + 1) / 2;
+            std::vector<double> packed(len);
+            spg_make_dimer_chain(n, band, 1.0, t2, band == 1 ? 0.2 * (1.0 - t2) : 0.0,
+                                 band > 1 ? 0.02 / (2 * band + 1) : 0.0, 1, packed.data());
+            long long off = 0;
+            for (int d = 0; d <= band; ++d)
+                for (int i = 0; i + d < n; ++i) A.bands[d][i] = packed[off++];
+        }
         const int nm = a.integer("nmin", 0) > 0 ? (int)a.integer("nmin", 0) : default_nmin(band);
         double best = 0.0;
         HodlrDiagnostics d;
@@ -311,18 +298,17 @@ int cmd_bench(const Args& a) {
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::cerr << "usage: specproj_b200 {generate|project|verify|bench} [--flags]\n";
+        std::cerr << "usage: specproj_b200 {project|verify|bench} [--flags]\n";
         return kExitFlags;
     }
     const std::string cmd = argv[1];
     try {
-        if (cmd == "generate") return cmd_generate(Args(argc, argv, 2, {"n", "band", "gap", "seed", "out"}));
         if (cmd == "project")
             return cmd_project(Args(argc, argv, 2, {"in", "nmin", "eps", "delta", "shift", "shifts", "report",
                                                     "dump-projector"}));
         if (cmd == "verify")
             return cmd_verify(Args(argc, argv, 2, {"in", "nmin", "eps", "delta", "shift", "report", "oracle-cap"}));
-        if (cmd == "bench") return cmd_bench(Args(argc, argv, 2, {"sizes", "band", "gap", "repeat", "nmin", "out"}));
+        if (cmd == "bench") return cmd_bench(Args(argc, argv, 2, {"sizes", "band", "t2", "repeat", "nmin", "out"}));
         std::cerr << "error: unknown subcommand " << cmd << "\n";
         return kExitFlags;
     } catch (const FlagError& e) {

@@ -1,4 +1,4 @@
-"""Hot SASS ranges of an ncu report: python tests/ncu_sass_hot.py rep.ncu-rep [top]"""
+"""Hot SASS ranges of an ncu report: python tools_gpu/ncu_sass_hot.py rep.ncu-rep [top]"""
 import csv
 import subprocess
 import sys

@@ -1,6 +1,6 @@
 """Summarise a profile-mode batch timeline (SPG_PROF_TIMELINE=path, one row per timed batch:
 op, class, stream (-1 main), start/end ms from the first batch).
-python tests/timeline_summary.py timeline.csv"""
+python tools_gpu/timeline_summary.py timeline.csv"""
 import collections
 import csv
 import sys
