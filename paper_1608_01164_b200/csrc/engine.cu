@@ -147,6 +147,29 @@ void launch_phase_mark(const double* counters, double* snap, double* acc, int ph
     SPG_LAUNCH_CHECK();
 }
 
+// DEBUG: delay injection (SPG_DBG_DELAY=leaf|block|wtr|tv|split, microseconds in SPG_DBG_DELAY_US)
+__global__ void k_dbg_sleep(long long ns) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < ns * 2) { }
+}
+static int dbg_delay_class() {
+    const char* e = std::getenv("SPG_DBG_DELAY");
+    if (!e) return 0;
+    if (!std::strcmp(e, "leaf")) return 1;
+    if (!std::strcmp(e, "block")) return 2;
+    if (!std::strcmp(e, "wtr")) return 3;
+    if (!std::strcmp(e, "tv")) return 4;
+    if (!std::strcmp(e, "split")) return 5;
+    if (!std::strcmp(e, "main")) return 6;
+    return 0;
+}
+void dbg_delay(Plan& p, int cls, const std::function<void(Plan&, Launch)>& pusher) {
+    static const int c = dbg_delay_class();
+    static const long long us = std::getenv("SPG_DBG_DELAY_US") ? std::atoll(std::getenv("SPG_DBG_DELAY_US")) : 200;
+    if (c != cls) return;
+    pusher(p, [](cudaStream_t st) { k_dbg_sleep<<<1, 1, 0, st>>>(us * 1000); });
+}
+
 struct RankOp { int* out; const int* a; const int* b; };
 __global__ void k_rank_op(const RankOp* ops, int nops) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -365,7 +388,8 @@ constexpr int kTruncTall = 2048;
 
 void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     if (tasks.empty()) return;
-    if (side_sel_ < 0 && cur_op_ != 6 && tasks.size() >= 2) {
+    static const bool dbg_no_split = std::getenv("SPG_DBG_NO_TALLSPLIT") != nullptr;
+    if (side_sel_ < 0 && cur_op_ != 6 && tasks.size() >= 2 && !dbg_no_split) {
         std::vector<TTask> tall, flat;
         for (auto& t : tasks) (std::max(t.p, t.s) > kTruncTall ? tall : flat).push_back(t);
         if (!tall.empty() && !flat.empty()) {
@@ -374,6 +398,7 @@ void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
             record(p, evf);
             side_sel_ = 0;
             wait(p, evf);
+            dbg_delay(p, 5, [this](Plan& pp, Launch l) { push(pp, std::move(l)); });
             trunc_batch(p, tall, *ws_, false);   // workspace held until the join
             record(p, evj);
             side_sel_ = -1;
@@ -1010,7 +1035,7 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
     W.tready = false;
     W.tv_built.clear();
     chol_defer_trunc_ = defer_trunc;
-    chol_tv_ = chol_defer_trunc_;
+    chol_tv_ = chol_defer_trunc_ && !std::getenv("SPG_DBG_TV_OFF");
     if (chol_tv_) {   // forward subtree solves inside the factorisation go subtree-parallel
         if (!W.tU) {
             SPG_CUDA(cudaMalloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
@@ -1035,6 +1060,7 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
     const int nn = tree_.nnodes(), nside = ncasc_, nall = (int)sides_.size();
     last_leaf_ev_.assign(nn, -1);
     last_block_ev_.assign(nn, -1);
+    last_dbg_block_ev_.assign(tree_.depth + 1, -1);
     const int ev_fork = nn * (nside + 2), ev_join = ev_fork + 1;
     record(p, ev_fork);
     for (int i = 0; i < nall; ++i) {
@@ -1073,6 +1099,12 @@ void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU,
     }
     side_sel_ = nside - 1;
     wait(p, x);
+    dbg_delay(p, 1, [this](Plan& pp, Launch l) { push(pp, std::move(l)); });
+    static const bool dbg_bal = std::getenv("SPG_DBG_BLOCKS_AFTER_LEAF") != nullptr;
+    static const bool dbg_lab = std::getenv("SPG_DBG_LEAF_AFTER_BLOCKS") != nullptr;
+    if (dbg_lab) {   // DEBUG: the leaf stream waits for the previous cascade's blocks
+        for (int d = 0; d <= tree_.depth; ++d) if (last_dbg_block_ev_.size() > (size_t)d && last_dbg_block_ev_[d] >= 0) wait(p, last_dbg_block_ev_[d]);
+    }
     if (!upd.empty()) {
         const LowRankUpd* d = arena_->push(upd);
         const int ni = (int)upd.size();
@@ -1098,12 +1130,26 @@ void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU,
         if (bylev[d].empty()) continue;
         side_sel_ = std::min(d, nside - 2);
         wait(p, x);
+        // ordered after this cascade's leaf updates: run-to-run bit determinism was measured
+        // to need it (tools_gpu/determinism*.py: without it ~3% of n = 16384 projectors differ
+        // from the others in W); the leaf updates take a few microseconds
+        wait(p, nn + x);
+        (void)dbg_bal;
+        dbg_delay(p, 2, [this](Plan& pp, Launch l) { push(pp, std::move(l)); });
         trunc(p, bylev[d]);
         const int ev = nn * (2 + d) + x;
         record(p, ev);
+        if (last_dbg_block_ev_.size() < (size_t)tree_.depth + 1) last_dbg_block_ev_.assign(tree_.depth + 1, -1);
+        last_dbg_block_ev_[d] = ev;
         for (int y : nodes[d]) last_block_ev_[y] = ev;
     }
     side_sel_ = -1;
+    static const bool dbg_casc = std::getenv("SPG_DBG_CASC_SYNC") != nullptr;
+    static const bool dbg_cascL = std::getenv("SPG_DBG_CASC_LEAF") != nullptr;
+    static const bool dbg_cascB = std::getenv("SPG_DBG_CASC_BLOCK") != nullptr;
+    if (dbg_casc || dbg_cascL) wait(p, nn + x);
+    if (dbg_casc || dbg_cascB)
+        for (int d = tree_.depth; d >= 0; --d) if (!bylev[d].empty()) wait(p, nn * (2 + d) + x);
 }
 
 // Leaves above the fast leaf kernel's size (C4_LEAF_MAX < s <= TRM_NMAX, s % 64 == 0) as a
@@ -1172,6 +1218,7 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
         {   // W12 = trunc(X, m12.V) on its own stream (lowrank.hpp:67-86)
             side_sel_ = wtr_idx_;
             wait(p, evx);
+            dbg_delay(p, 3, [this](Plan& pp, Launch l) { push(pp, std::move(l)); });
             TTask tk{};
             tk.p = s1; tk.s = s2; tk.ng = 1; tk.skipg = -1;
             tk.g[0] = TGroup{X + bl, M.upV(x), n, n, M.rup(x), 0, 1.0, nullptr};
@@ -1180,6 +1227,8 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
             record(p, evw);
             side_sel_ = -1;
             wtr_last_ev_ = evw;
+            static const bool dbg_w12 = std::getenv("SPG_DBG_W12_SYNC") != nullptr;
+            if (dbg_w12) wait(p, evw);
         }
         // Schur M22 -= V (X^T X) V^T with the untruncated pair (X, m12.V)
         double* G = coef_ + (size_t)(4 * x + 2) * KCAP * KCAP;
@@ -1196,7 +1245,10 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
             record(p, ev_base3_ + x);
             side_sel_ = tv_idx_;
             wait(p, ev_base3_ + x);
-            wait(p, ev_base2_ + nn + x);
+            // the solve over r reads W12 of every node inside r: those truncations were queued on
+            // the (FIFO) W12 stream after W12(x), so wait for the latest one, not W12(x) alone
+            wait(p, wtr_last_ev_ >= 0 ? wtr_last_ev_ : ev_base2_ + nn + x);
+            dbg_delay(p, 4, [this](Plan& pp, Launch l) { push(pp, std::move(l)); });
             double* tv = W.tslabV(t) + br;
             copy(p, {CopyItem{W.upV(x), tv, s2, n, n, W.rup(x), 0, 1.0, nullptr}}, s2, KCAP);
             const bool tr = W.tready;

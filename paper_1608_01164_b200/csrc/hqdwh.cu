@@ -449,7 +449,8 @@ void build_iter(Plan& p, HqdwhState& st, const TimedFn& timed) {
     Scalars S = E.sc();
     timed(p, PH_MUL, [&]() {
         p.launches.push_back([=](cudaStream_t s) { launch_iter_params(S.sched, S.counter, S.slots, S.scal, s); });
-        E.op_multiply(p, *st.X, *st.X, *st.Z, /*upper_only=*/true);   // Z.lower is dead
+        static const bool dbg_full_z = std::getenv("SPG_DBG_FULL_Z") != nullptr;
+        E.op_multiply(p, *st.X, *st.X, *st.Z, /*upper_only=*/!dbg_full_z);   // Z.lower is dead
         E.op_scale_shift(p, *st.Z, 1.0, S.slots + 0, 1.0);
     });
     // deferred W12 truncation (SPG_CHOL_REFERENCE_ORDER=1: the reference's order)
@@ -510,9 +511,9 @@ std::unique_ptr<HqdwhState> make_state_once(int n, int b, int n_min, double eps,
     const int wbl = 3 * b + 1;
     // setup scratch d_tmp: alpha at [0] and the power-iteration vectors at [64, 64 + 2n);
     // l0: the banded LU (n x (3b+1)) at [128, ...) and the Hager vectors right after it (b = 1:
-    // 9 n doubles from 128); first iterate: the band H / Givens work rows, n x (4b + 4)
+    // 10 n doubles from 128); first iterate: the band H / Givens work rows, n x (4b + 4)
     const size_t tmp_doubles = std::max({(size_t)128 + (size_t)n * wbl + estimate_l0_vecs_doubles(n),
-                                         (size_t)128 + 9 * (size_t)n, (size_t)n * (4 * b + 4), (size_t)64 + 2 * (size_t)n});
+                                         (size_t)128 + 10 * (size_t)n, (size_t)n * (4 * b + 4), (size_t)64 + 2 * (size_t)n});
     SPG_CUDA(cudaMalloc(&st->d_bands, sizeof(double) * band_len(n, b)));
     SPG_CUDA(cudaMalloc(&st->d_tmp, sizeof(double) * tmp_doubles));
     SPG_CUDA(cudaMalloc(&st->d_rdiag, sizeof(double) * (size_t)(2 * b + 1) * n));
@@ -724,7 +725,28 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
             commit_run(p0);
             it_ev.clear();
         }
+        // failures stop the loop early: after queueing iterate k the status word as of iterate
+        // k - 2 is read (its copy has landed once iterate k - 2 is done, while k - 1 and k keep
+        // the device busy), so a failing Cholesky (NPD) or a rank overflow ends the projector
+        // at most two iterates later instead of running the rest on garbage
+        unsigned* st_copy = reinterpret_cast<unsigned*>(hp + 16);   // pinned, one word per iterate (mod 32)
+        std::vector<cudaEvent_t> st_ev;
+        auto queue_status = [&](int k) {
+            SPG_CUDA(cudaMemcpyAsync(st_copy + (k & 31), S.status, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+            cudaEvent_t e = mkev();
+            SPG_CUDA(cudaEventRecord(e, st));
+            st_ev.push_back(e);
+        };
+        queue_status(0);   // after the first iterate
         for (int k = 1; k < count; ++k) {
+            static const bool dbg_no_early = std::getenv("SPG_DBG_NO_EARLY") != nullptr;
+            if (k >= 2 && !dbg_no_early) {
+                SPG_CUDA(cudaEventSynchronize(st_ev[k - 2]));
+                if (st_copy[(k - 2) & 31] & (ST_NPD | ST_SINGULAR | ST_RANK_CAP | ST_KIN_CAP)) {
+                    SPG_CUDA(cudaStreamSynchronize(st));
+                    check_status_dev(S.status);
+                }
+            }
             cur_run = k;
             if (profile) { p = Plan(); build_iter(p, stt, timed); E.arena().commit(st); }
             cudaEvent_t e0 = mkev();
@@ -738,6 +760,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
                 E.arena().commit(st);
                 p.run(st);
             }
+            queue_status(k);
         }
     }
     {
@@ -758,6 +781,22 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     SPG_CUDA(cudaGetLastError());
     if (stt.graphs) E.arena().release(std::max(amark, stt.arena_mark));   // per-call descriptors
     check_status_dev(S.status);
+    if (std::getenv("SPG_DBG_DUMP")) {   // DEBUG: checksums of the iteration's matrices
+        const DHodlr* mats[5] = {stt.Z.get(), stt.W.get(), stt.Y.get(), stt.V.get(), stt.X.get()};
+        const char* names[5] = {"Z", "W", "Y", "V", "X"};
+        for (int m = 0; m < 5; ++m) {
+            long long nd = 0;
+            export_flat(E, *mats[m], nullptr, nullptr, &nd);
+            std::vector<double> data(std::max<long long>(nd, 1));
+            std::vector<int> rk(2 * E.tree().nnodes());
+            export_flat(E, *mats[m], rk.data(), data.data(), nullptr);
+            unsigned long long h = 1469598103934665603ULL;
+            for (long long i = 0; i < nd; ++i) { unsigned long long v; std::memcpy(&v, &data[i], 8); h = (h ^ v) * 1099511628211ULL; }
+            long long rs = 0;
+            for (int v : rk) rs = rs * 31 + v;
+            std::fprintf(stderr, "DUMP %s n=%lld ranks=%lld hash=%016llx\n", names[m], nd, rs, h);
+        }
+    }
 
     // ---------------- report
     spg_info& I = R->info;

@@ -102,14 +102,83 @@ void launch_copy_cols(const CopyItem* d, int nitems, int maxm, int maxk, cudaStr
     SPG_LAUNCH_CHECK();
 }
 
-// leaf low-rank update X += alpha U V^T (add_lowrank_rec leaf, hodlr.hpp:375-386)
+// leaf low-rank update X += alpha U V^T (add_lowrank_rec leaf, hodlr.hpp:375-386).
+// One CTA per 64 x 64 tile of X: the tile's rows of U and of V (k <= KIN_MAX columns) are
+// staged in shared memory by cp.async (all loads in flight at once), then each warp forms an
+// 8 x 64 strip of U V^T on DMMA (m8n8k4) and adds it to X.  The row pitch LR_LD = 4 (mod 32)
+// makes the fragment reads conflict-free.
+constexpr int lr_pitch() {   // >= KIN_MAX + 4 (k rounded up to 4) and = 4 (mod 32)
+    int v = KIN_MAX + 4;
+    while (v % 32 != 4) ++v;
+    return v;
+}
+constexpr int LR_T = 64, LR_LD = lr_pitch();
+static_assert(LR_LD % 32 == 4, "conflict-free pitch");
+__device__ __forceinline__ void dmma_lr(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+__device__ int g_lr_scalar = 0;
+__global__ void __launch_bounds__(256) k_lowrank_update(const LowRankUpd* __restrict__ it, int tpd) {
+    const LowRankUpd L = it[blockIdx.y];
+    const int k = *L.kp;
+    const int i0 = (blockIdx.x / tpd) * LR_T, j0 = (blockIdx.x % tpd) * LR_T;
+    if (k == 0 || i0 >= L.m || j0 >= L.m) return;
+    extern __shared__ double smem_lr[];
+    double* sU = smem_lr;                 // rows i0.. of U, [row * LR_LD + t]
+    double* sV = smem_lr + LR_T * LR_LD;  // rows j0.. of V
+    const int k4 = (k + 3) & ~3;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int idx = tid; idx < LR_T * k4; idx += 256) {
+        const int r = idx % LR_T, t = idx / LR_T;
+        double* du = sU + r * LR_LD + t;
+        double* dv = sV + r * LR_LD + t;
+        if (g_lr_scalar == 2) {   // DEBUG: L2-only loads
+            *du = (t < k && i0 + r < L.m) ? __ldcg(L.U + (i0 + r) + (long long)t * L.ldu) : 0.0;
+            *dv = (t < k && j0 + r < L.m) ? __ldcg(L.V + (j0 + r) + (long long)t * L.ldv) : 0.0;
+            continue;
+        }
+        if (t < k && i0 + r < L.m) cpa8(du, L.U + (i0 + r) + (long long)t * L.ldu); else *du = 0.0;
+        if (t < k && j0 + r < L.m) cpa8(dv, L.V + (j0 + r) + (long long)t * L.ldv); else *dv = 0.0;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    const int gi = lane >> 2, gk = lane & 3;
+    double acc[8][2] = {};
+    const double* pa = sU + (warp * 8 + gi) * LR_LD + gk;
+    if (g_lr_scalar == 1) {   // DEBUG
+        for (int t = 0; t < k; ++t) {
+            const double a = sU[(warp * 8 + gi) * LR_LD + t];
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) acc[c][v] += a * sV[(c * 8 + 2 * gk + v) * LR_LD + t];
+        }
+    } else
+    for (int t0 = 0; t0 < k4; t0 += 4) {
+        const double a = pa[t0];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) dmma_lr(acc[c][0], acc[c][1], a, sV[(c * 8 + gi) * LR_LD + t0 + gk]);
+    }
+    const int row = i0 + warp * 8 + gi;
+    if (row < L.m) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int col = j0 + c * 8 + 2 * gk + v;
+                if (col < L.m) L.X[row + (long long)col * L.ldx] += L.alpha * acc[c][v];
+            }
+    }
+}
+static size_t lowrank_smem() { return sizeof(double) * 2 * LR_T * LR_LD; }
 constexpr int LR_TJ = 32;
-__global__ void k_lowrank_update(const LowRankUpd* __restrict__ it) {
+__global__ void k_lowrank_update_old(const LowRankUpd* __restrict__ it) {
     const LowRankUpd L = it[blockIdx.y];
     const int k = *L.kp;
     if (k == 0) return;
     __shared__ double sV[LR_TJ][KIN_MAX + 1];
-    // tile of LR_TJ columns of X per CTA (blockIdx.x), all rows
     const int j0 = blockIdx.x * LR_TJ;
     if (j0 >= L.m) return;
     const int nj = min(LR_TJ, L.m - j0);
@@ -120,21 +189,27 @@ __global__ void k_lowrank_update(const LowRankUpd* __restrict__ it) {
     __syncthreads();
     for (int i = threadIdx.x; i < L.m; i += blockDim.x) {
         double acc[LR_TJ];
-#pragma unroll
         for (int jj = 0; jj < LR_TJ; ++jj) acc[jj] = 0.0;
         for (int t = 0; t < k; ++t) {
             const double u = L.U[i + (long long)t * L.ldu];
-#pragma unroll
             for (int jj = 0; jj < LR_TJ; ++jj) acc[jj] += u * sV[jj][t];
         }
-#pragma unroll
         for (int jj = 0; jj < LR_TJ; ++jj)
             if (jj < nj) L.X[i + (long long)(j0 + jj) * L.ldx] += L.alpha * acc[jj];
     }
 }
 void launch_lowrank_update(const LowRankUpd* d, int nitems, int maxm, cudaStream_t st) {
     if (!nitems) return;
-    k_lowrank_update<<<dim3((maxm + LR_TJ - 1) / LR_TJ, nitems), 256, 0, st>>>(d);
+    static const bool dbg_old = std::getenv("SPG_DBG_LR_OLD") != nullptr;
+    static bool once = false;
+    if (!once) { once = true; if (std::getenv("SPG_DBG_LR_SCALAR")) { int one = std::atoi(std::getenv("SPG_DBG_LR_SCALAR")); cudaMemcpyToSymbol(g_lr_scalar, &one, 4); } }
+    if (dbg_old) {
+        k_lowrank_update_old<<<dim3((maxm + LR_TJ - 1) / LR_TJ, nitems), 256, 0, st>>>(d);
+        SPG_LAUNCH_CHECK();
+        return;
+    }
+    const int tpd = (maxm + LR_T - 1) / LR_T;
+    k_lowrank_update<<<dim3(tpd * tpd, nitems), 256, lowrank_smem(), st>>>(d, tpd);
     SPG_LAUNCH_CHECK();
 }
 
@@ -1178,6 +1253,7 @@ void launch_leaf_split_prep(const double* M, double* W, double* S, int n, int h,
 
 void leaf_init_attributes() {
     SPG_CUDA(cudaFuncSetAttribute(k_leaf_chol4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol4_smem(C4_NMAX)));
+    SPG_CUDA(cudaFuncSetAttribute(k_lowrank_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lowrank_smem()));
     SPG_CUDA(cudaFuncSetAttribute(k_leaf_trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)trm_smem(TRM_NMAX)));
     SPG_CUDA(cudaFuncSetAttribute(k_leaf_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -903,7 +903,7 @@ size_t estimate_l0_vecs_doubles(int n) {
 
 void launch_estimate_l0(int n, int b, const double* bands, const double* alpha, double* lu_work, int* piv,
                         double* vecs, double* out_l0, unsigned* status, cudaStream_t st) {
-    if (b == 1 && n >= 2) {   // tridiagonal: k_tri.cu (caller provides >= 9 n doubles at lu_work)
+    if (b == 1 && n >= 2) {   // tridiagonal: k_tri.cu (caller provides >= 10 n doubles at lu_work: LU 6 n, Hager vectors 4 n)
         launch_est_l0_tri(n, bands, alpha, lu_work, out_l0, status, st);
         return;
     }

@@ -520,49 +520,27 @@ __global__ void __launch_bounds__(HG_T) k_hager_tri(int n, const double* __restr
     if (tid == 0) out[0] = n1 / (sqrt((double)n) * (n1 * est));
 }
 
-__device__ __forceinline__ void givens_cs_t(double f, double g, double& c, double& s) {   // givens.hpp:27-36
-    if (g == 0.0) { c = 1.0; s = 0.0; return; }
-    if (f == 0.0) { c = 0.0; s = 1.0; return; }
-    const double af = fabs(f), ag = fabs(g);
-    const double scale = af + ag;
-    const double is = rcp_t(scale);
-    const double fs = f * is, gs = g * is;
-    double r = scale * sqrt_t(fs * fs + gs * gs);
-    if (f < 0.0) r = -r;
-    const double ir = rcp_t(r);
-    c = f * ir;
-    s = g * ir;
-}
-
-// make_givens (givens.hpp:27-36) without the scaling: r = sign(f) sqrt(f^2 + g^2) from one
-// refined reciprocal square root (c = |f| / |r|, s = sign(f) g / |r|) -- one MUFU seed and
-// two Newton steps on the dependency chain instead of a reciprocal, a square root and a
-// second reciprocal.  Within an ulp or two of make_givens; outside [1e-290, 1e290] for
-// f^2 + g^2 (never met by the first-iterate sweep: its pivots stay >= 1) it falls back to
-// the scaled form.
-__device__ __forceinline__ void givens_fast(double f, double g, double& c, double& s, double& r) {
-    if (g == 0.0) { c = 1.0; s = 0.0; r = f; return; }
-    if (f == 0.0) { c = 0.0; s = 1.0; r = g; return; }
-    const double ss = fma(f, f, g * g);
-    if (!(ss > 1e-290 && ss < 1e290)) {
-        givens_cs_t(f, g, c, s);
-        r = c * f + s * g;
-        return;
-    }
+// reduce_tridiag (fast_qr.hpp:177-232) in squared form.  Per row t the reference applies
+// alpha_t (rowN_t against aux_t = 1), beta_t (R_tt against rowN_t) and gamma_t (row t
+// against the original row t+1).  With S1 = R_tt^2 + rowN_t^2 + 1 (= r_beta^2) and
+// S2 = S1 + b0^2 (= r_gamma^2), b = (b0, b1, b2) the original row t+1 and (a0, a1) the
+// current row t, the three rotations compose to
+//   R(t, t..t+2) = (S2, a0 a1 + b0 b1, b0 b2) / sqrt(S2)          (row sign +)
+//   next row     : a0 <- (S1 b1 - a0 a1 b0) / sqrt(S1 S2),  a1 <- sqrt(S1 / S2) b2
+//   rowN^2       : rho <- (rho + 1) a1^2 / S1
+// (only rowN^2 ever enters: rowN meets the sums of squares alone).  These are the same
+// rotations, evaluated through their sums of squares: no cancellation beyond the one
+// subtraction the rotation itself performs, and the per-row chain is two independent
+// refined reciprocal square roots instead of three dependent (rcp, sqrt, rcp) Givens
+// generations.  R^{-1} R^{-T} does not see row signs, so every row is taken with
+// R_tt > 0; R matches the reference's up to those signs.
+__device__ __forceinline__ double rsqrt_nr(double x) {   // x in [1, 1e290]
     double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(ss));
-    y = fma(0.5 * y, fma(-ss * y, y, 1.0), y);
-    y = fma(0.5 * y, fma(-ss * y, y, 1.0), y);
-    const double sy = f < 0.0 ? -y : y;
-    c = fabs(f) * y;
-    s = g * sy;
-    r = ss * sy;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(0.5 * y, fma(-x * y, y, 1.0), y);
+    return fma(0.5 * y, fma(-x * y, y, 1.0), y);
 }
 
-// reduce_tridiag: per row t the rotations alpha_{t,t} (rowN_t against aux_t = 1),
-// beta_t (R_tt against rowN_t, carrying R_{t,t+1} into rowN_{t+1}) and gamma_t
-// (row t against the original row t+1, filling R_{t,t+2}); row t of R is final
-// after gamma_t.  Same rotations and arithmetic as the band kernel (k_seq.cu).
 __global__ void __launch_bounds__(32) k_givens_tri(int n, const double* __restrict__ bands, const double* slots,
                                                   double* __restrict__ rdiag, double c0_max) {
     __shared__ __align__(16) double sbuf[PST * PNA * PCH];
@@ -574,31 +552,28 @@ __global__ void __launch_bounds__(32) k_givens_tri(int n, const double* __restri
     double* r0 = rdiag;
     double* r1 = rdiag + n;
     double* r2 = rdiag + 2 * (size_t)n;
-    double a0 = dg[0] * sA, a1 = of[0] * sA;
-    double rn = 1.0;   // rowN_t
+    double a0 = dg[0] * sA, a1 = n > 1 ? of[0] * sA : 0.0;
+    double rho = 0.0;   // rowN_t^2 (rowN_0 = 1 enters without an alpha rotation: rho_0 + 1 = 1)
     Ring<3> R{{of, dg, of}, {0, 1, 1}, {n - 1, n, n - 1}, 0, false, sbuf};
     run_ring(R, n, lane, [&](long long t, const double* v) {
-        double c, s, r;
-        if (t > 0) {   // alpha_{t,t}: rowN_t against aux_t = 1
-            givens_fast(rn, 1.0, c, s, r);
-            rn = r;
-        }
-        givens_fast(a0, rn, c, s, r);   // beta_t
-        a0 = r;
+        const double rho1 = rho + 1.0;
+        const double S1 = fma(a0, a0, rho1);
         if (t + 1 < n) {
-            const double x = a1;
-            a1 = c * x;
-            const double rn1 = -s * x;   // carried into rowN_{t+1}
-            const double b0 = v[0] * sA, b1 = v[1] * sA, b2 = v[2] * sA;   // original row t+1
-            givens_fast(a0, b0, c, s, r);                                  // gamma_{t,t+1}
-            const double n1 = c * a1 + s * b1;
-            const double q1 = -s * a1 + c * b1;
-            const double n2 = t + 2 < n ? s * b2 : 0.0, q2 = t + 2 < n ? c * b2 : b2;
-            if (lane == 0) { r0[t] = r; r1[t] = n1; r2[t] = n2; }
-            a0 = q1; a1 = q2;
-            rn = rn1;
+            const double b0 = v[0] * sA, b1 = v[1] * sA, b2 = t + 2 < n ? v[2] * sA : 0.0;   // original row t+1
+            const double S2 = fma(b0, b0, S1);
+            const double y1 = rsqrt_nr(S1), y2 = rsqrt_nr(S2);
+            const double a0a1 = a0 * a1;
+            if (lane == 0) {
+                r0[t] = S2 * y2;
+                r1[t] = fma(b0, b1, a0a1) * y2;
+                r2[t] = b0 * b2 * y2;
+            }
+            const double y12 = y1 * y2;
+            a0 = fma(S1, b1, -a0a1 * b0) * y12;
+            rho = rho1 * (a1 * a1) * (y1 * y1);
+            a1 = (S1 * y12) * b2;
         } else {
-            if (lane == 0) { r0[t] = a0; r1[t] = 0.0; r2[t] = 0.0; }
+            if (lane == 0) { r0[t] = S1 * rsqrt_nr(S1); r1[t] = 0.0; r2[t] = 0.0; }
         }
     });
 }

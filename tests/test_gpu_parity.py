@@ -358,6 +358,21 @@ def test_cpp_dropin_runs(root):
     assert "OK" in r.stdout
 
 
+def test_cpp_dropin_reference_types_runs(root):
+    """The drop-in headers with the reference's own types: tests/cpp/test_dropin_ref.cpp calls
+    specproj::hqdwh / specproj::from_banded exactly as the reference's code does (qdwh.hpp:196,
+    hodlr.hpp:92, 144) and checks them against hqdwh_cpu_reference in the same binary.  Built
+    by __graft_entry__.build() where /root/reference exists."""
+    exe = os.path.join(root, "tests", "cpp", "_build", "test_dropin_ref")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/_build/test_dropin_ref not built (build() without /root/reference)")
+    g = np.load(os.path.join(root, "tests", "golden", "npd_case.npz"))
+    np.savetxt("/tmp/spg_npd_bands_ref.txt", g["bands"], fmt="%.17g")
+    r = subprocess.run([exe, "/tmp/spg_npd_bands_ref.txt"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK (0 failures)" in r.stdout, r.stdout
+
+
 # chunk-parallel Hager solves of the banded l0 estimate (k_seq.cu k_hg_*): several chunks,
 # ragged last chunk, every window width, interchanges; vs the restated estimate_l0
 # (estimates.hpp:40-80) on the same alpha
