@@ -147,7 +147,10 @@ void launch_phase_mark(const double* counters, double* snap, double* acc, int ph
     SPG_LAUNCH_CHECK();
 }
 
-// DEBUG: delay injection (SPG_DBG_DELAY=leaf|block|wtr|tv|split, microseconds in SPG_DBG_DELAY_US)
+// Race diagnostics: SPG_DBG_DELAY=leaf|block|wtr|tv|split queues a spin kernel of
+// SPG_DBG_DELAY_US microseconds (default 200) at the head of every launch group of that side
+// stream.  Results must not change (tools_gpu/chol_race.py, determinism*.py); a missing
+// cross-stream dependency shows up as run-to-run differences.
 __global__ void k_dbg_sleep(long long ns) {
     const long long t0 = clock64();
     while (clock64() - t0 < ns * 2) { }
@@ -388,8 +391,7 @@ constexpr int kTruncTall = 2048;
 
 void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     if (tasks.empty()) return;
-    static const bool dbg_no_split = std::getenv("SPG_DBG_NO_TALLSPLIT") != nullptr;
-    if (side_sel_ < 0 && cur_op_ != 6 && tasks.size() >= 2 && !dbg_no_split) {
+    if (side_sel_ < 0 && cur_op_ != 6 && tasks.size() >= 2) {
         std::vector<TTask> tall, flat;
         for (auto& t : tasks) (std::max(t.p, t.s) > kTruncTall ? tall : flat).push_back(t);
         if (!tall.empty() && !flat.empty()) {
@@ -1035,7 +1037,7 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
     W.tready = false;
     W.tv_built.clear();
     chol_defer_trunc_ = defer_trunc;
-    chol_tv_ = chol_defer_trunc_ && !std::getenv("SPG_DBG_TV_OFF");
+    chol_tv_ = chol_defer_trunc_;
     if (chol_tv_) {   // forward subtree solves inside the factorisation go subtree-parallel
         if (!W.tU) {
             SPG_CUDA(cudaMalloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
@@ -1060,7 +1062,6 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
     const int nn = tree_.nnodes(), nside = ncasc_, nall = (int)sides_.size();
     last_leaf_ev_.assign(nn, -1);
     last_block_ev_.assign(nn, -1);
-    last_dbg_block_ev_.assign(tree_.depth + 1, -1);
     const int ev_fork = nn * (nside + 2), ev_join = ev_fork + 1;
     record(p, ev_fork);
     for (int i = 0; i < nall; ++i) {
@@ -1100,11 +1101,6 @@ void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU,
     side_sel_ = nside - 1;
     wait(p, x);
     dbg_delay(p, 1, [this](Plan& pp, Launch l) { push(pp, std::move(l)); });
-    static const bool dbg_bal = std::getenv("SPG_DBG_BLOCKS_AFTER_LEAF") != nullptr;
-    static const bool dbg_lab = std::getenv("SPG_DBG_LEAF_AFTER_BLOCKS") != nullptr;
-    if (dbg_lab) {   // DEBUG: the leaf stream waits for the previous cascade's blocks
-        for (int d = 0; d <= tree_.depth; ++d) if (last_dbg_block_ev_.size() > (size_t)d && last_dbg_block_ev_[d] >= 0) wait(p, last_dbg_block_ev_[d]);
-    }
     if (!upd.empty()) {
         const LowRankUpd* d = arena_->push(upd);
         const int ni = (int)upd.size();
@@ -1130,26 +1126,21 @@ void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU,
         if (bylev[d].empty()) continue;
         side_sel_ = std::min(d, nside - 2);
         wait(p, x);
-        // ordered after this cascade's leaf updates: run-to-run bit determinism was measured
-        // to need it (tools_gpu/determinism*.py: without it ~3% of n = 16384 projectors differ
-        // from the others in W); the leaf updates take a few microseconds
+        // Ordering of the block truncations: after this cascade's leaf updates and, in the
+        // deferred mode, after W12(x)'s truncation.  Without these edges ~4% of the n = 16384
+        // projectors came out different from the others (W12 of the tallest blocks first,
+        // up to 1e-6 in P; tools_gpu/determinism*.py, chol_race.py with injected delays); with
+        // them 0 of several hundred.  The block truncations are needed later than the leaf
+        // updates, so the leaf chain does not wait for them.
         wait(p, nn + x);
-        (void)dbg_bal;
+        if (chol_defer_trunc_) wait(p, ev_base2_ + nn + x);
         dbg_delay(p, 2, [this](Plan& pp, Launch l) { push(pp, std::move(l)); });
         trunc(p, bylev[d]);
         const int ev = nn * (2 + d) + x;
         record(p, ev);
-        if (last_dbg_block_ev_.size() < (size_t)tree_.depth + 1) last_dbg_block_ev_.assign(tree_.depth + 1, -1);
-        last_dbg_block_ev_[d] = ev;
         for (int y : nodes[d]) last_block_ev_[y] = ev;
     }
     side_sel_ = -1;
-    static const bool dbg_casc = std::getenv("SPG_DBG_CASC_SYNC") != nullptr;
-    static const bool dbg_cascL = std::getenv("SPG_DBG_CASC_LEAF") != nullptr;
-    static const bool dbg_cascB = std::getenv("SPG_DBG_CASC_BLOCK") != nullptr;
-    if (dbg_casc || dbg_cascL) wait(p, nn + x);
-    if (dbg_casc || dbg_cascB)
-        for (int d = tree_.depth; d >= 0; --d) if (!bylev[d].empty()) wait(p, nn * (2 + d) + x);
 }
 
 // Leaves above the fast leaf kernel's size (C4_LEAF_MAX < s <= TRM_NMAX, s % 64 == 0) as a
@@ -1203,7 +1194,9 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
         // X = W11^{-T} m12.U (the solve needs W11's own W12 blocks: wait for their truncations)
         double* X = xpanels_[t];
         copy(p, {CopyItem{M.upU(x), X + bl, s1, n, n, M.rup(x), 0, 1.0, nullptr}}, s1, KCAP);
-        if (wtr_last_ev_ >= 0 && !tree_.leaf(l)) wait(p, wtr_last_ev_);
+        // every W12 truncation queued so far has finished before the solve (also when l is a
+        // leaf, whose solve reads no W12: measured run-to-run determinism needs this order)
+        if (wtr_last_ev_ >= 0) wait(p, wtr_last_ev_);
         if (chol_tv_ && tree_.depth - tree_.level[l] >= kCholTvMin) {   // subtree-parallel: tV inside l built
             wait(p, ev_base3_ + tree_.nnodes() + l);
             hsolve(p, W, {HSolveItem{l, X + bl, n, M.rup(x), 0, 0}});
@@ -1227,8 +1220,6 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
             record(p, evw);
             side_sel_ = -1;
             wtr_last_ev_ = evw;
-            static const bool dbg_w12 = std::getenv("SPG_DBG_W12_SYNC") != nullptr;
-            if (dbg_w12) wait(p, evw);
         }
         // Schur M22 -= V (X^T X) V^T with the untruncated pair (X, m12.V)
         double* G = coef_ + (size_t)(4 * x + 2) * KCAP * KCAP;

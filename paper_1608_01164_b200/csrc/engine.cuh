@@ -236,7 +236,7 @@ private:
     std::vector<char> tv_need_;
     std::vector<double*> xpanels_;      // per-depth untruncated W11^{-T} M12.U panels
     double* leaf_scr_ = nullptr;        // Schur block of a split leaf Cholesky (main stream only)
-    std::vector<int> last_leaf_ev_, last_block_ev_, last_dbg_block_ev_;   // latest side-stream event touching a leaf / block
+    std::vector<int> last_leaf_ev_, last_block_ev_;   // latest side-stream event touching a leaf / block
     void cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU, const double* QV, const int* qrank);
     void leaf_chol_split(Plan& p, const double* Ml, double* Wl, double* D, int s);
     std::unique_ptr<Arena> arena_;

@@ -449,8 +449,7 @@ void build_iter(Plan& p, HqdwhState& st, const TimedFn& timed) {
     Scalars S = E.sc();
     timed(p, PH_MUL, [&]() {
         p.launches.push_back([=](cudaStream_t s) { launch_iter_params(S.sched, S.counter, S.slots, S.scal, s); });
-        static const bool dbg_full_z = std::getenv("SPG_DBG_FULL_Z") != nullptr;
-        E.op_multiply(p, *st.X, *st.X, *st.Z, /*upper_only=*/!dbg_full_z);   // Z.lower is dead
+        E.op_multiply(p, *st.X, *st.X, *st.Z, /*upper_only=*/true);   // Z.lower is dead
         E.op_scale_shift(p, *st.Z, 1.0, S.slots + 0, 1.0);
     });
     // deferred W12 truncation (SPG_CHOL_REFERENCE_ORDER=1: the reference's order)
@@ -739,8 +738,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         };
         queue_status(0);   // after the first iterate
         for (int k = 1; k < count; ++k) {
-            static const bool dbg_no_early = std::getenv("SPG_DBG_NO_EARLY") != nullptr;
-            if (k >= 2 && !dbg_no_early) {
+            if (k >= 2) {
                 SPG_CUDA(cudaEventSynchronize(st_ev[k - 2]));
                 if (st_copy[(k - 2) & 31] & (ST_NPD | ST_SINGULAR | ST_RANK_CAP | ST_KIN_CAP)) {
                     SPG_CUDA(cudaStreamSynchronize(st));
@@ -781,7 +779,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     SPG_CUDA(cudaGetLastError());
     if (stt.graphs) E.arena().release(std::max(amark, stt.arena_mark));   // per-call descriptors
     check_status_dev(S.status);
-    if (std::getenv("SPG_DBG_DUMP")) {   // DEBUG: checksums of the iteration's matrices
+    if (std::getenv("SPG_DBG_DUMP")) {   // diagnostics: bit checksums of the iterate's matrices (determinism checks)
         const DHodlr* mats[5] = {stt.Z.get(), stt.W.get(), stt.Y.get(), stt.V.get(), stt.X.get()};
         const char* names[5] = {"Z", "W", "Y", "V", "X"};
         for (int m = 0; m < 5; ++m) {

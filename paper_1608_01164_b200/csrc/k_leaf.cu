@@ -119,7 +119,6 @@ __device__ __forceinline__ void dmma_lr(double& d0, double& d1, double a, double
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
-__device__ int g_lr_scalar = 0;
 __global__ void __launch_bounds__(256) k_lowrank_update(const LowRankUpd* __restrict__ it, int tpd) {
     const LowRankUpd L = it[blockIdx.y];
     const int k = *L.kp;
@@ -134,11 +133,6 @@ __global__ void __launch_bounds__(256) k_lowrank_update(const LowRankUpd* __rest
         const int r = idx % LR_T, t = idx / LR_T;
         double* du = sU + r * LR_LD + t;
         double* dv = sV + r * LR_LD + t;
-        if (g_lr_scalar == 2) {   // DEBUG: L2-only loads
-            *du = (t < k && i0 + r < L.m) ? __ldcg(L.U + (i0 + r) + (long long)t * L.ldu) : 0.0;
-            *dv = (t < k && j0 + r < L.m) ? __ldcg(L.V + (j0 + r) + (long long)t * L.ldv) : 0.0;
-            continue;
-        }
         if (t < k && i0 + r < L.m) cpa8(du, L.U + (i0 + r) + (long long)t * L.ldu); else *du = 0.0;
         if (t < k && j0 + r < L.m) cpa8(dv, L.V + (j0 + r) + (long long)t * L.ldv); else *dv = 0.0;
     }
@@ -147,15 +141,6 @@ __global__ void __launch_bounds__(256) k_lowrank_update(const LowRankUpd* __rest
     const int gi = lane >> 2, gk = lane & 3;
     double acc[8][2] = {};
     const double* pa = sU + (warp * 8 + gi) * LR_LD + gk;
-    if (g_lr_scalar == 1) {   // DEBUG
-        for (int t = 0; t < k; ++t) {
-            const double a = sU[(warp * 8 + gi) * LR_LD + t];
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-#pragma unroll
-                for (int v = 0; v < 2; ++v) acc[c][v] += a * sV[(c * 8 + 2 * gk + v) * LR_LD + t];
-        }
-    } else
     for (int t0 = 0; t0 < k4; t0 += 4) {
         const double a = pa[t0];
 #pragma unroll
@@ -173,41 +158,8 @@ __global__ void __launch_bounds__(256) k_lowrank_update(const LowRankUpd* __rest
     }
 }
 static size_t lowrank_smem() { return sizeof(double) * 2 * LR_T * LR_LD; }
-constexpr int LR_TJ = 32;
-__global__ void k_lowrank_update_old(const LowRankUpd* __restrict__ it) {
-    const LowRankUpd L = it[blockIdx.y];
-    const int k = *L.kp;
-    if (k == 0) return;
-    __shared__ double sV[LR_TJ][KIN_MAX + 1];
-    const int j0 = blockIdx.x * LR_TJ;
-    if (j0 >= L.m) return;
-    const int nj = min(LR_TJ, L.m - j0);
-    for (int idx = threadIdx.x; idx < nj * k; idx += blockDim.x) {
-        const int jj = idx % nj, t = idx / nj;
-        sV[jj][t] = L.V[j0 + jj + (long long)t * L.ldv];
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < L.m; i += blockDim.x) {
-        double acc[LR_TJ];
-        for (int jj = 0; jj < LR_TJ; ++jj) acc[jj] = 0.0;
-        for (int t = 0; t < k; ++t) {
-            const double u = L.U[i + (long long)t * L.ldu];
-            for (int jj = 0; jj < LR_TJ; ++jj) acc[jj] += u * sV[jj][t];
-        }
-        for (int jj = 0; jj < LR_TJ; ++jj)
-            if (jj < nj) L.X[i + (long long)(j0 + jj) * L.ldx] += L.alpha * acc[jj];
-    }
-}
 void launch_lowrank_update(const LowRankUpd* d, int nitems, int maxm, cudaStream_t st) {
     if (!nitems) return;
-    static const bool dbg_old = std::getenv("SPG_DBG_LR_OLD") != nullptr;
-    static bool once = false;
-    if (!once) { once = true; if (std::getenv("SPG_DBG_LR_SCALAR")) { int one = std::atoi(std::getenv("SPG_DBG_LR_SCALAR")); cudaMemcpyToSymbol(g_lr_scalar, &one, 4); } }
-    if (dbg_old) {
-        k_lowrank_update_old<<<dim3((maxm + LR_TJ - 1) / LR_TJ, nitems), 256, 0, st>>>(d);
-        SPG_LAUNCH_CHECK();
-        return;
-    }
     const int tpd = (maxm + LR_T - 1) / LR_T;
     k_lowrank_update<<<dim3(tpd * tpd, nitems), 256, lowrank_smem(), st>>>(d, tpd);
     SPG_LAUNCH_CHECK();
