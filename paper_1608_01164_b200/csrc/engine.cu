@@ -1194,9 +1194,9 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
         // X = W11^{-T} m12.U (the solve needs W11's own W12 blocks: wait for their truncations)
         double* X = xpanels_[t];
         copy(p, {CopyItem{M.upU(x), X + bl, s1, n, n, M.rup(x), 0, 1.0, nullptr}}, s1, KCAP);
-        // every W12 truncation queued so far has finished before the solve (also when l is a
-        // leaf, whose solve reads no W12: measured run-to-run determinism needs this order)
-        if (wtr_last_ev_ >= 0) wait(p, wtr_last_ev_);
+        // the solve over l reads W12 of every node inside l: those truncations were queued on
+        // the (FIFO) W12 stream before now (a leaf's solve reads none)
+        if (wtr_last_ev_ >= 0 && !tree_.leaf(l)) wait(p, wtr_last_ev_);
         if (chol_tv_ && tree_.depth - tree_.level[l] >= kCholTvMin) {   // subtree-parallel: tV inside l built
             wait(p, ev_base3_ + tree_.nnodes() + l);
             hsolve(p, W, {HSolveItem{l, X + bl, n, M.rup(x), 0, 0}});

@@ -399,15 +399,21 @@ def test_stacked_qr_r_vs_reference_kat(golden_dir, name):
     n = int(name.split("_n")[1].split("_")[0])
     A = S.BandedSymmetric.from_packed(n, b, bands)
     Rref = g[name + "_R"].reshape(2 * b + 1, n)
-    Rg = S.stacked_qr_r(A, "givens")
     scale = np.abs(Rref).max()
-    assert np.abs(Rg - Rref).max() <= 1e-13 * scale
-    Rc = S.stacked_qr_r(A, "cholesky")
-    sgn = np.sign(Rref[0])                          # row signs of the Givens R
-    Rs = np.zeros_like(Rref)
-    for d in range(2 * b + 1):
-        Rs[d, :n - d] = Rref[d, :n - d] * sgn[:n - d]
-    assert np.abs(Rc - Rs).max() <= 1e-12 * scale
+    # rows compared with R_tt > 0 (R^{-1} R^{-T} does not see row signs; the b = 1 sweep
+    # returns positive rows, the banded sweep the reference's own signs)
+    Rs = _rows_positive(Rref)
+    assert np.abs(_rows_positive(S.stacked_qr_r(A, "givens")) - Rs).max() <= 1e-13 * scale
+    assert np.abs(_rows_positive(S.stacked_qr_r(A, "cholesky")) - Rs).max() <= 1e-12 * scale
+
+
+def _rows_positive(R):
+    n = R.shape[1]
+    out = R.copy()
+    sg = np.sign(R[0])
+    for d in range(R.shape[0]):
+        out[d, :n - d] *= sg[:n - d]
+    return out
 
 
 @pytest.mark.parametrize("n,b", [(3000, 1), (2000, 5), (1500, 16)])
@@ -415,8 +421,8 @@ def test_stacked_qr_r_vs_reference(reflib, n, b):
     A = S.dimer_chain(n, 1.0, 0.9, 0.01, 31 + b, b=b, s=0.02 / (2 * b + 1) if b > 1 else 0.0).scaled(300.0)
     rd = np.zeros((2 * b + 1) * n)
     reflib.L.ref_reduce(n, b, R._d(A.packed()), R._d(rd))
-    Rref = rd.reshape(2 * b + 1, n)
-    assert np.abs(S.stacked_qr_r(A, "givens") - Rref).max() <= 1e-12 * np.abs(Rref).max()
+    Rref = _rows_positive(rd.reshape(2 * b + 1, n))
+    assert np.abs(_rows_positive(S.stacked_qr_r(A, "givens")) - Rref).max() <= 1e-12 * np.abs(Rref).max()
 
 
 # (n, b, t2, n_min): c0 > 1e6 (Givens sweep: b = 1 and b = 3) and c0 < 1e6 (band Cholesky)
@@ -480,7 +486,12 @@ def test_baseline_config_vs_reference_probes(golden_dir, cfg):
     m = g["PrefOm"].shape[1]
     Om = np.random.default_rng(int(g["seed"])).standard_normal((n, int(g.get("ncols_generated", m))))[:, :m]
     E = r.apply(Om) - g["PrefOm"]
-    assert HALKO * np.linalg.norm(E, axis=0).max() <= 100 * eps
+    en = np.linalg.norm(E, axis=0)
+    # ||E||_2 <= 10 sqrt(2/pi) max_i ||E w_i|| (prob >= 1 - 10^-m), or, when E is spread over
+    # many comparable singular values (config 5: eps = 1e-8 truncations in every block), the
+    # Frobenius route ||E||_2 <= ||E||_F with ||E||_F^2 = E||E w||^2 estimated from the m probes
+    # (factor 2 margin: chi-square with >= m degrees of freedom)
+    assert min(HALKO * en.max(), 2.0 * np.sqrt(np.mean(en ** 2))) <= 100 * eps, (en.max(), np.sqrt(np.mean(en ** 2)))
     idem = power_norm(lambda x: r.apply(r.apply(x)) - r.apply(x), n, iters=30)
     assert idem <= 100 * eps
     r.close()
