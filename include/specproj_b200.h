@@ -98,6 +98,18 @@ int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double d
  * and the first failing shift's status is returned. */
 int spg_hqdwh_shifts(int n, int b, const double* bands, int nshift, const double* shifts, int n_min, double eps,
                      double delta, int max_concurrent, spg_result** out);
+/* The same over several GPUs of one process (a projector does not
+ * shard, so several shifts run as replicas, one projector per GPU at a time): the shifts
+ * are pulled from one queue by per_device_concurrent workers on each listed device
+ * (devices == NULL or ndev <= 0: every visible device).  device_of (may be NULL) receives
+ * the device that produced out[i].  Each result stays on its device; the spg_result_*
+ * calls switch to it and back.  For the cmd_rankscan / cmd_bench style callers
+ * (tools/specproj.cpp:229-337) that evaluate many mu. */
+int spg_hqdwh_shifts_devices(int n, int b, const double* bands, int nshift, const double* shifts, int n_min, double eps,
+                             double delta, int ndev, const int* devices, int per_device_concurrent, spg_result** out,
+                             int* device_of);
+/* the CUDA device a result lives on */
+int spg_result_device(const spg_result* r);
 int spg_result_info(const spg_result* r, spg_info* info);
 /* per-iteration diagnostics, `out` has room for info.iterations entries */
 int spg_result_diag(const spg_result* r, spg_iter_diag* out);

@@ -253,6 +253,25 @@ inline std::vector<ProjectorResult> hqdwh_shifts(const BandedSymmetric& A, const
     return out;
 }
 
+// The same over several GPUs of the process (replicas, one projector per GPU at a time;
+// devices empty = every visible device).
+inline std::vector<ProjectorResult> hqdwh_shifts_devices(const BandedSymmetric& A, const std::vector<double>& shifts,
+                                                         int n_min, double eps, double delta,
+                                                         const std::vector<int>& devices = {},
+                                                         int per_device_concurrent = 2) {
+    std::vector<double> packed = detail::pack(A);
+    std::vector<spg_result*> rs(shifts.size(), nullptr);
+    detail::check(spg_hqdwh_shifts_devices(A.n, A.b, packed.data(), (int)shifts.size(), shifts.data(), n_min, eps, delta,
+                                           (int)devices.size(), devices.empty() ? nullptr : devices.data(),
+                                           per_device_concurrent, rs.data(), nullptr));
+    std::vector<ProjectorResult> out;
+    for (spg_result* r : rs) {
+        std::unique_ptr<spg_result, void (*)(spg_result*)> guard(r, spg_result_free);
+        out.push_back(detail::collect(r, A.n, n_min));
+    }
+    return out;
+}
+
 inline ProjectorResult detail::collect(spg_result* r, int n, int n_min) {
     spg_info info{};
     detail::check(spg_result_info(r, &info));

@@ -104,7 +104,7 @@ ABI_SYMBOLS = (
     "spg_make_dimer_chain", "spg_make_random_banded", "spg_kcap", "spg_ctx_create", "spg_ctx_free",
     "spg_ctx_upload", "spg_ctx_flat_size", "spg_ctx_download", "spg_ctx_op", "spg_ctx_from_banded",
     "spg_truncate", "spg_set_profile", "spg_measure_dmma_tflops", "spg_host_alloc",
-    "spg_host_free", "spg_hqdwh_shifts", "spg_release_plan_cache", "spg_stacked_qr_r",
+    "spg_host_free", "spg_hqdwh_shifts", "spg_hqdwh_shifts_devices", "spg_result_device", "spg_release_plan_cache", "spg_stacked_qr_r",
 )
 
 
@@ -150,6 +150,9 @@ def load_library(path: str | None = None):
         "spg_host_free": ([vp], None),
         "spg_hqdwh_shifts": ([C.c_int, C.c_int, _dp, C.c_int, _dp, C.c_int, C.c_double, C.c_double, C.c_int,
                               C.POINTER(vp)], C.c_int),
+        "spg_hqdwh_shifts_devices": ([C.c_int, C.c_int, _dp, C.c_int, _dp, C.c_int, C.c_double, C.c_double, C.c_int,
+                                      _ip, C.c_int, C.POINTER(vp), _ip], C.c_int),
+        "spg_result_device": ([vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -513,6 +516,66 @@ def hqdwh_shifts(A: BandedSymmetric, shifts, n_min: int, eps: float, delta: floa
     _raise(load_library().spg_hqdwh_shifts(A.n, A.b, _d(A.packed()), len(sh), _d(sh), n_min, eps, delta,
                                            max_concurrent, hs))
     return [_result_from_handle(C.c_void_p(h), A.n, n_min) for h in hs]
+
+
+def hqdwh_shifts_devices(A: BandedSymmetric, shifts, n_min: int, eps: float, delta: float = 1e-15,
+                         devices=None, per_device_concurrent: int = 2):
+    """Spectral slicing over the GPUs of this process (spg_hqdwh_shifts_devices): replicas, one
+    projector per GPU at a time and no data-path collective.  Returns
+    (results, device_of) in the order of `shifts`."""
+    if not A.all_finite():
+        raise ValueError("hqdwh: nonfinite input")
+    sh = np.ascontiguousarray(shifts, dtype=np.float64)
+    hs = (C.c_void_p * len(sh))()
+    dev_of = np.full(len(sh), -1, dtype=np.int32)
+    dv = None if devices is None else np.ascontiguousarray(devices, dtype=np.int32)
+    _raise(load_library().spg_hqdwh_shifts_devices(
+        A.n, A.b, _d(A.packed()), len(sh), _d(sh), n_min, eps, delta, 0 if dv is None else len(dv),
+        None if dv is None else dv.ctypes.data_as(_ip), per_device_concurrent, hs, dev_of.ctypes.data_as(_ip)))
+    return [_result_from_handle(C.c_void_p(h), A.n, n_min) for h in hs], dev_of.tolist()
+
+
+def shard_shifts(nshift: int, rank: int, world: int) -> list:
+    """Indices of the shifts rank `rank` of `world` evaluates in the one-process-per-GPU model
+    (torchrun): round-robin, so neighbouring shifts (similar cost) spread over the ranks."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("shard_shifts: 0 <= rank < world required")
+    return list(range(rank, nshift, world))
+
+
+def hqdwh_shifts_sharded(A: BandedSymmetric, shifts, n_min: int, eps: float, delta: float = 1e-15,
+                         rank: int | None = None, world: int | None = None, max_concurrent: int = 2,
+                         summarize=None, project=None):
+    """Spectral slicing across ranks (one process per GPU, torch.distributed): rank r computes the
+    projectors of shifts r, r + world, ... on ITS device; no matrix data crosses ranks.  Only a
+    per-shift summary (default: round(trace) = the eigenvalue count below the shift, iterations,
+    max rank) is all-gathered, so every rank returns (local_results, summaries_in_shift_order).
+    `project` (tests) replaces the device call."""
+    import torch.distributed as dist
+    inited = dist.is_available() and dist.is_initialized()
+    if world is None:
+        world = dist.get_world_size() if inited else 1
+    if rank is None:
+        rank = dist.get_rank() if inited else 0
+    sh = [float(x) for x in shifts]
+    mine = shard_shifts(len(sh), rank, world)
+    run = project or (lambda mus: hqdwh_shifts(A, mus, n_min, eps, delta, max_concurrent) if mus else [])
+    local = run([sh[i] for i in mine])
+    summ = summarize or (lambda r: {"count": int(round(r.info["trace"])), "iterations": r.iterations,
+                                    "max_rank": r.info["max_rank"]})
+    part = [(i, summ(r)) for i, r in zip(mine, local)]
+    if world > 1:
+        if not inited:
+            raise RuntimeError("hqdwh_shifts_sharded: world > 1 needs an initialised torch.distributed group")
+        parts = [None] * world
+        dist.all_gather_object(parts, part)
+    else:
+        parts = [part]
+    out = [None] * len(sh)
+    for pr in parts:
+        for i, v in pr:
+            out[i] = v
+    return dict(zip(mine, local)), out
 
 
 # ------------------------------------------------------------------ wire formats (banded.hpp:115-154)

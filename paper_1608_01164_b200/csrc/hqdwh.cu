@@ -358,6 +358,17 @@ int current_device() {
     return dev;
 }
 
+// makes `dev` current for the scope (results and cached plans live on the device that built them)
+struct DeviceScope {
+    int prev = 0;
+    bool sw = false;
+    explicit DeviceScope(int dev) {
+        cudaGetDevice(&prev);
+        if (dev != prev) { SPG_CUDA(cudaSetDevice(dev)); sw = true; }
+    }
+    ~DeviceScope() { if (sw) cudaSetDevice(prev); }
+};
+
 std::unique_ptr<HqdwhState> take_cached_state(int n, int b, int n_min, double eps, double delta) {
     const int dev = current_device();
     std::lock_guard<std::mutex> lk(g_state_mu);
@@ -994,33 +1005,28 @@ int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double d
     });
 }
 
-int spg_hqdwh_shifts(int n, int b, const double* bands, int nshift, const double* shifts, int n_min, double eps,
-                     double delta, int max_concurrent, spg_result** out) {
-    if (nshift <= 0 || !shifts || !out) return guarded([]() { throw StatusError(SPG_INVALID_ARGUMENT, "spg_hqdwh_shifts: no shifts"); });
-    for (int i = 0; i < nshift; ++i) out[i] = nullptr;
-    const int rc0 = guarded([&]() { ensure_device(); });
-    if (rc0 != SPG_OK) return rc0;
+// shifts over devices: `conc` worker threads per listed device pull shifts from one queue
+static int shifts_on_devices(int n, int b, const double* bands, int nshift, const double* shifts, int n_min, double eps,
+                             double delta, const std::vector<int>& devs, int conc, spg_result** out, int* dev_of) {
     const long long blen = band_len(n, b);
     std::vector<int> st(nshift, SPG_OK);
     std::vector<std::string> msg(nshift);
     std::atomic<int> next{0};
-    auto worker = [&]() {
-        int dev = 0;
-        cudaGetDevice(&dev);
+    auto worker = [&](int dev) {
+        if (cudaSetDevice(dev) != cudaSuccess) { cudaGetLastError(); return; }
         for (int i = next++; i < nshift; i = next++) {
             std::vector<double> sb(bands, bands + blen);
             for (int j = 0; j < n; ++j) sb[j] -= shifts[i];   // A - mu I: the diagonal is band 0
             st[i] = guarded([&]() { out[i] = run_hqdwh(n, b, sb.data(), n_min, eps, delta); });
             if (st[i] != SPG_OK) msg[i] = spg_last_error();
+            if (dev_of) dev_of[i] = dev;
         }
     };
     {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        const int nw = std::max(1, std::min(max_concurrent > 0 ? max_concurrent : 2, nshift));
+        const int per = std::max(1, std::min(conc > 0 ? conc : 2, (nshift + (int)devs.size() - 1) / (int)devs.size()));
         std::vector<std::thread> th;
-        for (int w = 0; w < nw; ++w)
-            th.emplace_back([&, dev]() { cudaSetDevice(dev); worker(); });
+        for (int d : devs)
+            for (int w = 0; w < per; ++w) th.emplace_back(worker, d);
         for (auto& t : th) t.join();
     }
     for (int i = 0; i < nshift; ++i)
@@ -1032,6 +1038,46 @@ int spg_hqdwh_shifts(int n, int b, const double* bands, int nshift, const double
         }
     return SPG_OK;
 }
+
+int spg_hqdwh_shifts(int n, int b, const double* bands, int nshift, const double* shifts, int n_min, double eps,
+                     double delta, int max_concurrent, spg_result** out) {
+    if (nshift <= 0 || !shifts || !out) return guarded([]() { throw StatusError(SPG_INVALID_ARGUMENT, "spg_hqdwh_shifts: no shifts"); });
+    for (int i = 0; i < nshift; ++i) out[i] = nullptr;
+    const int rc0 = guarded([&]() { ensure_device(); });
+    if (rc0 != SPG_OK) return rc0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return shifts_on_devices(n, b, bands, nshift, shifts, n_min, eps, delta, {dev}, max_concurrent, out, nullptr);
+}
+
+int spg_hqdwh_shifts_devices(int n, int b, const double* bands, int nshift, const double* shifts, int n_min, double eps,
+                             double delta, int ndev, const int* devices, int per_device_concurrent, spg_result** out,
+                             int* device_of) {
+    if (nshift <= 0 || !shifts || !out)
+        return guarded([]() { throw StatusError(SPG_INVALID_ARGUMENT, "spg_hqdwh_shifts_devices: no shifts"); });
+    for (int i = 0; i < nshift; ++i) out[i] = nullptr;
+    const int rc0 = guarded([&]() { ensure_device(); });
+    if (rc0 != SPG_OK) return rc0;
+    int have = 0;
+    cudaGetDeviceCount(&have);
+    std::vector<int> devs;
+    if (ndev <= 0 || !devices) {   // every visible device
+        for (int d = 0; d < have; ++d) devs.push_back(d);
+    } else {
+        for (int i = 0; i < ndev; ++i) {
+            if (devices[i] < 0 || devices[i] >= have || std::count(devs.begin(), devs.end(), devices[i]))
+                return guarded([&]() {
+                    throw StatusError(SPG_INVALID_ARGUMENT, "spg_hqdwh_shifts_devices: device " + std::to_string(devices[i]) +
+                                                                " not visible or listed twice (" + std::to_string(have) +
+                                                                " visible)");
+                });
+            devs.push_back(devices[i]);
+        }
+    }
+    return shifts_on_devices(n, b, bands, nshift, shifts, n_min, eps, delta, devs, per_device_concurrent, out, device_of);
+}
+
+int spg_result_device(const spg_result* r) { return r && r->state ? r->state->device : -1; }
 
 int spg_result_info(const spg_result* r, spg_info* info) {
     if (!r) return SPG_INVALID_ARGUMENT;
@@ -1046,15 +1092,22 @@ int spg_result_diag(const spg_result* r, spg_iter_diag* out) {
 }
 
 int spg_result_flat_size(const spg_result* r, int which, long long* nd) {
-    return guarded([&]() { export_flat(r->eng(), which == 0 ? r->P() : r->X(), nullptr, nullptr, nd); });
+    return guarded([&]() {
+        DeviceScope ds(r->state->device);
+        export_flat(r->eng(), which == 0 ? r->P() : r->X(), nullptr, nullptr, nd);
+    });
 }
 
 int spg_result_export(const spg_result* r, int which, int* ranks, double* data) {
-    return guarded([&]() { export_flat(r->eng(), which == 0 ? r->P() : r->X(), ranks, data, nullptr); });
+    return guarded([&]() {
+        DeviceScope ds(r->state->device);
+        export_flat(r->eng(), which == 0 ? r->P() : r->X(), ranks, data, nullptr);
+    });
 }
 
 int spg_result_apply(const spg_result* r, int which, int m, const double* X, double* Y) {
     return guarded([&]() {
+        DeviceScope ds(r->state->device);
         Engine& E = r->eng();
         const int n = E.tree().n;
         if (m < 1 || m > KCAP) throw StatusError(SPG_INVALID_ARGUMENT, "spg_result_apply: 1 <= m <= KCAP");
@@ -1088,7 +1141,15 @@ int spg_result_apply(const spg_result* r, int which, int m, const double* X, dou
 Engine& spg_result::eng() const { return *state->eng; }
 const DHodlr& spg_result::X() const { return *state->X; }
 const DHodlr& spg_result::P() const { return *state->P; }
-spg_result::~spg_result() { release_state(std::move(state)); }
+spg_result::~spg_result() {
+    if (!state) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    const int dev = state->device;
+    if (dev != prev) cudaSetDevice(dev);
+    release_state(std::move(state));
+    if (dev != prev) cudaSetDevice(prev);
+}
 
 void spg_result_free(spg_result* r) { delete r; }
 

@@ -137,6 +137,30 @@ def test_multi_shift_matches_single_projectors():
         assert round(r.P.trace()) == int((ev < mu).sum())
 
 
+@pytest.mark.gpu
+def test_multi_shift_over_devices():
+    """spg_hqdwh_shifts_devices on the visible GPUs (one here): same results as single calls,
+    device bookkeeping, result calls from a thread whose current device differs are safe."""
+    A = S.dimer_chain(1024, 1.0, 0.5, 0.1, 6)
+    shifts = [0.0, 0.9, -0.9, 0.3]
+    rs, dev_of = S.hqdwh_shifts_devices(A, shifts, 64, 1e-10)              # every visible device
+    assert all(d >= 0 for d in dev_of)
+    L = S.load_library()
+    for mu, r, d in zip(shifts, rs, dev_of):
+        assert L.spg_result_device(r._handle) == d
+        single = S.hqdwh(A.shifted(mu), 64, 1e-10)
+        a, b = r.P.to_flat(), single.P.to_flat()
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+    rs1, dev1 = S.hqdwh_shifts_devices(A, shifts[:2], 64, 1e-10, devices=[0], per_device_concurrent=1)
+    assert dev1 == [0, 0]
+    np.testing.assert_array_equal(rs1[1].P.to_flat()[1], rs[1].P.to_flat()[1])
+    with pytest.raises(ValueError):
+        S.hqdwh_shifts_devices(A, shifts, 64, 1e-10, devices=[0, 99])
+    with pytest.raises(ValueError):
+        S.hqdwh_shifts_devices(A, shifts, 64, 1e-10, devices=[0, 0])
+
+
 @need_cli
 @pytest.mark.gpu
 def test_cli_multi_shift_reports(tmp_path):
