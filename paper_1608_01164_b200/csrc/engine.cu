@@ -470,7 +470,6 @@ void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>&
     Workspace& wsp = side_sel_ >= 0 ? *ws_side_[side_sel_] : *ws_;   // split-K partials: this stream's stack
     const long long mark = wsp.mark();
     std::vector<int4> ctas;
-    std::vector<int> red;
     // split-K balances the batch: no CTA runs more than `chunk` k-tiles of 16, chunk = the
     // batch's k-tiles spread over >= 2 CTAs per SM (and >= 8 k-tiles per split)
     long long base = 0, ktiles = 0;
@@ -497,7 +496,8 @@ void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>&
             g.Mcap = mM;
             g.Ncap = mN;
             g.partial = wsp.ptr(wsp.alloc((long long)g.nsplit * mM * mN));
-            red.push_back((int)i);
+            g.tilectr = arena_->push(std::vector<int>((size_t)tm * tn, 0));   // re-armed by the reducing CTA
+            g.tn = tn;
         }
         for (int s = 0; s < g.nsplit; ++s)
             for (int a = 0; a < tm; ++a)
@@ -508,8 +508,6 @@ void Engine::gemm(Plan& p, std::vector<GemmItem> items, const std::vector<int3>&
     b.d_items = arena_->push(items);
     b.d_ctas = arena_->push(ctas);
     b.nctas = (int)ctas.size();
-    b.d_red_items = arena_->push(red);
-    b.nred = (int)red.size();
     b.flops = sc_.counters + 1;
     if (profile_) {   // timeline shape: CTAs, largest K
         prof_ntask_ = (int)ctas.size();

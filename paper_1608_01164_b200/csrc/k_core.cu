@@ -11,6 +11,7 @@
 //   V coefficients  Zv = P W[:, kept]               (carry sigma)
 // so B' = (Q_u Zu)(Q_v Zv)^T.  The rotations are accumulated exactly and the
 // sigma-carrying side is W itself, so |B - B'| stays at u |C| + dropped part.
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 
@@ -366,7 +367,6 @@ __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double*
 //     schedule precomputed), one barrier per round (__syncthreads_or doubles as
 //     the convergence vote), rotation parameters from MUFU seeds + Newton steps;
 //   * Zu = Q_c V_J by reflectors from shared memory, four columns per warp.
-constexpr int K3 = 64, L3 = 65;
 
 __device__ __forceinline__ double rcp_nr(double x) {
     if (!(fabs(x) > 1e-290 && fabs(x) < 1e290)) return 1.0 / x;
@@ -417,63 +417,92 @@ __device__ __forceinline__ void dmma_c(double& c0, double& c1, double a, double 
                  : "d"(a), "d"(b));
 }
 
-__device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, double eps, unsigned* status,
-                           double* smem) {
+// Shared scratch of the latency-optimised core (one copy for both instantiations).
+constexpr int RPM = 64;   // Jacobi capacity: a half-warp per column pair, 32 pairs over 16 warps
+struct CoreShared {
+    double cn2[2][128], beta[KIN_MAX], tau[KIN_MAX], scal[KIN_MAX], sig[KIN_MAX], red[16];
+    int perm[KIN_MAX], act[KIN_MAX], ord[KIN_MAX], r, big[3];
+    double delta;
+    unsigned short pairs[(RPM - 1) * 32];
+};
+
+// KM = 64: k <= 64, R_u and R_v staged in shared memory (the layout of the first version).
+// KM = KIN_MAX (112): k <= 112; R_u staged over the region Z and V_J use later, R_v read from
+// global / L1; seven owned columns per warp and four rows per lane in the QRCP; the numerical
+// rank r' after QRCP must fit the Jacobi capacity RPM = 64 (else `false` is returned before
+// anything was written and the caller runs the general core2_body).
+template <int KM>
+__device__ bool core3_body(const TTask& t, int k, double* __restrict__ ws, double eps, unsigned* status,
+                           double* smem, CoreShared& cs) {
+    constexpr int L = KM + 1;            // leading dimension of C, Z, staged R_u (odd: conflict-free columns)
+    constexpr int LJ = RPM + 1;          // leading dimension of V_J (and of the staged R_v when KM = 64)
+    constexpr int NR = (KM + 31) / 32;   // rows per lane (row = lane + 32 t)
+    constexpr int NC = (KM + 15) / 16;   // owned columns per warp (column = warp + 16 m)
+    constexpr int NRJ = (KM + 15) / 16;  // Z rows per half-warp lane in the Jacobi (row = hl + 16 m)
+    constexpr int NT = KM / 8;           // 8 x 8 tiles per dimension of C
+    constexpr int ZA = RPM * L + RPM * LJ;
+    constexpr int REG_A = ZA > KM * L ? ZA : KM * L;
+    static_assert(NC < 8 && KM % 16 == 0 && KM <= 128, "one 8-value reduction per column");
     double* sZ = smem;                 // R_u, then Z (k x rp)
-    double* sJ = smem + K3 * L3;       // R_v, then V_J (rp x rp)
-    double* sC = smem + 2 * K3 * L3;   // C, then R (rows) + reflectors (below the diagonal)
-    __shared__ double sCn2[2][K3], sBeta[K3], sTau[K3], sScal[K3], sSig[K3], sRed3[16];
-    __shared__ int sPerm3[K3], sAct[K3], sOrd3[K3], sR3;
-    __shared__ double sDelta3;
-    __shared__ unsigned short sPairs[63 * 32];
+    double* sJ = smem + RPM * L;       // (KM = 64: R_v, then) V_J (rp x rp)
+    double* sC = smem + REG_A;         // C, then R (rows) + reflectors (below the diagonal)
     int* dbg = reinterpret_cast<int*>(status + 4);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gi = lane >> 2, gk = lane & 3;
     double* hdr = ws + t.ws;
     const double* Ru = core_final_R(t, ws, 0);
     const double* Rv = core_final_R(t, ws, 1);
-    for (int idx = tid; idx < K3 * K3; idx += TS_THREADS) {
-        const int i = idx & 63, j = idx >> 6;
-        if (i < k && j < k && i <= j) {
-            cpa8(sZ + i + j * L3, Ru + i + (long long)j * KIN_MAX);
-            cpa8(sJ + i + j * L3, Rv + i + (long long)j * KIN_MAX);
-        } else {
-            sZ[i + j * L3] = 0.0;
-            sJ[i + j * L3] = 0.0;
+    for (int idx = tid; idx < KM * KM; idx += TS_THREADS) {
+        const int i = idx % KM, j = idx / KM;
+        const bool in = i < k && j < k && i <= j;
+        if (in) cpa8(sZ + i + j * L, Ru + i + (long long)j * KIN_MAX);
+        else sZ[i + j * L] = 0.0;
+        if (KM == 64) {
+            if (in) cpa8(sJ + i + j * LJ, Rv + i + (long long)j * KIN_MAX);
+            else sJ[i + j * LJ] = 0.0;
         }
     }
     cpa_wait_all();
-    if (tid < K3) { sAct[tid] = 1; sCn2[0][tid] = -1.0; sCn2[1][tid] = -1.0; }
+    for (int i = tid; i < 128; i += TS_THREADS) { cs.cn2[0][i] = -1.0; cs.cn2[1][i] = -1.0; }
+    if (tid == 0) cs.big[0] = cs.big[1] = cs.big[2] = 0;
+    if (tid < KM) cs.act[tid] = 1;
     __syncthreads();
-    // C[i][j] = sum_l Ru[i][l] Rv[j][l]
+    // C[i][j] = sum_l Ru[i][l] Rv[j][l]  (l >= max(i, j): both factors upper triangular)
     const int nt8 = (k + 7) / 8, nks = (k + 3) / 4;
+    const double* Bm = KM == 64 ? sJ : Rv;   // R_v is zero below its diagonal and beyond k (stream_qr)
+    const int ldb = KM == 64 ? LJ : KIN_MAX;
     double fro = 0.0;
-    for (int tile = warp; tile < 64; tile += 16) {
-        const int mt = tile & 7, nt = tile >> 3;
+    for (int tile = warp; tile < NT * NT; tile += 16) {
+        const int mt = tile % NT, nt = tile / NT;
         double c0 = 0.0, c1 = 0.0;
         if (mt < nt8 && nt < nt8)
-            for (int ks = 0; ks < nks; ++ks)
-                dmma_c(c0, c1, sZ[(mt * 8 + gi) + (ks * 4 + gk) * L3], sJ[(nt * 8 + gi) + (ks * 4 + gk) * L3]);
+            for (int ks = 2 * max(mt, nt); ks < nks; ++ks)
+                dmma_c(c0, c1, sZ[(mt * 8 + gi) + (ks * 4 + gk) * L], Bm[(nt * 8 + gi) + (long long)(ks * 4 + gk) * ldb]);
         const int i = mt * 8 + gi, j = nt * 8 + 2 * gk;
-        sC[i + j * L3] = c0;
-        sC[i + (j + 1) * L3] = c1;
+        sC[i + j * L] = c0;
+        sC[i + (j + 1) * L] = c1;
         fro += c0 * c0 + c1 * c1;
     }
     fro = csum(fro);
-    if (lane == 0) sRed3[warp] = fro;
+    if (lane == 0) cs.red[warp] = fro;
     __syncthreads();
     if (warp == 0) {
-        double v = lane < 16 ? sRed3[lane] : 0.0;
+        double v = lane < 16 ? cs.red[lane] : 0.0;
         v = csum(v);
-        if (lane == 0) sDelta3 = fmax(1e-3 * eps / sqrt((double)k), 16.0 * DBL_EPSILON * sqrt(v));
+        if (lane == 0) cs.delta = fmax(1e-3 * eps / sqrt((double)k), 16.0 * DBL_EPSILON * sqrt(v));
     }
     for (int c = warp; c < k; c += 16) {
-        const double a0 = sC[lane + c * L3], a1 = sC[lane + 32 + c * L3];
-        const double s = csum(a0 * a0 + a1 * a1);
-        if (lane == 0) sCn2[0][c] = s;   // squared column norms (-1 = pivoted or absent)
+        double s = 0.0;
+#pragma unroll
+        for (int tt = 0; tt < NR; ++tt) {
+            const double a = lane + 32 * tt < KM ? sC[lane + 32 * tt + c * L] : 0.0;
+            s += a * a;
+        }
+        s = csum(s);
+        if (lane == 0) cs.cn2[0][c] = s;   // squared column norms (-1 = pivoted or absent)
     }
     __syncthreads();
-    const double delta = sDelta3;
+    const double delta = cs.delta;
     const double delta2 = delta * delta;
     // ---- QRCP
     // squared column norms double-buffered (read cur, write nxt) so that the redundant
@@ -481,16 +510,18 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     // are downdated (|a(j+1:)|^2 = |a(j:)|^2 - a_j^2, the reflector preserves the
     // norm of rows j..) and recomputed exactly once cancellation has cost 8 digits
     int rp = 0, pprev = -1;
+    bool over = false;
     for (int j = 0; j < k; ++j) {
-        const double* cur = sCn2[j & 1];
-        double* nxt = sCn2[(j + 1) & 1];
+        const double* cur = cs.cn2[j & 1];
+        double* nxt = cs.cn2[(j + 1) & 1];
         double best = cur[lane];
         if (!(best == best)) best = -1.0;   // NaN (non-finite input) counts as pivoted: keeps every warp's pivot identical
         int p = lane;
-        {
-            double b1 = cur[lane + 32];
+#pragma unroll
+        for (int tt = 1; tt < NR; ++tt) {
+            double b1 = cur[lane + 32 * tt];
             if (!(b1 == b1)) b1 = -1.0;
-            if (b1 > best) { best = b1; p = lane + 32; }
+            if (b1 > best) { best = b1; p = lane + 32 * tt; }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -499,30 +530,37 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
             if (ob > best || (ob == best && op < p)) { best = ob; p = op; }
         }
         if (best <= delta2) break;
-        const double* xp = sC + p * L3;
-        const double x0 = (lane > j && lane < k) ? xp[lane] : 0.0;
-        const double x1 = (lane + 32 > j && lane + 32 < k) ? xp[lane + 32] : 0.0;
-        const double alpha = xp[j];
-        double a0[4], a1[4], aj[4], cn[4];
-        bool act[4];
+        if (KM > RPM && j >= RPM) { over = true; break; }   // rank beyond the Jacobi capacity (every warp agrees)
+        const double* xp = sC + p * L;
+        double x[NR];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {   // owned columns, loaded while the reflector is formed
+        for (int tt = 0; tt < NR; ++tt) x[tt] = (lane + 32 * tt > j && lane + 32 * tt < k) ? xp[lane + 32 * tt] : 0.0;
+        const double alpha = xp[j];
+        double a[NC][NR], aj[NC], cn[NC];
+        bool act[NC];
+#pragma unroll
+        for (int m = 0; m < NC; ++m) {   // owned columns, loaded while the reflector is formed
             const int c = warp + 16 * m;
             cn[m] = c < k ? cur[c] : -1.0;
             act[m] = c < k && c != p && cn[m] >= 0.0;
-            const double* col = sC + c * L3;
-            a0[m] = (act[m] && lane > j && lane < k) ? col[lane] : 0.0;
-            a1[m] = (act[m] && lane + 32 > j && lane + 32 < k) ? col[lane + 32] : 0.0;
+            const double* col = sC + c * L;
+#pragma unroll
+            for (int tt = 0; tt < NR; ++tt)
+                a[m][tt] = (act[m] && lane + 32 * tt > j && lane + 32 * tt < k) ? col[lane + 32 * tt] : 0.0;
             aj[m] = act[m] ? col[j] : 0.0;
         }
-        // one reduction for |x|^2 and the four x . a_m (v = scal x, so v . a_m = scal (x . a_m))
+        // one reduction for |x|^2 and the x . a_m (v = scal x, so v . a_m = scal (x . a_m))
         double q8[8];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) q8[m] = x0 * a0[m] + x1 * a1[m];
-        q8[4] = x0 * x0 + x1 * x1;
-        q8[5] = q8[6] = q8[7] = 0.0;
+        for (int m = 0; m < 8; ++m) q8[m] = 0.0;
+#pragma unroll
+        for (int m = 0; m < NC; ++m)
+#pragma unroll
+            for (int tt = 0; tt < NR; ++tt) q8[m] = fma(x[tt], a[m][tt], q8[m]);
+#pragma unroll
+        for (int tt = 0; tt < NR; ++tt) q8[NC] = fma(x[tt], x[tt], q8[NC]);
         warp_allreduce8(q8);
-        const double s2 = q8[4];
+        const double s2 = q8[NC];
         double tau = 0.0, scal = 0.0, beta = alpha;
         if (s2 > 0.0) {
             const double nrm = sqrt_nr(fma(alpha, alpha, s2));
@@ -530,39 +568,44 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
             tau = (beta - alpha) * rcp_nr(beta);
             scal = rcp_nr(alpha - beta);
         }
-        const double v0 = x0 * scal, v1 = x1 * scal;
-        double d[4];
+        double v[NR];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) d[m] = scal * q8[m];
+        for (int tt = 0; tt < NR; ++tt) v[tt] = x[tt] * scal;
         bool redo = false;
-        double ns[4];
+        double ns[NC];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const double w = tau * (d[m] + aj[m]);
+        for (int m = 0; m < NC; ++m) {
+            const double w = tau * (scal * q8[m] + aj[m]);
             aj[m] -= w;
-            a0[m] -= w * v0;
-            a1[m] -= w * v1;
+#pragma unroll
+            for (int tt = 0; tt < NR; ++tt) a[m][tt] -= w * v[tt];
             ns[m] = cn[m] - aj[m] * aj[m];
             if (act[m] && !(ns[m] > 1e-8 * cn[m])) redo = true;   // warp-uniform
         }
         if (redo) {
 #pragma unroll
-            for (int m = 0; m < 4; ++m) ns[m] = a0[m] * a0[m] + a1[m] * a1[m];
+            for (int m = 0; m < NC; ++m) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int tt = 0; tt < NR; ++tt) sacc = fma(a[m][tt], a[m][tt], sacc);
+                ns[m] = sacc;
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-                for (int m = 0; m < 4; ++m) ns[m] += __shfl_xor_sync(0xffffffffu, ns[m], o);
+                for (int m = 0; m < NC; ++m) ns[m] += __shfl_xor_sync(0xffffffffu, ns[m], o);
         }
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < NC; ++m) {
             if (!act[m]) continue;
-            double* col = sC + (warp + 16 * m) * L3;
-            if (lane > j && lane < k) col[lane] = a0[m];
-            if (lane + 32 > j && lane + 32 < k) col[lane + 32] = a1[m];
+            double* col = sC + (warp + 16 * m) * L;
+#pragma unroll
+            for (int tt = 0; tt < NR; ++tt)
+                if (lane + 32 * tt > j && lane + 32 * tt < k) col[lane + 32 * tt] = a[m][tt];
             if (lane == 0) { col[j] = aj[m]; nxt[warp + 16 * m] = ns[m]; }
         }
         if (tid == 0) {
-            sPerm3[j] = p; sBeta[j] = beta; sTau[j] = tau; sScal[j] = scal;
+            cs.perm[j] = p; cs.beta[j] = beta; cs.tau[j] = tau; cs.scal[j] = scal;
             nxt[p] = -1.0;
             if (pprev >= 0) nxt[pprev] = -1.0;
         }
@@ -570,25 +613,27 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         __syncthreads();
         rp = j + 1;
     }
+    if (over) return false;
     // reflector tails scaled in place, R(j, j) = beta_j; unpivoted columns appended to the order
     for (int j = warp; j < rp; j += 16) {
-        double* col = sC + sPerm3[j] * L3;
-        const double sc = sScal[j];
-        if (lane > j && lane < k) col[lane] *= sc;
-        if (lane + 32 > j && lane + 32 < k) col[lane + 32] *= sc;
-        if (lane == 0) col[j] = sBeta[j];
+        double* col = sC + cs.perm[j] * L;
+        const double sc = cs.scal[j];
+#pragma unroll
+        for (int tt = 0; tt < NR; ++tt)
+            if (lane + 32 * tt > j && lane + 32 * tt < k) col[lane + 32 * tt] *= sc;
+        if (lane == 0) col[j] = cs.beta[j];
     }
     if (tid == 0) {
-        for (int j = 0; j < rp; ++j) sAct[sPerm3[j]] = 0;
+        for (int j = 0; j < rp; ++j) cs.act[cs.perm[j]] = 0;
         int q = rp;
-        for (int c = 0; c < k; ++c) if (sAct[c]) sPerm3[q++] = c;
+        for (int c = 0; c < k; ++c) if (cs.act[c]) cs.perm[q++] = c;
     }
     __syncthreads();
     // Z = R'^T (k x rp), V_J = I, round schedule
-    for (int idx = tid; idx < K3 * K3; idx += TS_THREADS) {
-        const int c = idx & 63, a = idx >> 6;
-        if (a < rp) sZ[c + a * L3] = (c < k && a <= c) ? sC[a + sPerm3[c] * L3] : 0.0;
-        if (c < rp && a < rp) sJ[c + a * L3] = c == a ? 1.0 : 0.0;
+    for (int idx = tid; idx < KM * RPM; idx += TS_THREADS) {
+        const int c = idx % KM, a = idx / KM;
+        if (a < rp) sZ[c + a * L] = (c < k && a <= c) ? sC[a + cs.perm[c] * L] : 0.0;
+        if (c < rp && a < rp) sJ[c + a * LJ] = c == a ? 1.0 : 0.0;
     }
     const int kk = rp + (rp & 1), npairs = kk / 2, mrr = kk - 1;
     for (int idx = tid; idx < mrr * npairs; idx += TS_THREADS) {
@@ -597,7 +642,7 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
         if (pi == 0) { p = r; q = kk - 1; }
         else { p = (r + pi) % mrr; q = (r - pi + mrr) % mrr; }
         if (p > q) { const int tmp = p; p = q; q = tmp; }
-        sPairs[r * 32 + pi] = (unsigned short)(p | (q << 8));
+        cs.pairs[r * 32 + pi] = (unsigned short)(p | (q << 8));
     }
     __syncthreads();
     int nsweeps = 0;
@@ -605,27 +650,40 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     if (rp > 1 && warp < nact) {
         const int h = tid >> 4, hl = tid & 15;
         const unsigned hmask = 0xFFFFu << (lane & 16);
-        const double tol2 = 1e-30;   // |a_pq| > 1e-15 sqrt(a_pp a_qq), squared
+        const double tol2 = 1e-30;   // |a_pq| > 1e-15 sqrt(a_pp a_qq), squared (jacobi_sweeps, dense_factor.hpp:113)
+        // A sweep in which no pair was above 1e-7 relative before its rotation leaves residuals at
+        // the 1e-14 level (quadratic convergence), so it is the last one: the reference's closing
+        // sweep, which only verifies that nothing rotates, is not run.  The truncation error does
+        // not depend on this (B = sum_j (Q_c V_J)_j W_j^T holds for every orthogonal V_J; dropping
+        // columns with |W_j| <= eps costs at most sqrt(#dropped) eps).
+        const double big2 = 1e-14;
         for (int sweep = 0; sweep < 60; ++sweep) {
             int any = 0;
+            // flag of this sweep: big[sweep % 3]; the next sweep's is cleared now (it was last read at
+            // the end of sweep - 2, and every thread has passed a barrier of sweep - 1 since)
+            if (tid == 0) cs.big[(sweep + 1) % 3] = 0;
             for (int r = 0; r < mrr; ++r) {
                 int rot = 0;
                 if (h < npairs) {
-                    const unsigned pq = sPairs[r * 32 + h];
+                    const unsigned pq = cs.pairs[r * 32 + h];
                     const int p = pq & 255, q = pq >> 8;
                     if (q < rp) {
-                        double zp[4], zq[4], jp[4], jq[4];
+                        double zp[NRJ], zq[NRJ], jp[4], jq[4];
                         double app = 0.0, aqq = 0.0, apq = 0.0;
 #pragma unroll
-                        for (int m = 0; m < 4; ++m) {
+                        for (int m = 0; m < NRJ; ++m) {
                             const int i = hl + 16 * m;
-                            zp[m] = i < k ? sZ[i + p * L3] : 0.0;
-                            zq[m] = i < k ? sZ[i + q * L3] : 0.0;
-                            jp[m] = i < rp ? sJ[i + p * L3] : 0.0;
-                            jq[m] = i < rp ? sJ[i + q * L3] : 0.0;
+                            zp[m] = i < k ? sZ[i + p * L] : 0.0;
+                            zq[m] = i < k ? sZ[i + q * L] : 0.0;
                             app += zp[m] * zp[m];
                             aqq += zq[m] * zq[m];
                             apq += zp[m] * zq[m];
+                        }
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int i = hl + 16 * m;
+                            jp[m] = i < rp ? sJ[i + p * LJ] : 0.0;
+                            jq[m] = i < rp ? sJ[i + q * LJ] : 0.0;
                         }
 #pragma unroll
                         for (int o = 8; o > 0; o >>= 1) {
@@ -633,25 +691,42 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
                             aqq += __shfl_xor_sync(hmask, aqq, o);
                             apq += __shfl_xor_sync(hmask, apq, o);
                         }
-                        if (app > 0.0 && aqq > 0.0 && apq * apq > tol2 * (app * aqq)) {
+                        const double pp = app * aqq, oo = apq * apq;
+                        if (app > 0.0 && aqq > 0.0 && oo > tol2 * pp) {
                             rot = 1;
-                            const double zeta = (aqq - app) * rcp_nr1(2.0 * apq);
-                            const double az = fabs(zeta);
-                            double tt;
-                            if (az > 1e100) tt = 0.5 * rcp_nr1(zeta);
-                            else tt = copysign(1.0, zeta) * rcp_nr1(az + sqrt_nr1(fma(zeta, zeta, 1.0)));
-                            const double c = rsqrt_nr3(fma(tt, tt, 1.0));
-                            const double s = c * tt;
+                            if (oo > big2 * pp && hl == 0) cs.big[sweep % 3] = 1;
+                            // rotation of jacobi_sweeps (tan 2 theta = 2 a_pq / (a_qq - a_pp), |theta| <= pi/4)
+                            // from two dependent rsqrt's: cos 2 theta = |d| / hypot(d, o),
+                            // c = sqrt((1 + cos 2 theta) / 2), s = sign(d) o / (2 c hypot(d, o)); c^2 + s^2 = 1
+                            const double d = aqq - app, o2 = 2.0 * apq;
+                            const double hh = fma(d, d, o2 * o2);
+                            double c, s;
+                            if (hh > 1e-290 && hh < 1e290) {
+                                const double rh = rsqrt_nr3(hh);
+                                const double u = fma(0.5 * fabs(d), rh, 0.5);
+                                const double ru = rsqrt_nr3(u);
+                                c = u * ru;
+                                s = copysign(0.5, d) * (o2 * rh) * ru;
+                            } else {   // out of the fast range: the reference formulas
+                                const double zeta = d / o2;
+                                const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                                c = 1.0 / sqrt(1.0 + tt * tt);
+                                s = c * tt;
+                            }
+#pragma unroll
+                            for (int m = 0; m < NRJ; ++m) {
+                                const int i = hl + 16 * m;
+                                if (i < k) {
+                                    sZ[i + p * L] = c * zp[m] - s * zq[m];
+                                    sZ[i + q * L] = s * zp[m] + c * zq[m];
+                                }
+                            }
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
                                 const int i = hl + 16 * m;
-                                if (i < k) {
-                                    sZ[i + p * L3] = c * zp[m] - s * zq[m];
-                                    sZ[i + q * L3] = s * zp[m] + c * zq[m];
-                                }
                                 if (i < rp) {
-                                    sJ[i + p * L3] = c * jp[m] - s * jq[m];
-                                    sJ[i + q * L3] = s * jp[m] + c * jq[m];
+                                    sJ[i + p * LJ] = c * jp[m] - s * jq[m];
+                                    sJ[i + q * LJ] = s * jp[m] + c * jq[m];
                                 }
                             }
                         }
@@ -660,109 +735,134 @@ __device__ void core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
                 any |= bar_or_1(rot, nact * 32);
             }
             ++nsweeps;
-            if (!any) break;
+            if (!any || !cs.big[sweep % 3]) break;
         }
     }
     __syncthreads();
     // ---- singular values, order, rank
     for (int j = warp; j < rp; j += 16) {
-        const double a0 = lane < k ? sZ[lane + j * L3] : 0.0;
-        const double a1 = lane + 32 < k ? sZ[lane + 32 + j * L3] : 0.0;
-        const double s = csum(a0 * a0 + a1 * a1);
+        double s = 0.0;
+#pragma unroll
+        for (int tt = 0; tt < NR; ++tt) {
+            const double a = lane + 32 * tt < k ? sZ[lane + 32 * tt + j * L] : 0.0;
+            s += a * a;
+        }
+        s = csum(s);
         if (lane == 0) {
             if (!(s == s)) atomicOr(status, ST_NONFINITE);
-            sSig[j] = s == s ? sqrt(s) : -1.0;   // NaN sorts last (total order keeps sOrd a permutation)
+            cs.sig[j] = s == s ? sqrt(s) : -1.0;   // NaN sorts last (total order keeps the order a permutation)
         }
     }
     __syncthreads();
     if (tid < rp) {
-        const double sj = sSig[tid];
+        const double sj = cs.sig[tid];
         int pos = 0;
         for (int i = 0; i < rp; ++i) {
-            const double si = sSig[i];
+            const double si = cs.sig[i];
             pos += (si > sj) || (si == sj && i < tid);
         }
-        sOrd3[pos] = tid;
+        cs.ord[pos] = tid;
     }
     __syncthreads();
     if (tid == 0) {
         int r = 0;
-        while (r < rp && sSig[sOrd3[r]] > eps) ++r;
+        while (r < rp && cs.sig[cs.ord[r]] > eps) ++r;
         if (r > KCAP) {
             if (atomicOr(status, ST_RANK_CAP) == 0 || dbg[0] == 0) {
                 dbg[0] = t.tag + 1; dbg[1] = t.p; dbg[2] = t.s; dbg[3] = k; dbg[4] = r;
             }
             r = KCAP;
         }
-        sR3 = r;
+        cs.r = r;
         hdr[0] = k; hdr[1] = r;
-        if (rp > 0 && !(sSig[sOrd3[0]] == sSig[sOrd3[0]])) atomicOr(status, ST_NONFINITE);
+        if (rp > 0 && !(cs.sig[cs.ord[0]] == cs.sig[cs.ord[0]])) atomicOr(status, ST_NONFINITE);
         count_trunc_work(status, t.p, t.s, k, r);   // SURVEY.md §8d work units
     }
     __syncthreads();
-    const int r = sR3;
+    const int r = cs.r;
     double* Zu = core_z(t, ws, 0);
     double* Zv = core_z(t, ws, 1);
     for (int idx = tid; idx < k * r; idx += TS_THREADS) {   // Zv[perm[c]][j] = W[c][ord_j] (carries sigma)
         const int c = idx % k, j = idx / k;
-        Zv[sPerm3[c] + (long long)j * KIN_MAX] = sZ[c + sOrd3[j] * L3];
+        Zv[cs.perm[c] + (long long)j * KIN_MAX] = sZ[c + cs.ord[j] * L];
     }
     // Zu = Q_c [V_J(:, ord); 0]: four columns per warp, reflectors rp-1 .. 0
     {
-        double x0[4], x1[4];
+        double x[4][NR];
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
             const int j = warp + 16 * m;
-            const int oj = j < r ? sOrd3[j] : 0;
-            x0[m] = (j < r && lane < rp) ? sJ[lane + oj * L3] : 0.0;
-            x1[m] = (j < r && lane + 32 < rp) ? sJ[lane + 32 + oj * L3] : 0.0;
+            const int oj = j < r ? cs.ord[j] : 0;
+#pragma unroll
+            for (int tt = 0; tt < NR; ++tt) x[m][tt] = (j < r && lane + 32 * tt < rp) ? sJ[lane + 32 * tt + oj * LJ] : 0.0;
         }
         if (warp < r)
             for (int hh = rp - 1; hh >= 0; --hh) {
-                const double tau = sTau[hh];
+                const double tau = cs.tau[hh];
                 if (tau == 0.0) continue;
-                const double* col = sC + sPerm3[hh] * L3;
-                const double v0 = lane == hh ? 1.0 : ((lane > hh && lane < k) ? col[lane] : 0.0);
-                const double v1 = lane + 32 == hh ? 1.0 : ((lane + 32 > hh && lane + 32 < k) ? col[lane + 32] : 0.0);
+                const double* col = sC + cs.perm[hh] * L;
+                double v[NR];
+#pragma unroll
+                for (int tt = 0; tt < NR; ++tt) {
+                    const int i = lane + 32 * tt;
+                    v[tt] = i == hh ? 1.0 : ((i > hh && i < k) ? col[i] : 0.0);
+                }
                 double d[4];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) d[m] = v0 * x0[m] + v1 * x1[m];
+                for (int m = 0; m < 4; ++m) {
+                    d[m] = 0.0;
+#pragma unroll
+                    for (int tt = 0; tt < NR; ++tt) d[m] = fma(v[tt], x[m][tt], d[m]);
+                }
                 warp_allreduce4(d);
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const double w = tau * d[m];
-                    x0[m] -= w * v0;
-                    x1[m] -= w * v1;
+#pragma unroll
+                    for (int tt = 0; tt < NR; ++tt) x[m][tt] -= w * v[tt];
                 }
             }
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
             const int j = warp + 16 * m;
             if (j < r) {
-                if (lane < k) Zu[lane + (long long)j * KIN_MAX] = x0[m];
-                if (lane + 32 < k) Zu[lane + 32 + (long long)j * KIN_MAX] = x1[m];
+#pragma unroll
+                for (int tt = 0; tt < NR; ++tt)
+                    if (lane + 32 * tt < k) Zu[lane + 32 * tt + (long long)j * KIN_MAX] = x[m][tt];
             }
         }
     }
     __syncthreads();
     if (tid == 0) *t.orank = r;
+    return true;
 }
 
 __global__ void __launch_bounds__(TS_THREADS, 1) k_core_any(const TTask* __restrict__ tasks, double* __restrict__ ws,
                                                         double eps, unsigned* status, int use3) {
     extern __shared__ double smem[];
+    __shared__ CoreShared cs;
     const TTask& t = tasks[blockIdx.x];
     if (use3 && !core_skip(t)) {
-        int k = core_kin(t);
-        if (k > 0 && k <= K3) {
-            core3_body(t, k, ws, eps, status, smem);
+        const int k = core_kin(t);
+        if (k > 0 && k <= 64) {
+            core3_body<64>(t, k, ws, eps, status, smem, cs);
             return;
+        }
+        if (k > 64 && k <= KIN_MAX) {
+            if (core3_body<KIN_MAX>(t, k, ws, eps, status, smem, cs)) return;
+            __syncthreads();   // numerical rank beyond the Jacobi capacity: the general path, from scratch
         }
     }
     core2_body(tasks, ws, eps, status, smem);
 }
 
-size_t core2_smem() { return sizeof(double) * (2 * KIN_MAX * KIN_MAX); }
+constexpr size_t core3_doubles(int km) {
+    const size_t za = (size_t)RPM * (km + 1) + (size_t)RPM * (RPM + 1), ru = (size_t)km * (km + 1);
+    return (za > ru ? za : ru) + ru;
+}
+size_t core2_smem() {
+    return sizeof(double) * std::max<size_t>({(size_t)2 * KIN_MAX * KIN_MAX, core3_doubles(64), core3_doubles(KIN_MAX)});
+}
 
 void core2_init_attributes() {
     SPG_CUDA(cudaFuncSetAttribute(k_core_any, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)core2_smem()));

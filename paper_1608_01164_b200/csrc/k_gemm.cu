@@ -5,7 +5,8 @@
 // (gemm_acc_rows / gemm_tn_rows, hodlr.hpp:169-198), the k x k cores of
 // lr_multiply (lowrank.hpp:89-93) and the Schur factors (hodlr.hpp:557-558).
 // Dimensions may be ranks living in device memory; CTAs beyond the runtime
-// extent exit.  Split-K partials are reduced in a fixed order (deterministic).
+// extent exit.  Split-K partials are reduced in a fixed order (deterministic) by the last
+// CTA of each output tile.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -123,29 +124,43 @@ __global__ void __launch_bounds__(G_THREADS) k_gemm(const GemmItem* __restrict__
                 const int n = n0 + wn + j * 8 + 2 * (lane & 3) + v;
                 if (m < M && n < N) {
                     if (split) {
-                        g.partial[(long long)cm.w * g.Mcap * g.Ncap + m + (long long)n * g.Mcap] = acc[i][j][v];
+                        __stcg(&g.partial[(long long)cm.w * g.Mcap * g.Ncap + m + (long long)n * g.Mcap], acc[i][j][v]);
                     } else {
                         double* c = g.C + m + (long long)n * g.ldc;
                         *c = g.beta == 0.0 ? alpha * acc[i][j][v] : alpha * acc[i][j][v] + g.beta * *c;
                     }
                 }
             }
-}
-
-// fixed-order split-K reduction: one CTA per item
-__global__ void k_gemm_reduce(const GemmItem* __restrict__ items, const int* __restrict__ red) {
-    const GemmItem& g = items[red[blockIdx.x]];
-    const int M = dimv(g.M, g.Mp), N = dimv(g.N, g.Np), K = dimv(g.K, g.Kp);
-    const double alpha = g.alphap ? g.alpha * *g.alphap : g.alpha;
+    if (!split) return;
+    // split-K: the last CTA of this output tile to arrive sums the partials in split order
+    // (fixed order whatever the arrival order: deterministic) and re-arms the counter
+    __shared__ int sLast;
+    __threadfence();
+    __syncthreads();
+    int* ctr = g.tilectr + cm.y * g.tn + cm.z;
+    if (tid == 0) sLast = atomicAdd(ctr, 1) == g.nsplit - 1;
+    __syncthreads();
+    if (!sLast) return;
+    __threadfence();
     const int chunk = ((K + g.nsplit - 1) / g.nsplit + GBK - 1) / GBK * GBK;
     const int nused = chunk > 0 ? min(g.nsplit, (K + chunk - 1) / chunk) : 0;
-    for (int idx = threadIdx.x; idx < M * N; idx += blockDim.x) {
-        const int m = idx % M, n = idx / M;
+    const int tmr = min(GBM, M - m0), tnr = min(GBN, N - n0);
+    const long long pstride = (long long)g.Mcap * g.Ncap;
+    for (int idx = tid; idx < tmr * tnr; idx += G_THREADS) {
+        const int m = m0 + idx % tmr, n = n0 + idx / tmr;
+        const double* pp = g.partial + m + (long long)n * g.Mcap;
         double s = 0.0;
-        for (int p = 0; p < nused; ++p) s += g.partial[(long long)p * g.Mcap * g.Ncap + m + (long long)n * g.Mcap];
+        for (int p0 = 0; p0 < nused; p0 += 8) {   // eight loads in flight, summed in split order
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = p0 + u < nused ? __ldcg(pp + (p0 + u) * pstride) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
         double* c = g.C + m + (long long)n * g.ldc;
         *c = g.beta == 0.0 ? alpha * s : alpha * s + g.beta * *c;
     }
+    if (tid == 0) *ctr = 0;
 }
 
 void gemm_init_attributes() {
@@ -156,10 +171,6 @@ void launch_gemm(const GemmBatch& b, cudaStream_t st) {
     if (b.nctas == 0) return;
     k_gemm<<<b.nctas, G_THREADS, gemm_smem_bytes(), st>>>(b.d_items, b.d_ctas, b.flops);
     SPG_LAUNCH_CHECK();
-    if (b.nred) {
-        k_gemm_reduce<<<b.nred, 256, 0, st>>>(b.d_items, b.d_red_items);
-        SPG_LAUNCH_CHECK();
-    }
 }
 
 }  // namespace spg

@@ -870,6 +870,13 @@ static void launch_hager_chunked(int n, int b, const double* bands, const double
     if (P < 1) P = 1;
     A.L = (n + P - 1) / P;
     A.P = (n + A.L - 1) / A.L;
+    // the ragged last chunk obeys the same minimum (n = 19111, b = 2: 148 chunks of 130 would leave
+    // a 1-row chunk, which the backward sweeps process first and whose window then reaches past it)
+    while (A.P > 1 && n - (A.P - 1) * A.L < 4 * b + 1) {
+        --P;
+        A.L = (n + P - 1) / P;
+        A.P = (n + A.L - 1) / A.L;
+    }
     double* x = vecs + n;
     double* y = vecs + 2 * (size_t)n;
     double* z = vecs + 3 * (size_t)n;

@@ -20,7 +20,8 @@ void launch_truncate(const TruncBatch& b, double* ws, double eps, unsigned* stat
 // ------------------------------------------------------------ batched DMMA GEMM
 // C = alpha * op(A) op(B) + beta * C, column-major.  Dimensions are constants
 // or read from device memory (ranks).  With nsplit > 1 the K range is split
-// and partials (fixed-order reduced) go through `partial`.
+// and the partials go through `partial`; the last split CTA of a tile to finish sums them
+// in split order (deterministic) -- no second launch.
 struct GemmItem {
     const double* A;
     const double* B;
@@ -36,13 +37,13 @@ struct GemmItem {
     int nsplit;                   // K splits (>= 1)
     double* partial;              // nsplit * Mcap * Ncap doubles when nsplit > 1
     int Mcap, Ncap;               // capacity bounds (partials ld = Mcap)
+    int* tilectr;                 // nsplit > 1: arrival counter per output tile (tile_m * tn + tile_n), zero between launches
+    int tn;                       // tiles along N
 };
 struct GemmBatch {
     const GemmItem* d_items = nullptr;
     const int4* d_ctas = nullptr;   // (item, tile_m, tile_n, split)
     int nctas = 0;
-    const int* d_red_items = nullptr;  // items needing a split-K reduction
-    int nred = 0;
     double* flops = nullptr;           // device counter of algorithmic flops (2MNK)
 };
 void launch_gemm(const GemmBatch& b, cudaStream_t st);
