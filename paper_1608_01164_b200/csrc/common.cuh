@@ -1,5 +1,6 @@
 // Shared definitions for the B200 hQDWH engine (sm_100a, FP64).
 #pragma once
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 #include <atomic>
@@ -39,6 +40,20 @@ struct CudaError : std::runtime_error {
             throw ::spg::CudaError(std::string("CUDA error ") + cudaGetErrorString(e_) + \
                                    " at " + __FILE__ + ":" + std::to_string(__LINE__));   \
     } while (0)
+
+// Device allocation of the library.  SPG_DBG_POISON=1 fills every new allocation with 0xFF
+// bytes (NaN doubles, -1 ints): reads of memory nothing wrote show up as NaN / NPD failures
+// instead of depending on what the allocator hands back (diagnostics).
+template <class T>
+inline cudaError_t dev_malloc(T** p, size_t bytes) {
+    static const bool poison = std::getenv("SPG_DBG_POISON") != nullptr;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    if (e == cudaSuccess && poison) {   // the fill is on the legacy stream: finish it before anything else runs
+        e = cudaMemset(*p, 0xFF, bytes);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    return e;
+}
 
 // Asynchronous global -> shared copies (cp.async, 8 bytes each).  Staging loops
 // written as "for (i = tid; i < n; i += blockDim.x) s[i] = g[i]" wait for every

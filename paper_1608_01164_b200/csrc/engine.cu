@@ -53,7 +53,7 @@ void HTree::subtree(int r, std::vector<int>& internal, std::vector<int>& lvs) co
 }
 
 // ================================================================ arena / workspace
-Arena::Arena(size_t bytes) : cap_(bytes) { SPG_CUDA(cudaMalloc(&dev_, bytes)); host_.reserve(1 << 20); }
+Arena::Arena(size_t bytes) : cap_(bytes) { SPG_CUDA(dev_malloc(&dev_, bytes)); host_.reserve(1 << 20); }
 Arena::~Arena() { if (dev_) cudaFree(dev_); }
 
 void* Arena::push_raw(const void* src, size_t bytes) {
@@ -76,7 +76,7 @@ void Arena::commit(cudaStream_t st) {
     }
 }
 
-Workspace::Workspace(size_t n) : cap_(n) { SPG_CUDA(cudaMalloc(&base_, n * sizeof(double))); }
+Workspace::Workspace(size_t n) : cap_(n) { SPG_CUDA(dev_malloc(&base_, n * sizeof(double))); }
 Workspace::~Workspace() { if (base_) cudaFree(base_); }
 long long Workspace::alloc(long long n) {
     const long long off = (top_ + 31) & ~31LL;
@@ -96,15 +96,15 @@ void DHodlr::alloc(const HTree& tree, Arena& arena) {
     for (int id : tree.leaves) { leaf_off.push_back(off); off += ((long long)tree.size[id] * tree.size[id] + 3) & ~3LL; }
     leaf_doubles = off;
     slab_doubles = (size_t)std::max(tree.depth, 1) * KCAP * tree.n;
-    SPG_CUDA(cudaMalloc(&leaves, sizeof(double) * (leaf_doubles + 2 * slab_doubles)));
+    SPG_CUDA(dev_malloc(&leaves, sizeof(double) * (leaf_doubles + 2 * slab_doubles)));
     U = leaves + leaf_doubles;
     V = U + slab_doubles;
-    SPG_CUDA(cudaMalloc(&rank, sizeof(int) * 2 * tree.nnodes()));
+    SPG_CUDA(dev_malloc(&rank, sizeof(int) * 2 * tree.nnodes()));
     d_leaf_off = arena.push(leaf_off);
     dinv_off.clear();
     long long doff = 0;
     for (int id : tree.leaves) { dinv_off.push_back(doff); doff += (long long)((tree.size[id] + 31) / 32) * 1024; }
-    SPG_CUDA(cudaMalloc(&dinv, sizeof(double) * std::max<long long>(doff, 1)));
+    SPG_CUDA(dev_malloc(&dinv, sizeof(double) * std::max<long long>(doff, 1)));
     d_dinv_off = arena.push(dinv_off);
 }
 
@@ -222,15 +222,15 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     for (auto& e : events_) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (int t = 0; t < std::max(1, tree_.depth); ++t) {
         double* p;
-        SPG_CUDA(cudaMalloc(&p, sizeof(double) * (size_t)n * KCAP));
+        SPG_CUDA(dev_malloc(&p, sizeof(double) * (size_t)n * KCAP));
         chol_panels_.push_back(p);
-        SPG_CUDA(cudaMalloc(&p, sizeof(double) * (size_t)n * KCAP));
+        SPG_CUDA(dev_malloc(&p, sizeof(double) * (size_t)n * KCAP));
         xpanels_.push_back(p);
     }
     int max_leaf = 0;
     for (int x = 0; x < tree_.nnodes(); ++x) if (tree_.leaf(x)) max_leaf = std::max(max_leaf, tree_.size[x]);
     if (max_leaf > C4_LEAF_MAX)
-        SPG_CUDA(cudaMalloc(&leaf_scr_, sizeof(double) * (size_t)(TRM_NMAX / 2) * (TRM_NMAX / 2)));
+        SPG_CUDA(dev_malloc(&leaf_scr_, sizeof(double) * (size_t)(TRM_NMAX / 2) * (TRM_NMAX / 2)));
     // device tree
     std::vector<int> tb = tree_.begin, ts = tree_.size, tl = tree_.left, tr = tree_.right, tv = tree_.level,
                      to = tree_.leaf_ord;
@@ -239,8 +239,11 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     dtree_.right = arena_->push(tr); dtree_.level = arena_->push(tv); dtree_.leaf_ord = arena_->push(to);
     // scalars
     const size_t nsc = 32 + 32 + 256 + 32;
-    SPG_CUDA(cudaMalloc(&scalar_mem_, nsc * sizeof(double)));
-    SPG_CUDA(cudaMemset(scalar_mem_, 0, nsc * sizeof(double)));
+    SPG_CUDA(dev_malloc(&scalar_mem_, nsc * sizeof(double)));
+    // on the engine's own stream: a memset on the legacy default stream is asynchronous and not
+    // ordered with a cudaStreamNonBlocking stream, so with the GPU busy (another projector of
+    // the same process) it could land after the setup kernels had written alpha / the schedule
+    SPG_CUDA(cudaMemsetAsync(scalar_mem_, 0, nsc * sizeof(double), st_));
     SPG_CUDA(cudaMallocHost(&host_pinned_, 64 * sizeof(double)));
     sc_.scal = scalar_mem_;
     sc_.slots = scalar_mem_ + 32;
@@ -252,12 +255,12 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
     // persistent panels and coefficient blocks
     for (int i = 0; i < 4; ++i) {
         double* p;
-        SPG_CUDA(cudaMalloc(&p, sizeof(double) * (size_t)n * KCAP));
+        SPG_CUDA(dev_malloc(&p, sizeof(double) * (size_t)n * KCAP));
         panels_.push_back(p);
     }
-    SPG_CUDA(cudaMalloc(&coef_, sizeof(double) * (size_t)KCAP * KCAP * 4 * tree_.nnodes()));
-    SPG_CUDA(cudaMalloc(&pcoef_, sizeof(double) * (size_t)KCAP * KCAP * tree_.nnodes()));
-    SPG_CUDA(cudaMalloc(&iranks_, sizeof(int) * 4 * tree_.nnodes()));
+    SPG_CUDA(dev_malloc(&coef_, sizeof(double) * (size_t)KCAP * KCAP * 4 * tree_.nnodes()));
+    SPG_CUDA(dev_malloc(&pcoef_, sizeof(double) * (size_t)KCAP * KCAP * tree_.nnodes()));
+    SPG_CUDA(dev_malloc(&iranks_, sizeof(int) * 4 * tree_.nnodes()));
     arena_->commit(st_);
 }
 
@@ -720,7 +723,7 @@ void Engine::psolve(Plan& p, const DHodlr& W, const std::vector<HSolveItem>& ite
 void Engine::op_solve_prep(Plan& p, DHodlr& W) {
     const int n = tree_.n;
     if (!W.tU) {
-        SPG_CUDA(cudaMalloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
+        SPG_CUDA(dev_malloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
         W.tV = W.tU + W.slab_doubles;
     }
     W.tready = false;
@@ -1038,7 +1041,7 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
     chol_tv_ = chol_defer_trunc_;
     if (chol_tv_) {   // forward subtree solves inside the factorisation go subtree-parallel
         if (!W.tU) {
-            SPG_CUDA(cudaMalloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
+            SPG_CUDA(dev_malloc(&W.tU, sizeof(double) * 2 * W.slab_doubles));
             W.tV = W.tU + W.slab_doubles;
         }
         W.tready = true;

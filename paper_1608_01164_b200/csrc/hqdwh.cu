@@ -228,7 +228,7 @@ void export_flat(Engine& E, const DHodlr& H, int* ranks, double* data, long long
     const HTree& t = E.tree();
     const int nn = t.nnodes();
     long long* doff;
-    SPG_CUDA(cudaMalloc(&doff, sizeof(long long) * (nn + 1)));
+    SPG_CUDA(dev_malloc(&doff, sizeof(long long) * (nn + 1)));
     cudaStream_t st = E.stream();
     k_flat_offsets<<<1, 32, 0, st>>>(E.dtree(), H.rank, doff);
     long long total = 0;
@@ -239,7 +239,7 @@ void export_flat(Engine& E, const DHodlr& H, int* ranks, double* data, long long
         // staging in the engine workspace when it is large enough (free once the projector is done)
         double* buf = nullptr;
         const bool own = (size_t)std::max<long long>(total, 1) > E.ws().capacity();
-        if (own) SPG_CUDA(cudaMalloc(&buf, sizeof(double) * std::max<long long>(total, 1)));
+        if (own) SPG_CUDA(dev_malloc(&buf, sizeof(double) * std::max<long long>(total, 1)));
         else buf = E.ws().base();
         k_flat_pack<<<nn, 256, 0, st>>>(E.dtree(), H.view(), doff, buf);
         SPG_CUDA(cudaMemcpyAsync(data, buf, sizeof(double) * total, cudaMemcpyDeviceToHost, st));
@@ -272,8 +272,8 @@ void import_flat(Engine& E, DHodlr& H, const int* ranks, const double* data) {
     SPG_CUDA(cudaMemcpyAsync(H.rank, rk.data(), sizeof(int) * 2 * nn, cudaMemcpyHostToDevice, st));
     long long* doff;
     double* buf;
-    SPG_CUDA(cudaMalloc(&doff, sizeof(long long) * (nn + 1)));
-    SPG_CUDA(cudaMalloc(&buf, sizeof(double) * std::max<long long>(total, 1)));
+    SPG_CUDA(dev_malloc(&doff, sizeof(long long) * (nn + 1)));
+    SPG_CUDA(dev_malloc(&buf, sizeof(double) * std::max<long long>(total, 1)));
     SPG_CUDA(cudaMemcpyAsync(buf, data, sizeof(double) * total, cudaMemcpyHostToDevice, st));
     k_flat_offsets<<<1, 32, 0, st>>>(E.dtree(), H.rank, doff);
     k_flat_unpack<<<nn, 256, 0, st>>>(E.dtree(), H.view(), doff, buf);
@@ -524,12 +524,12 @@ std::unique_ptr<HqdwhState> make_state_once(int n, int b, int n_min, double eps,
     // 10 n doubles from 128); first iterate: the band H / Givens work rows, n x (4b + 4)
     const size_t tmp_doubles = std::max({(size_t)128 + (size_t)n * wbl + estimate_l0_vecs_doubles(n),
                                          (size_t)128 + 10 * (size_t)n, (size_t)n * (4 * b + 4), (size_t)64 + 2 * (size_t)n});
-    SPG_CUDA(cudaMalloc(&st->d_bands, sizeof(double) * band_len(n, b)));
-    SPG_CUDA(cudaMalloc(&st->d_tmp, sizeof(double) * tmp_doubles));
-    SPG_CUDA(cudaMalloc(&st->d_rdiag, sizeof(double) * (size_t)(2 * b + 1) * n));
-    SPG_CUDA(cudaMalloc(&st->d_diag, sizeof(double) * 2 * 64));
-    SPG_CUDA(cudaMalloc(&st->d_piv, sizeof(int) * n));
-    SPG_CUDA(cudaMalloc(&st->d_phase, sizeof(double) * 128));
+    SPG_CUDA(dev_malloc(&st->d_bands, sizeof(double) * band_len(n, b)));
+    SPG_CUDA(dev_malloc(&st->d_tmp, sizeof(double) * tmp_doubles));
+    SPG_CUDA(dev_malloc(&st->d_rdiag, sizeof(double) * (size_t)(2 * b + 1) * n));
+    SPG_CUDA(dev_malloc(&st->d_diag, sizeof(double) * 2 * 64));
+    SPG_CUDA(dev_malloc(&st->d_piv, sizeof(int) * n));
+    SPG_CUDA(dev_malloc(&st->d_phase, sizeof(double) * 128));
     for (int f : E.tree().leaves) st->leaf_entries += (long long)E.tree().size[f] * E.tree().size[f];
     return st;
 }
@@ -963,11 +963,11 @@ int spg_stacked_qr_r(int n, int b, const double* bands, int method, double* rdia
         double *db, *dw, *dr, *ds;
         unsigned* dst;
         const long long blen = band_len(n, b);
-        SPG_CUDA(cudaMalloc(&db, sizeof(double) * blen));
-        SPG_CUDA(cudaMalloc(&dw, sizeof(double) * (size_t)n * (4 * b + 4)));
-        SPG_CUDA(cudaMalloc(&dr, sizeof(double) * (size_t)n * (2 * b + 1)));
-        SPG_CUDA(cudaMalloc(&ds, sizeof(double) * 8));
-        SPG_CUDA(cudaMalloc(&dst, sizeof(unsigned) * 16));
+        SPG_CUDA(dev_malloc(&db, sizeof(double) * blen));
+        SPG_CUDA(dev_malloc(&dw, sizeof(double) * (size_t)n * (4 * b + 4)));
+        SPG_CUDA(dev_malloc(&dr, sizeof(double) * (size_t)n * (2 * b + 1)));
+        SPG_CUDA(dev_malloc(&ds, sizeof(double) * 8));
+        SPG_CUDA(dev_malloc(&dst, sizeof(unsigned) * 16));
         // slots[0] = c0 selects the construction (launch_givens_reduce), slots[5] = scale 1
         double slots[8] = {method == 1 ? 1e308 : 0.0, 0, 0, 0, 0, 1.0, 0, 0};
         SPG_CUDA(cudaMemcpy(db, bands, sizeof(double) * blen, cudaMemcpyHostToDevice));
@@ -1119,9 +1119,9 @@ int spg_result_apply(const spg_result* r, int which, int m, const double* X, dou
             for (int c = 0; c < m; ++c) cm[i + (size_t)c * n] = X[(size_t)i * m + c];
         double *dx, *dy;
         int* dm;
-        SPG_CUDA(cudaMalloc(&dx, sizeof(double) * (size_t)n * m));
-        SPG_CUDA(cudaMalloc(&dy, sizeof(double) * (size_t)n * m));
-        SPG_CUDA(cudaMalloc(&dm, sizeof(int)));
+        SPG_CUDA(dev_malloc(&dx, sizeof(double) * (size_t)n * m));
+        SPG_CUDA(dev_malloc(&dy, sizeof(double) * (size_t)n * m));
+        SPG_CUDA(dev_malloc(&dm, sizeof(int)));
         SPG_CUDA(cudaMemcpyAsync(dx, cm.data(), sizeof(double) * cm.size(), cudaMemcpyHostToDevice, st));
         SPG_CUDA(cudaMemcpyAsync(dm, &m, sizeof(int), cudaMemcpyHostToDevice, st));
         SPG_CUDA(cudaMemsetAsync(dy, 0, sizeof(double) * (size_t)n * m, st));
@@ -1246,7 +1246,7 @@ int spg_ctx_from_banded(spg_ctx* c, int dst, int b, const double* bands) {
         const int n = E.tree().n;
         const long long len = band_len(n, b);
         double* d;
-        SPG_CUDA(cudaMalloc(&d, sizeof(double) * len));
+        SPG_CUDA(dev_malloc(&d, sizeof(double) * len));
         SPG_CUDA(cudaMemcpy(d, bands, sizeof(double) * len, cudaMemcpyHostToDevice));
         DHodlr& H = *c->slots.at(dst);
         H.zero(E.stream());
@@ -1300,11 +1300,11 @@ int spg_truncate(int p, int s, int k, const double* U, const double* V, double e
         for (int i = 0; i < s; ++i) for (int j = 0; j < k; ++j) cv[i + (size_t)j * s] = V[(size_t)i * k + j];
         double *du, *dv, *ou, *ov;
         int* dr;
-        SPG_CUDA(cudaMalloc(&du, sizeof(double) * std::max<size_t>(cu.size(), 1)));
-        SPG_CUDA(cudaMalloc(&dv, sizeof(double) * std::max<size_t>(cv.size(), 1)));
-        SPG_CUDA(cudaMalloc(&ou, sizeof(double) * (size_t)p * KCAP));
-        SPG_CUDA(cudaMalloc(&ov, sizeof(double) * (size_t)s * KCAP));
-        SPG_CUDA(cudaMalloc(&dr, sizeof(int)));
+        SPG_CUDA(dev_malloc(&du, sizeof(double) * std::max<size_t>(cu.size(), 1)));
+        SPG_CUDA(dev_malloc(&dv, sizeof(double) * std::max<size_t>(cv.size(), 1)));
+        SPG_CUDA(dev_malloc(&ou, sizeof(double) * (size_t)p * KCAP));
+        SPG_CUDA(dev_malloc(&ov, sizeof(double) * (size_t)s * KCAP));
+        SPG_CUDA(dev_malloc(&dr, sizeof(int)));
         SPG_CUDA(cudaMemcpy(du, cu.data(), sizeof(double) * cu.size(), cudaMemcpyHostToDevice));
         SPG_CUDA(cudaMemcpy(dv, cv.data(), sizeof(double) * cv.size(), cudaMemcpyHostToDevice));
         SPG_CUDA(cudaMemset(E.sc().status, 0, 14 * sizeof(unsigned)));

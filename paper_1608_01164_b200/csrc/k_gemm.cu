@@ -196,7 +196,7 @@ double measure_dmma_tflops() {
     int nsm = 0;
     SPG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
     double* d;
-    SPG_CUDA(cudaMalloc(&d, sizeof(double)));
+    SPG_CUDA(dev_malloc(&d, sizeof(double)));
     const int iters = 20000, blocks = nsm * 4;
     k_dmma_peak<<<blocks, 256>>>(d, 100);
     SPG_CUDA(cudaDeviceSynchronize());
