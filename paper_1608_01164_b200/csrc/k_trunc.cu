@@ -401,56 +401,77 @@ __device__ void stream_apply(int k, int r, int nrows, const double* refl, const 
         for (int i = tid; i < TS_TAUT; i += blockDim.x) cpa8(sTT + i, taut + (long long)b * TS_TAUT + i);
         cpa_wait_all();
         __syncthreads();
-        for (int c = warp; c < r; c += nwarps) {
-            double o[SB / 32];
+        // two output columns per warp: the reflector block is read from shared memory once for
+        // both, and the 2 x 8 panel dots go through two 8-value reductions (34 shuffles for two
+        // columns instead of 80)
+        for (int cp = warp; 2 * cp < r; cp += nwarps) {
+            const int c0 = 2 * cp, c1 = c0 + 1;
+            const bool h1 = c1 < r;
+            double o0[SB / 32], o1[SB / 32];
 #pragma unroll
-            for (int t = 0; t < SB / 32; ++t) o[t] = 0.0;
-            double* zc = sZ + c * KIN_MAX;
+            for (int t = 0; t < SB / 32; ++t) o0[t] = o1[t] = 0.0;
+            double* z0 = sZ + c0 * KIN_MAX;
+            double* z1 = sZ + (h1 ? c1 : c0) * KIN_MAX;
             for (int pn = npan - 1; pn >= 0; --pn) {
                 const int j0 = pn * TS_NB, nb = min(TS_NB, k - j0);
                 const double* Tp = sTT + KIN_MAX + pn * TS_NB * TS_NB;
-                double w[TS_NB];
+                double w0[TS_NB], w1[TS_NB];
 #pragma unroll
                 for (int a = 0; a < TS_NB; ++a) {
-                    double s = 0.0;
+                    double s0 = 0.0, s1 = 0.0;
                     if (a < nb)
 #pragma unroll
-                        for (int t = 0; t < SB / 32; ++t) s += sV[(lane + 32 * t) + (j0 + a) * SB] * o[t];
-                    w[a] = s;
+                        for (int t = 0; t < SB / 32; ++t) {
+                            const double v = sV[(lane + 32 * t) + (j0 + a) * SB];
+                            s0 += v * o0[t];
+                            s1 += v * o1[t];
+                        }
+                    w0[a] = s0;
+                    w1[a] = s1;
                 }
-#pragma unroll
-                for (int of = 16; of > 0; of >>= 1)
-#pragma unroll
-                    for (int a = 0; a < TS_NB; ++a) w[a] += __shfl_xor_sync(0xffffffffu, w[a], of);
-                double za[TS_NB];
+                warp_allreduce8(w0);
+                warp_allreduce8(w1);
 #pragma unroll
                 for (int a = 0; a < TS_NB; ++a) {
-                    za[a] = a < nb ? zc[j0 + a] : 0.0;
-                    w[a] += za[a];
+                    w0[a] += a < nb ? z0[j0 + a] : 0.0;
+                    w1[a] += a < nb ? z1[j0 + a] : 0.0;
                 }
-                double wt[TS_NB];
 #pragma unroll
-                for (int a = 0; a < TS_NB; ++a) {   // (T w)_a = sum_{i >= a} T(a, i) w_i
-                    double s = 0.0;
+                for (int a = 0; a < TS_NB; ++a) {   // in place: (T w)_a = sum_{i >= a} T(a, i) w_i
+                    double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-                    for (int i = a; i < TS_NB; ++i) s += Tp[a + i * TS_NB] * w[i];
-                    wt[a] = s;
+                    for (int i = a; i < TS_NB; ++i) {
+                        const double tv = Tp[a + i * TS_NB];
+                        s0 += tv * w0[i];
+                        s1 += tv * w1[i];
+                    }
+                    w0[a] = s0;
+                    w1[a] = s1;
                 }
 #pragma unroll
                 for (int t = 0; t < SB / 32; ++t) {
-                    double s = o[t];
+                    double s0 = o0[t], s1 = o1[t];
 #pragma unroll
                     for (int a = 0; a < TS_NB; ++a)
-                        if (a < nb) s -= sV[(lane + 32 * t) + (j0 + a) * SB] * wt[a];
-                    o[t] = s;
+                        if (a < nb) {
+                            const double v = sV[(lane + 32 * t) + (j0 + a) * SB];
+                            s0 -= v * w0[a];
+                            s1 -= v * w1[a];
+                        }
+                    o0[t] = s0;
+                    o1[t] = s1;
                 }
-                __syncwarp();
+                __syncwarp();   // every lane has read this panel's z entries
 #pragma unroll
                 for (int a = 0; a < TS_NB; ++a)
-                    if (lane == a && a < nb) zc[j0 + a] = za[a] - wt[a];
+                    if (lane == a && a < nb) {
+                        z0[j0 + a] -= w0[a];
+                        if (h1) z1[j0 + a] -= w1[a];
+                    }
                 __syncwarp();
             }
-            write(b * SB, c, o);
+            write(b * SB, c0, o0);
+            if (h1) write(b * SB, c1, o1);
         }
     }
 }
