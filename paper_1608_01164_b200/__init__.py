@@ -37,7 +37,10 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "libspecproj_b200.so")
+# SPG_LIB picks another build of the same C-ABI (tests run the wide-capacity build
+# libspecproj_b200_w.so through the parity tests this way); default: the in-tree library
+_LIB_PATH = os.environ.get("SPG_LIB") or os.path.join(HERE, "libspecproj_b200.so")
+WIDE_LIB_PATH = os.path.join(HERE, "libspecproj_b200_w.so")
 
 
 def lib_path() -> str:

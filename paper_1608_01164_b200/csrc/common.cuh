@@ -15,8 +15,17 @@ namespace spg {
 // truncation input (concatenation of <= 2 groups) at most KIN_MAX = 2*KCAP.
 // KIN_MAX bounds the shared-memory footprint of the recompression kernels:
 // R (k x k) + one 128-row sub-block (128 x k) + Jacobi (2 k^2) all fit in 227 KB.
-constexpr int KCAP = 56;
-constexpr int KIN_MAX = 2 * KCAP;   // 112
+// The library is built twice from these sources: KCAP = 56 (libspecproj_b200.so, everything in
+// shared memory) and the wide build SPG_KCAP = 80 (libspecproj_b200_w.so, namespace spgw), which
+// the first one loads and re-runs a projector on when a rank passes 56.  In the wide build R of
+// the TSQR, the general core's matrices and the reflector block of the generic Q application
+// stay in global memory / L2 (kWide): slower per column, no capacity wall at 112.
+#ifndef SPG_KCAP
+#define SPG_KCAP 56
+#endif
+constexpr int KCAP = SPG_KCAP;
+constexpr int KIN_MAX = 2 * KCAP;   // 112 (wide: 160)
+constexpr bool kWide = KIN_MAX > 112;
 constexpr int SB = 128;             // TSQR sub-block rows
 constexpr int TS_THREADS = 512;     // threads of the TSQR / apply kernels
 

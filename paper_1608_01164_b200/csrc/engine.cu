@@ -439,7 +439,7 @@ void Engine::trunc_batch(Plan& p, std::vector<TTask> tasks, Workspace& wsp, bool
         t.wsz[0] = 0;
         t.wsz[1] = ts_side_doubles(t.p, t.seg[0], t.nseg[0]);
         t.wcore = TS_HEADER + t.wsz[1] + ts_side_doubles(t.s, t.seg[1], t.nseg[1]);
-        t.ws = wsp.alloc(t.wcore + (long long)KIN_MAX * KIN_MAX);
+        t.ws = wsp.alloc(t.wcore + (long long)(kWide ? 3 : 1) * KIN_MAX * KIN_MAX);   // wide: + the general core's two matrices
         for (int side = 0; side < 2; ++side) {
             for (int s = 0; s < t.nseg[side]; ++s) it0.push_back(make_int3((int)i, side, s));
             if (t.nseg[side] > 1) itm.push_back(make_int3((int)i, side, -1));

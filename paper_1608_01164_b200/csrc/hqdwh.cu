@@ -9,6 +9,8 @@
 //   k >= 1    : Z = X X, Z = cZ + I, W = chol(Z), Y = X W^{-1}, V = Y W^{-T}
 //   every k   : X = (b/c) X + (a - b/c) V  (or M-scaled), symmetrize
 //   final     : P = (I - X) / 2
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -207,6 +209,7 @@ enum Phase { PH_SETUP, PH_FIRST, PH_MUL, PH_CHOL, PH_SOLVE, PH_SOLVET, PH_AXPBY,
 struct HqdwhState;
 void release_state(std::unique_ptr<HqdwhState> s);
 struct spg_result {
+    void* wide = nullptr;                // result of the wide-capacity library (then nothing else is set)
     std::unique_ptr<HqdwhState> state;   // engine + HODLR matrices (P, X = U) + cached graphs
     spg_info info{};
     std::vector<spg_iter_diag> diag;
@@ -939,6 +942,88 @@ int ensure_device() {
 
 }  // namespace
 
+// ---------------------------------------------------------------- rank capacity growth
+// The reference's truncate has no rank cap (lowrank.hpp:67-86).  This library holds ranks up to
+// KCAP = 56 in shared-memory-resident kernels; when a projector overflows (SPG_RANK_CAPACITY) it
+// is re-planned in the wide-capacity build of the same sources (libspecproj_b200_w.so next to
+// this library, KCAP = 80, loaded on first use) and the caller gets that result behind the same
+// handle.  SPG_NO_WIDE=1 keeps the error.
+#ifndef SPG_WIDE_BUILD
+namespace {
+struct WideApi {
+    void* lib = nullptr;
+    int (*hqdwh)(int, int, const double*, int, double, double, void**) = nullptr;
+    int (*info)(const void*, spg_info*) = nullptr;
+    int (*diag)(const void*, spg_iter_diag*) = nullptr;
+    int (*flat_size)(const void*, int, long long*) = nullptr;
+    int (*exportf)(const void*, int, int*, double*) = nullptr;
+    int (*apply)(const void*, int, int, const double*, double*) = nullptr;
+    int (*device)(const void*) = nullptr;
+    void (*freef)(void*) = nullptr;
+    const char* (*last_error)() = nullptr;
+    int (*release_cache)() = nullptr;
+    std::string why;
+};
+WideApi* wide_api() {
+    static WideApi api;
+    static std::once_flag once;
+    std::call_once(once, []() {
+        if (std::getenv("SPG_NO_WIDE")) { api.why = "SPG_NO_WIDE set"; return; }
+        Dl_info di;
+        if (!dladdr(reinterpret_cast<const void*>(&spg_last_error), &di) || !di.dli_fname) { api.why = "dladdr failed"; return; }
+        std::string path = di.dli_fname;
+        const size_t sl = path.find_last_of('/');
+        path = (sl == std::string::npos ? std::string() : path.substr(0, sl + 1)) + "libspecproj_b200_w.so";
+        void* h = dlopen(path.c_str(), RTLD_NOW | RTLD_LOCAL);
+        if (!h) { api.why = std::string("dlopen: ") + dlerror(); return; }
+        auto sym = [&](const char* n) { return dlsym(h, n); };
+        api.hqdwh = reinterpret_cast<decltype(api.hqdwh)>(sym("spg_hqdwh"));
+        api.info = reinterpret_cast<decltype(api.info)>(sym("spg_result_info"));
+        api.diag = reinterpret_cast<decltype(api.diag)>(sym("spg_result_diag"));
+        api.flat_size = reinterpret_cast<decltype(api.flat_size)>(sym("spg_result_flat_size"));
+        api.exportf = reinterpret_cast<decltype(api.exportf)>(sym("spg_result_export"));
+        api.apply = reinterpret_cast<decltype(api.apply)>(sym("spg_result_apply"));
+        api.device = reinterpret_cast<decltype(api.device)>(sym("spg_result_device"));
+        api.freef = reinterpret_cast<decltype(api.freef)>(sym("spg_result_free"));
+        api.last_error = reinterpret_cast<decltype(api.last_error)>(sym("spg_last_error"));
+        api.release_cache = reinterpret_cast<decltype(api.release_cache)>(sym("spg_release_plan_cache"));
+        if (!api.hqdwh || !api.info || !api.diag || !api.flat_size || !api.exportf || !api.apply || !api.device ||
+            !api.freef || !api.last_error) {
+            api.why = "wide library lacks an entry point";
+            dlclose(h);
+            return;
+        }
+        api.lib = h;
+    });
+    return api.lib ? &api : nullptr;
+}
+}  // namespace
+#endif
+
+// one projector with the capacity fallback (status code; *out set on success)
+static int project_with_growth(int n, int b, const double* bands, int n_min, double eps, double delta, spg_result** out) {
+    *out = nullptr;
+    int rc = guarded([&]() { *out = run_hqdwh(n, b, bands, n_min, eps, delta); });
+#ifndef SPG_WIDE_BUILD
+    if (rc == SPG_RANK_CAPACITY) {
+        WideApi* w = wide_api();
+        if (!w) return rc;
+        const std::string first = g_err;
+        void* wr = nullptr;
+        const int rc2 = w->hqdwh(n, b, bands, n_min, eps, delta, &wr);
+        if (rc2 != SPG_OK) {
+            g_err = std::string(w->last_error()) + " [wide-capacity retry after: " + first + "]";
+            return rc2;
+        }
+        auto R = std::make_unique<spg_result>();
+        R->wide = wr;
+        *out = R.release();
+        return SPG_OK;
+    }
+#endif
+    return rc;
+}
+
 // ====================================================================== C-ABI
 extern "C" {
 
@@ -953,7 +1038,26 @@ int spg_measure_dmma_tflops(double* out) {
 }
 int spg_kcap(void) { return KCAP; }
 
-int spg_release_plan_cache(void) { return drop_cached_states(); }
+int spg_release_plan_cache(void) {
+    int nfreed = drop_cached_states();
+#ifndef SPG_WIDE_BUILD
+    if (std::getenv("SPG_NO_WIDE") == nullptr) {
+        // only if the wide library is already loaded (no load just to free nothing)
+        Dl_info di;
+        if (dladdr(reinterpret_cast<const void*>(&spg_last_error), &di) && di.dli_fname) {
+            std::string path = di.dli_fname;
+            const size_t sl = path.find_last_of('/');
+            path = (sl == std::string::npos ? std::string() : path.substr(0, sl + 1)) + "libspecproj_b200_w.so";
+            if (void* h = dlopen(path.c_str(), RTLD_NOW | RTLD_LOCAL | RTLD_NOLOAD)) {
+                dlclose(h);
+                if (WideApi* w = wide_api())
+                    if (w->release_cache) nfreed += w->release_cache();
+            }
+        }
+    }
+#endif
+    return nfreed;
+}
 
 int spg_stacked_qr_r(int n, int b, const double* bands, int method, double* rdiag) {
     return guarded([&]() {
@@ -999,10 +1103,9 @@ void spg_host_free(void* p) {
 
 int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double delta, spg_result** out) {
     *out = nullptr;
-    return guarded([&]() {
-        ensure_device();
-        *out = run_hqdwh(n, b, bands, n_min, eps, delta);
-    });
+    const int rc0 = guarded([&]() { ensure_device(); });
+    if (rc0 != SPG_OK) return rc0;
+    return project_with_growth(n, b, bands, n_min, eps, delta, out);
 }
 
 // shifts over devices: `conc` worker threads per listed device pull shifts from one queue
@@ -1017,7 +1120,7 @@ static int shifts_on_devices(int n, int b, const double* bands, int nshift, cons
         for (int i = next++; i < nshift; i = next++) {
             std::vector<double> sb(bands, bands + blen);
             for (int j = 0; j < n; ++j) sb[j] -= shifts[i];   // A - mu I: the diagonal is band 0
-            st[i] = guarded([&]() { out[i] = run_hqdwh(n, b, sb.data(), n_min, eps, delta); });
+            st[i] = project_with_growth(n, b, sb.data(), n_min, eps, delta, &out[i]);
             if (st[i] != SPG_OK) msg[i] = spg_last_error();
             if (dev_of) dev_of[i] = dev;
         }
@@ -1077,21 +1180,39 @@ int spg_hqdwh_shifts_devices(int n, int b, const double* bands, int nshift, cons
     return shifts_on_devices(n, b, bands, nshift, shifts, n_min, eps, delta, devs, per_device_concurrent, out, device_of);
 }
 
-int spg_result_device(const spg_result* r) { return r && r->state ? r->state->device : -1; }
+int spg_result_device(const spg_result* r) {
+#ifndef SPG_WIDE_BUILD
+    if (r && r->wide) return wide_api()->device(r->wide);
+#endif
+    return r && r->state ? r->state->device : -1;
+}
 
 int spg_result_info(const spg_result* r, spg_info* info) {
     if (!r) return SPG_INVALID_ARGUMENT;
+#ifndef SPG_WIDE_BUILD
+    if (r->wide) return wide_api()->info(r->wide, info);
+#endif
     *info = r->info;
     return SPG_OK;
 }
 
 int spg_result_diag(const spg_result* r, spg_iter_diag* out) {
     if (!r) return SPG_INVALID_ARGUMENT;
+#ifndef SPG_WIDE_BUILD
+    if (r->wide) return wide_api()->diag(r->wide, out);
+#endif
     for (size_t i = 0; i < r->diag.size(); ++i) out[i] = r->diag[i];
     return SPG_OK;
 }
 
 int spg_result_flat_size(const spg_result* r, int which, long long* nd) {
+#ifndef SPG_WIDE_BUILD
+    if (r && r->wide) {
+        const int rc = wide_api()->flat_size(r->wide, which, nd);
+        if (rc != SPG_OK) g_err = wide_api()->last_error();
+        return rc;
+    }
+#endif
     return guarded([&]() {
         DeviceScope ds(r->state->device);
         export_flat(r->eng(), which == 0 ? r->P() : r->X(), nullptr, nullptr, nd);
@@ -1099,6 +1220,13 @@ int spg_result_flat_size(const spg_result* r, int which, long long* nd) {
 }
 
 int spg_result_export(const spg_result* r, int which, int* ranks, double* data) {
+#ifndef SPG_WIDE_BUILD
+    if (r && r->wide) {
+        const int rc = wide_api()->exportf(r->wide, which, ranks, data);
+        if (rc != SPG_OK) g_err = wide_api()->last_error();
+        return rc;
+    }
+#endif
     return guarded([&]() {
         DeviceScope ds(r->state->device);
         export_flat(r->eng(), which == 0 ? r->P() : r->X(), ranks, data, nullptr);
@@ -1106,6 +1234,13 @@ int spg_result_export(const spg_result* r, int which, int* ranks, double* data) 
 }
 
 int spg_result_apply(const spg_result* r, int which, int m, const double* X, double* Y) {
+#ifndef SPG_WIDE_BUILD
+    if (r && r->wide) {
+        const int rc = wide_api()->apply(r->wide, which, m, X, Y);
+        if (rc != SPG_OK) g_err = wide_api()->last_error();
+        return rc;
+    }
+#endif
     return guarded([&]() {
         DeviceScope ds(r->state->device);
         Engine& E = r->eng();
@@ -1142,6 +1277,9 @@ Engine& spg_result::eng() const { return *state->eng; }
 const DHodlr& spg_result::X() const { return *state->X; }
 const DHodlr& spg_result::P() const { return *state->P; }
 spg_result::~spg_result() {
+#ifndef SPG_WIDE_BUILD
+    if (wide) { wide_api()->freef(wide); wide = nullptr; }
+#endif
     if (!state) return;
     int prev = 0;
     cudaGetDevice(&prev);

@@ -82,7 +82,9 @@ __device__ __forceinline__ double* core_z(const TTask& t, double* ws, int side) 
 
 __device__ __noinline__ void core2_body(const TTask* __restrict__ tasks, double* __restrict__ ws, double eps,
                                        unsigned* status, double* smem) {
-    double* sA = smem;                       // k x k, ld KIN_MAX: C -> QR; later V_J (r' x r')
+    // wide build: both matrices live in the task's core scratch (global / L2), after gR
+    double* sA = kWide ? ws + tasks[blockIdx.x].ws + tasks[blockIdx.x].wcore + (long long)KIN_MAX * KIN_MAX
+                       : smem;               // k x k, ld KIN_MAX: C -> QR; later V_J (r' x r')
     double* sZ = sA + KIN_MAX * KIN_MAX;     // k x r', ld KIN_MAX: Z = R'^T -> W -> Zu
     __shared__ double sCn[KIN_MAX], sTau[KIN_MAX], sSig[KIN_MAX], sRed[32];
     __shared__ int sPerm[KIN_MAX], sOrd[KIN_MAX];
@@ -837,6 +839,7 @@ __device__ bool core3_body(const TTask& t, int k, double* __restrict__ ws, doubl
     return true;
 }
 
+constexpr int KM2 = KIN_MAX < 112 ? KIN_MAX : 112;   // column capacity of the second latency-optimised instance
 __global__ void __launch_bounds__(TS_THREADS, 1) k_core_any(const TTask* __restrict__ tasks, double* __restrict__ ws,
                                                         double eps, unsigned* status, int use3) {
     extern __shared__ double smem[];
@@ -848,8 +851,8 @@ __global__ void __launch_bounds__(TS_THREADS, 1) k_core_any(const TTask* __restr
             core3_body<64>(t, k, ws, eps, status, smem, cs);
             return;
         }
-        if (k > 64 && k <= KIN_MAX) {
-            if (core3_body<KIN_MAX>(t, k, ws, eps, status, smem, cs)) return;
+        if (k > 64 && k <= KM2) {
+            if (core3_body<KM2>(t, k, ws, eps, status, smem, cs)) return;
             __syncthreads();   // numerical rank beyond the Jacobi capacity: the general path, from scratch
         }
     }
@@ -861,7 +864,8 @@ constexpr size_t core3_doubles(int km) {
     return (za > ru ? za : ru) + ru;
 }
 size_t core2_smem() {
-    return sizeof(double) * std::max<size_t>({(size_t)2 * KIN_MAX * KIN_MAX, core3_doubles(64), core3_doubles(KIN_MAX)});
+    return sizeof(double) * std::max<size_t>({kWide ? (size_t)0 : (size_t)2 * KIN_MAX * KIN_MAX, core3_doubles(64),
+                                              core3_doubles(KM2)});
 }
 
 void core2_init_attributes() {

@@ -28,7 +28,12 @@ constexpr int HS_TC = 8;     // right-hand-side columns per CTA
 // W, Dinv, the coupling bases and the coupling right-hand sides are read straight
 // from global memory into DMMA fragments (each warp issues all loads of a tile
 // before its first DMMA), X of the current leaf lives in shared memory.
-constexpr int H2_THREADS = 512, H2_WARPS = 16, H2_GLD = 68;
+constexpr int h2_gld() {   // >= KCAP + 4 and = 4 (mod 32): 68 for KCAP = 56
+    int v = KCAP + 4;
+    while (v % 32 != 4) ++v;
+    return v;
+}
+constexpr int H2_THREADS = 512, H2_WARPS = 16, H2_GLD = h2_gld();
 
 __device__ __forceinline__ void dmma84(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"

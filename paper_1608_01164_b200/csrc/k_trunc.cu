@@ -289,8 +289,8 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
 __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ tasks, const int3* __restrict__ items,
                                                     double* __restrict__ ws, unsigned* status, int merge) {
     extern __shared__ double smem[];
-    double* sR = smem;                        // KIN_MAX^2
-    double* sB = sR + KIN_MAX * KIN_MAX;      // SB * KIN_MAX
+    double* sR = smem;                        // KIN_MAX^2 (wide build: R stays in the task's global R area)
+    double* sB = sR + (kWide ? 0 : KIN_MAX * KIN_MAX);   // SB * KIN_MAX
     double* sTau = sB + LDB * KIN_MAX;        // TS_TAUT: taus + panel T's
     double* sX = sTau + TS_TAUT;              // TS_XS: partial W of the split trailing tiles
     const int3 it = items[blockIdx.x];
@@ -337,8 +337,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
             for (int c = threadIdx.x >> 7; c < k; c += CPT)
                 if (in) B[(long long)c * LDB + i] *= sScl[c];
         };
-        stream_qr(k, nr, base, base + nsub * SB * KIN_MAX, base + nsub * SB * KIN_MAX + nsub * TS_TAUT, sR, sB,
-                  sTau, sX, load);
+        double* Rdst = base + nsub * SB * KIN_MAX + nsub * TS_TAUT;
+        stream_qr(k, nr, base, base + nsub * SB * KIN_MAX, Rdst, kWide ? Rdst : sR, sB, sTau, sX, load);
     } else {
         const int ns = t.nseg[side];
         if (ns <= 1) return;
@@ -363,8 +363,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
             }
             cpa_wait_all();
         };
-        stream_qr(k, mrows, mb, mb + nsubm * SB * KIN_MAX, mb + nsubm * SB * KIN_MAX + nsubm * TS_TAUT, sR, sB,
-                  sTau, sX, load);
+        double* Rdst = mb + nsubm * SB * KIN_MAX + nsubm * TS_TAUT;
+        stream_qr(k, mrows, mb, mb + nsubm * SB * KIN_MAX, Rdst, kWide ? Rdst : sR, sB, sTau, sX, load);
     }
 }
 
@@ -385,7 +385,7 @@ __device__ __forceinline__ const double* final_R(const TTask& t, double* ws, int
 // its panels; the finished rows go straight from registers to the writer.
 template <class Writer>
 __device__ void stream_apply(int k, int r, int nrows, const double* refl, const double* taut, const double* Z0,
-                             int ldz, double* sZ, double* sV, double* sTT, const Writer& write) {
+                             int ldz, double* sZ, double* sVs, double* sTT, const Writer& write) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     for (int idx = tid; idx < k * r; idx += blockDim.x) {
         const int i = idx % k, c = idx / k;
@@ -397,10 +397,12 @@ __device__ void stream_apply(int k, int r, int nrows, const double* refl, const 
     for (int b = nsub - 1; b >= 0; --b) {
         __syncthreads();
         const double* vb = refl + (long long)b * SB * KIN_MAX;
-        for (int i = tid; i < SB * k; i += blockDim.x) cpa8(sV + i, vb + i);
+        if (!kWide)
+            for (int i = tid; i < SB * k; i += blockDim.x) cpa8(sVs + i, vb + i);
         for (int i = tid; i < TS_TAUT; i += blockDim.x) cpa8(sTT + i, taut + (long long)b * TS_TAUT + i);
         cpa_wait_all();
         __syncthreads();
+        const double* sV = kWide ? vb : sVs;   // wide build: the reflector block is read from L1 / L2
         // two output columns per warp: the reflector block is read from shared memory once for
         // both, and the 2 x 8 panel dots go through two 8-value reductions (34 shuffles for two
         // columns instead of 80)
@@ -605,8 +607,8 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
                                                      double* __restrict__ ws, int merge) {
     extern __shared__ double smem[];
     double* sZ = smem;                         // KIN_MAX x KCAP
-    double* sV = sZ + KIN_MAX * KCAP;          // SB x KIN_MAX
-    double* sTT = sV + SB * KIN_MAX;           // TS_TAUT
+    double* sV = sZ + KIN_MAX * KCAP;          // SB x KIN_MAX (not staged in the wide build)
+    double* sTT = sV + (kWide ? 0 : SB * KIN_MAX);   // TS_TAUT
     const int3 it = items[blockIdx.x];
     const TTask& t = tasks[it.x];
     const int side = it.y;
@@ -673,9 +675,9 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
 }
 
 // ------------------------------------------------------------------ host side
-size_t trunc_smem_tsqr() { return sizeof(double) * (KIN_MAX * KIN_MAX + LDB * KIN_MAX + TS_TAUT + TS_XS); }
+size_t trunc_smem_tsqr() { return sizeof(double) * ((kWide ? 0 : KIN_MAX * KIN_MAX) + LDB * KIN_MAX + TS_TAUT + TS_XS); }
 size_t trunc_smem_apply() {
-    return std::max(sizeof(double) * (KIN_MAX * KCAP + SB * KIN_MAX + TS_TAUT), apply_dmma_smem());
+    return std::max(sizeof(double) * (KIN_MAX * KCAP + (kWide ? 0 : SB * KIN_MAX) + TS_TAUT), apply_dmma_smem());
 }
 
 void trunc_init_attributes() {

@@ -4,6 +4,7 @@ when it was built).  Tolerances follow north_star: ||P - P_ref||_2 <= 100*eps,
 round(trace P) = nu, ||P^2 - P||_2 <= 100*eps."""
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -535,3 +536,71 @@ def test_baseline_config_vs_reference_dense(reflib, cfg):
     assert nd <= 100 * eps, nd
     assert ni <= 100 * eps, ni
     assert round(np.trace(Pg)) == n // 2
+
+
+# ------------------------------------------------------------------ rank capacity growth
+def test_rank_overflow_replans_in_wide_library(reflib, root):
+    """Ranks above the shared-memory capacity (56): the projector is re-planned in the wide-capacity
+    build (KCAP = 80) instead of failing, as the reference's uncapped truncate (lowrank.hpp:67-86)
+    would simply continue.  Banded b = 8, t2 = 0.999, eps = 1e-14: an intermediate product reaches
+    rank 58.  Compared densely with the reference; SPG_NO_WIDE=1 keeps the capacity error."""
+    n, b, nmin, eps = 4096, 8, 128, 1e-14
+    A = S.dimer_chain(n, 1.0, 0.999, 0.0, 1, b=b, s=0.05 / (2 * b + 1))
+    r = S.hqdwh(A, nmin, eps)
+    assert r.info["kcap"] == 80 and S.load_library().spg_kcap() == 56     # the wide library produced it
+    ref = reflib.hqdwh(A.bands, nmin, eps)
+    assert r.iterations == ref["iterations"]
+    assert [d.max_rank for d in r.per_iteration] == [int(x) for x in ref["diag"][:, 3]]
+    Pg = r.P.to_dense()
+    Pr = reflib.to_dense(ref["P"], n)
+    reflib.L.ref_result_free(ref["handle"])
+    X = np.random.default_rng(3).standard_normal((n, 5))
+    np.testing.assert_allclose(r.apply(X), Pg @ X, atol=1e-11)            # device apply behind the forwarded handle
+    r.close()
+    assert np.linalg.norm(Pg - Pr, 2) <= 1e-10
+    assert round(np.trace(Pg)) == int(round(np.trace(Pr)))
+    code = ("import paper_1608_01164_b200 as S\n"
+            f"A = S.dimer_chain({n}, 1.0, 0.999, 0.0, 1, b={b}, s=0.05 / (2 * {b} + 1))\n"
+            "try:\n"
+            f"    S.hqdwh(A, {nmin}, {eps})\n"
+            "    print('no error')\n"
+            "except S.RankCapacityError as e:\n"
+            "    print('RankCapacityError', e)\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=root,
+                         env={**os.environ, "SPG_NO_WIDE": "1"})
+    assert "RankCapacityError" in out.stdout and "KCAP=56" in out.stdout, out.stdout + out.stderr
+
+
+def test_wide_library_passes_the_parity_tests(root):
+    """The wide-capacity build (R of the TSQR, the general core's matrices and the generic Q
+    application's reflector block in global memory) is the same arithmetic in another memory
+    plan: it runs the truncation KATs, the op-level parity tests, the goldens, the small-gap
+    config and the determinism test on its own (SPG_LIB selects the library)."""
+    sel = ("truncate_kats or truncate_contract or truncate_vs_reference or ops_vs_restatement or ops_identity_kats "
+           "or hqdwh_vs_golden or smallgap_config or test_deterministic or edge_cases or error_propagation")
+    out = subprocess.run([sys.executable, "-m", "pytest", os.path.join(root, "tests", "test_gpu_parity.py"), "-m", "gpu",
+                          "-q", "-x", "-k", sel, "-p", "no:cacheprovider"], capture_output=True, text=True, timeout=1500,
+                         cwd=root, env={**os.environ, "SPG_LIB": S.WIDE_LIB_PATH})
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    import re
+    m = re.search(r"(\d+) passed", out.stdout)
+    assert m and int(m.group(1)) >= 20 and "failed" not in out.stdout, out.stdout[-1500:]
+    # and a truncation only it can hold: 150 input columns (general core, matrices in global memory),
+    # rank 70 out, against numpy (truncate's contract: error <= eps per dropped direction)
+    code = ("import numpy as np, paper_1608_01164_b200 as S\n"
+            "print(S.load_library().spg_kcap())\n"
+            "g = np.random.default_rng(5)\n"
+            "for p, s, k, r in ((500, 300, 150, 70), (1000, 4000, 130, 64), (257, 129, 113, 40)):\n"
+            "    Q1 = np.linalg.qr(g.standard_normal((p, r)))[0]; Q2 = np.linalg.qr(g.standard_normal((s, r)))[0]\n"
+            "    sig = np.logspace(0, -6, r)\n"
+            "    B = (Q1 * sig) @ Q2.T\n"
+            "    M = g.standard_normal((r, k))\n"
+            "    U = (Q1 * sig) @ M; V = Q2 @ np.linalg.pinv(M).T\n"
+            "    Uo, Vo = S.truncate(U, V, 1e-10)\n"
+            "    print(Uo.shape[1], np.linalg.norm(Uo @ Vo.T - B, 2))\n")
+    chk = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=root,
+                         env={**os.environ, "SPG_LIB": S.WIDE_LIB_PATH})
+    lines = chk.stdout.split()
+    assert lines and lines[0] == "80", chk.stdout + chk.stderr
+    vals = [(int(lines[i]), float(lines[i + 1])) for i in range(1, len(lines), 2)]
+    assert [v[0] for v in vals] == [70, 64, 40] and all(v[1] < 1e-9 for v in vals), chk.stdout + chk.stderr
