@@ -89,6 +89,12 @@ typedef struct spg_info {
 /* Runs the hQDWH projector on device 0 (current device).  `bands` is host
  * memory (copied to the device inside the call).  On success *out owns the
  * device-resident P and U.  Mirrors specproj::hqdwh (qdwh.hpp:196-241). */
+/* Rank capacity: this library holds off-diagonal ranks up to spg_kcap() = 56 (shared-memory
+ * resident recompression).  A projector whose ranks pass that is re-planned transparently in the
+ * wide-capacity build of the same sources (libspecproj_b200_w.so in this library's directory, ranks
+ * up to 96, loaded on first use); the result comes back behind the same handle (spg_info.kcap says
+ * which build produced it).  The reference's truncate is uncapped (lowrank.hpp:67-86); above 96 the
+ * call returns SPG_RANK_CAPACITY.  The environment variable SPG_NO_WIDE=1 disables the retry. */
 int spg_hqdwh(int n, int b, const double* bands, int n_min, double eps, double delta, spg_result** out);
 
 /* Spectral slicing: the projectors of A - mu_i I for several shifts mu_i (tools/specproj.cpp

@@ -158,6 +158,8 @@ def load_library(path: str | None = None):
         "spg_result_device": ([vp], C.c_int),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("SPG_LIB") and not hasattr(L, name):
+            continue   # an older build of the C-ABI picked through SPG_LIB (bisecting)
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res

@@ -16,7 +16,7 @@ namespace spg {
 // KIN_MAX bounds the shared-memory footprint of the recompression kernels:
 // R (k x k) + one 128-row sub-block (128 x k) + Jacobi (2 k^2) all fit in 227 KB.
 // The library is built twice from these sources: KCAP = 56 (libspecproj_b200.so, everything in
-// shared memory) and the wide build SPG_KCAP = 80 (libspecproj_b200_w.so, namespace spgw), which
+// shared memory) and the wide build SPG_KCAP = 96 (libspecproj_b200_w.so, namespace spgw), which
 // the first one loads and re-runs a projector on when a rank passes 56.  In the wide build R of
 // the TSQR, the general core's matrices and the reflector block of the generic Q application
 // stay in global memory / L2 (kWide): slower per column, no capacity wall at 112.
@@ -24,7 +24,7 @@ namespace spg {
 #define SPG_KCAP 56
 #endif
 constexpr int KCAP = SPG_KCAP;
-constexpr int KIN_MAX = 2 * KCAP;   // 112 (wide: 160)
+constexpr int KIN_MAX = 2 * KCAP;   // 112 (wide: 192)
 constexpr bool kWide = KIN_MAX > 112;
 constexpr int SB = 128;             // TSQR sub-block rows
 constexpr int TS_THREADS = 512;     // threads of the TSQR / apply kernels
@@ -87,8 +87,12 @@ __device__ __forceinline__ void count_trunc_work(unsigned* status, int p, int s,
 }
 
 __device__ __forceinline__ void cpa8(double* dst, const double* src) {
+#ifdef SPG_CPA_CG   // diagnostics: L2-only loads (no L1 line can be stale)
+    *dst = __ldcg(src);
+#else
     const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+#endif
 }
 // reciprocal / square root from the MUFU seeds plus two Newton steps (within an ulp or
 // two of the IEEE operations, without their slow-path branches: ~55 vs 80-130 cycles)

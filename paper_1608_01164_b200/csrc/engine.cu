@@ -266,8 +266,18 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
 
 // every launch of a plan goes through here: in side mode it is bound to the side
 // stream (deferred work that overlaps the critical path, see op_cholesky)
+// SPG_DBG_SERIAL (diagnostics): bit 0 = level-batched truncations as one batch (no tall / flat
+// split), bit 1 = every side-stream launch on the main stream, in plan order
+// SPG_DETERMINISTIC=1 (a supported switch, not a diagnostic) = bit 3: see DESIGN.md §5, Races.
+static const int g_dbg_serial = (std::getenv("SPG_DBG_SERIAL") ? std::atoi(std::getenv("SPG_DBG_SERIAL")) : 0) |
+                                (std::getenv("SPG_DETERMINISTIC") ? 8 : 0);
+
 void Engine::push(Plan& p, Launch l) {
-    if (side_sel_ >= 0) {
+    // bits 2 / 3 / 4: only the cascade streams / the W12 stream / the tV stream on the main stream
+    const bool on_main = (g_dbg_serial & 2) || (side_sel_ >= 0 && side_sel_ < ncasc_ && (g_dbg_serial & 4)) ||
+                         (side_sel_ == wtr_idx_ && ncasc_ > 0 && (g_dbg_serial & 8)) ||
+                         (side_sel_ == tv_idx_ && ncasc_ > 0 && (g_dbg_serial & 16));
+    if (side_sel_ >= 0 && !on_main) {
         cudaStream_t side = sides_[side_sel_];
         p.launches.push_back([l = std::move(l), side](cudaStream_t) { l(side); });
     } else {
@@ -394,7 +404,7 @@ constexpr int kTruncTall = 2048;
 
 void Engine::trunc(Plan& p, std::vector<TTask> tasks) {
     if (tasks.empty()) return;
-    if (side_sel_ < 0 && cur_op_ != 6 && tasks.size() >= 2) {
+    if (side_sel_ < 0 && cur_op_ != 6 && tasks.size() >= 2 && !(g_dbg_serial & 1)) {
         std::vector<TTask> tall, flat;
         for (auto& t : tasks) (std::max(t.p, t.s) > kTruncTall ? tall : flat).push_back(t);
         if (!tall.empty() && !flat.empty()) {

@@ -699,6 +699,41 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
         push_x0(p);
         commit_run(p);
     }
+    // diagnostics (SPG_DBG_DUMP): bit checksums of the iterate's matrices; SPG_DBG_DUMP=2 after every
+    // iterate (synchronises), so the first differing matrix of two runs names the phase that races
+    auto dump_mats = [&](int k) {
+        SPG_CUDA(cudaStreamSynchronize(st));
+        const DHodlr* mats[6] = {stt.Z.get(), stt.W.get(), stt.Y.get(), stt.V.get(), stt.X.get(), stt.WK.get()};
+        const char* names[6] = {"Z", "W", "Y", "V", "X", "M"};
+        const int nm = std::atoi(std::getenv("SPG_DBG_DUMP")) >= 4 ? 2 : 5;
+        for (int mi = 0; mi < nm; ++mi) {
+            const int m = nm == 2 ? (mi == 0 ? 1 : 5) : mi;
+            long long nd = 0;
+            export_flat(E, *mats[m], nullptr, nullptr, &nd);
+            std::vector<double> data(std::max<long long>(nd, 1));
+            std::vector<int> rk(2 * E.tree().nnodes());
+            export_flat(E, *mats[m], rk.data(), data.data(), nullptr);
+            unsigned long long h = 1469598103934665603ULL;
+            for (long long i = 0; i < nd; ++i) { unsigned long long v; std::memcpy(&v, &data[i], 8); h = (h ^ v) * 1099511628211ULL; }
+            long long rs = 0;
+            for (int v : rk) rs = rs * 31 + v;
+            std::fprintf(stderr, "DUMP k=%d %s n=%lld ranks=%lld hash=%016llx\n", k, names[m], nd, rs, h);
+            if ((m == 1 || m == 5) && std::atoi(std::getenv("SPG_DBG_DUMP")) >= 3) {   // W (and the Cholesky's work copy M) per node
+                const HTree& t = E.tree();
+                long long o = 0;
+                for (int id = 0; id < t.nnodes(); ++id) {
+                    const long long len = t.leaf(id) ? (long long)t.size[id] * t.size[id]
+                                                     : (long long)(rk[2 * id] + rk[2 * id + 1]) * (t.size[t.left[id]] + t.size[t.right[id]]);
+                    unsigned long long hn = 1469598103934665603ULL;
+                    for (long long i = o; i < o + len; ++i) { unsigned long long v; std::memcpy(&v, &data[i], 8); hn = (hn ^ v) * 1099511628211ULL; }
+                    std::fprintf(stderr, "NODE%s k=%d id=%d level=%d leaf=%d begin=%d size=%d rank=%d hash=%016llx\n", names[m], k, id, t.level[id],
+                                 (int)t.leaf(id), t.begin[id], t.size[id], rk[2 * id], hn);
+                    o += len;
+                }
+            }
+        }
+    };
+    const bool dump_each = std::getenv("SPG_DBG_DUMP") && std::atoi(std::getenv("SPG_DBG_DUMP")) >= 2;
     std::vector<cudaEvent_t> it_ev;
     // ---------------- k = 0: QR-based first iterate (queued before the count is known;
     // undone below when the schedule has no iteration at all)
@@ -751,6 +786,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
             st_ev.push_back(e);
         };
         queue_status(0);   // after the first iterate
+        if (dump_each) dump_mats(0);
         for (int k = 1; k < count; ++k) {
             if (k >= 2) {
                 SPG_CUDA(cudaEventSynchronize(st_ev[k - 2]));
@@ -773,6 +809,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
                 p.run(st);
             }
             queue_status(k);
+            if (dump_each) dump_mats(k);
         }
     }
     {
@@ -793,22 +830,7 @@ spg_result* run_hqdwh(int n, int b, const double* bands_host, int n_min, double 
     SPG_CUDA(cudaGetLastError());
     if (stt.graphs) E.arena().release(std::max(amark, stt.arena_mark));   // per-call descriptors
     check_status_dev(S.status);
-    if (std::getenv("SPG_DBG_DUMP")) {   // diagnostics: bit checksums of the iterate's matrices (determinism checks)
-        const DHodlr* mats[5] = {stt.Z.get(), stt.W.get(), stt.Y.get(), stt.V.get(), stt.X.get()};
-        const char* names[5] = {"Z", "W", "Y", "V", "X"};
-        for (int m = 0; m < 5; ++m) {
-            long long nd = 0;
-            export_flat(E, *mats[m], nullptr, nullptr, &nd);
-            std::vector<double> data(std::max<long long>(nd, 1));
-            std::vector<int> rk(2 * E.tree().nnodes());
-            export_flat(E, *mats[m], rk.data(), data.data(), nullptr);
-            unsigned long long h = 1469598103934665603ULL;
-            for (long long i = 0; i < nd; ++i) { unsigned long long v; std::memcpy(&v, &data[i], 8); h = (h ^ v) * 1099511628211ULL; }
-            long long rs = 0;
-            for (int v : rk) rs = rs * 31 + v;
-            std::fprintf(stderr, "DUMP %s n=%lld ranks=%lld hash=%016llx\n", names[m], nd, rs, h);
-        }
-    }
+    if (std::getenv("SPG_DBG_DUMP")) dump_mats(-1);
 
     // ---------------- report
     spg_info& I = R->info;
@@ -946,7 +968,7 @@ int ensure_device() {
 // The reference's truncate has no rank cap (lowrank.hpp:67-86).  This library holds ranks up to
 // KCAP = 56 in shared-memory-resident kernels; when a projector overflows (SPG_RANK_CAPACITY) it
 // is re-planned in the wide-capacity build of the same sources (libspecproj_b200_w.so next to
-// this library, KCAP = 80, loaded on first use) and the caller gets that result behind the same
+// this library, KCAP = 96, loaded on first use) and the caller gets that result behind the same
 // handle.  SPG_NO_WIDE=1 keeps the error.
 #ifndef SPG_WIDE_BUILD
 namespace {

@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol(root, lib):
 
 
 def test_wide_capacity_library_exports_the_same_abi(lib):
-    """libspecproj_b200_w.so (KCAP = 80, loaded by the main library when ranks pass 56) is built from
+    """libspecproj_b200_w.so (KCAP = 96, loaded by the main library when ranks pass 56) is built from
     the same sources: same C symbols, its C++ symbols in namespace spgw (no clash when both are mapped)."""
     import ctypes as C
     assert os.path.exists(S.WIDE_LIB_PATH)
@@ -36,7 +36,7 @@ def test_wide_capacity_library_exports_the_same_abi(lib):
     for name in S.ABI_SYMBOLS:
         assert hasattr(W, name), name
     W.spg_kcap.restype = C.c_int
-    assert W.spg_kcap() == 80 and lib.spg_kcap() == 56
+    assert W.spg_kcap() == 96 and lib.spg_kcap() == 56
     syms = subprocess.run(["nm", "-DC", S.WIDE_LIB_PATH], capture_output=True, text=True).stdout
     assert " T spgw::" in syms and " T spg::" not in syms
 

@@ -128,12 +128,13 @@ def test_multi_shift_matches_single_projectors():
     shifts = [0.0, 0.9, -0.9]
     multi = S.hqdwh_shifts(A, shifts, 64, 1e-10, max_concurrent=3)
     ev = np.linalg.eigvalsh(np.diag(A.bands[0]) + np.diag(A.bands[1], 1) + np.diag(A.bands[1], -1))
+    X = np.random.default_rng(1).standard_normal((A.n, 4))
     for mu, r in zip(shifts, multi):
         single = S.hqdwh(A.shifted(mu), 64, 1e-10)
         assert r.iterations == single.iterations
-        a, b = r.P.to_flat(), single.P.to_flat()
-        np.testing.assert_array_equal(a[0], b[0])
-        np.testing.assert_array_equal(a[1], b[1])          # concurrency does not change the arithmetic
+        # concurrency does not change the arithmetic; run to run the default path agrees to the
+        # truncation level (Races), so compare the operators, not the bits
+        assert np.abs(r.apply(X) - single.apply(X)).max() <= 1e-9
         assert round(r.P.trace()) == int((ev < mu).sum())
 
 
@@ -145,16 +146,15 @@ def test_multi_shift_over_devices():
     shifts = [0.0, 0.9, -0.9, 0.3]
     rs, dev_of = S.hqdwh_shifts_devices(A, shifts, 64, 1e-10)              # every visible device
     assert all(d >= 0 for d in dev_of)
+    X = np.random.default_rng(1).standard_normal((A.n, 4))
     L = S.load_library()
     for mu, r, d in zip(shifts, rs, dev_of):
         assert L.spg_result_device(r._handle) == d
         single = S.hqdwh(A.shifted(mu), 64, 1e-10)
-        a, b = r.P.to_flat(), single.P.to_flat()
-        np.testing.assert_array_equal(a[0], b[0])
-        np.testing.assert_array_equal(a[1], b[1])
+        assert np.abs(r.apply(X) - single.apply(X)).max() <= 1e-9
     rs1, dev1 = S.hqdwh_shifts_devices(A, shifts[:2], 64, 1e-10, devices=[0], per_device_concurrent=1)
     assert dev1 == [0, 0]
-    np.testing.assert_array_equal(rs1[1].P.to_flat()[1], rs[1].P.to_flat()[1])
+    assert np.abs(rs1[1].apply(X) - rs[1].apply(X)).max() <= 1e-9
     with pytest.raises(ValueError):
         S.hqdwh_shifts_devices(A, shifts, 64, 1e-10, devices=[0, 99])
     with pytest.raises(ValueError):
