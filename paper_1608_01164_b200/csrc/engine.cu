@@ -470,6 +470,13 @@ void Engine::trunc_batch(Plan& p, std::vector<TTask> tasks, Workspace& wsp, bool
         prof_rows_ = 0;
         for (const auto& t : tasks) prof_rows_ = std::max(prof_rows_, std::max(t.p, t.s));
     }
+    static const bool poison = std::getenv("SPG_DBG_POISON") != nullptr;
+    if (poison) {   // diagnostics: the batch's workspace region starts as NaN on its own stream
+        const long long lo = mark, hi = wsp.mark();
+        push(p, [ws, lo, hi](cudaStream_t st) {
+            SPG_CUDA(cudaMemsetAsync(ws + lo, 0xFF, sizeof(double) * (size_t)(hi - lo), st));
+        });
+    }
     push_timed(p, PC_TRUNC, [b, ws, eps, status](cudaStream_t st) { launch_truncate(b, ws, eps, status, st); });
     if (release) wsp.release(mark);
 }

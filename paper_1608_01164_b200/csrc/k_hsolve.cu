@@ -277,9 +277,10 @@ __global__ void __launch_bounds__(H2_THREADS) k_hsolve2(DevTree t, DevHodlrView 
             for (int mt = warp; mt < (nout + 7) / 8; mt += H2_WARPS) {
                 const int row = 8 * mt + gi;
                 const bool rv = row < nout;
-                double a[14];
+                constexpr int KST = (KCAP + 3) / 4;   // k-steps of the widest coupling (14 for KCAP = 56)
+                double a[KST];
 #pragma unroll
-                for (int u = 0; u < 14; ++u) {
+                for (int u = 0; u < KST; ++u) {
                     const int aa = 4 * u + gk;
                     a[u] = (u < kst && rv && aa < k) ? -Pout[row + aa * ldp] : 0.0;
                 }
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(H2_THREADS) k_hsolve2(DevTree t, DevHodlrView 
                 double c0 = cv0 ? x0[0] : 0.0;
                 double c1 = cv1 ? x0[ldx] : 0.0;
 #pragma unroll
-                for (int u = 0; u < 14; ++u)
+                for (int u = 0; u < KST; ++u)
                     if (u < kst) dmma84(c0, c1, a[u], sG[(4 * u + gk) + gi * H2_GLD]);
                 if (cv0) x0[0] = c0;
                 if (cv1) x0[ldx] = c1;

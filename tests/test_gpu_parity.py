@@ -579,13 +579,16 @@ def test_baseline_config_vs_reference_dense(reflib, cfg):
 
 
 # ------------------------------------------------------------------ rank capacity growth
-def test_rank_overflow_replans_in_wide_library(reflib, root):
+@pytest.mark.parametrize("b,t2", [(8, 0.999), (16, 0.99)])
+def test_rank_overflow_replans_in_wide_library(reflib, root, b, t2):
     """Ranks above the shared-memory capacity (56): the projector is re-planned in the wide-capacity
     build (KCAP = 96) instead of failing, as the reference's uncapped truncate (lowrank.hpp:67-86)
     would simply continue.  Banded b = 8, t2 = 0.999, eps = 1e-14: an intermediate product reaches
     rank 58.  Compared densely with the reference; SPG_NO_WIDE=1 keeps the capacity error."""
-    n, b, nmin, eps = 4096, 8, 128, 1e-14
-    A = S.dimer_chain(n, 1.0, 0.999, 0.0, 1, b=b, s=0.05 / (2 * b + 1))
+    # b = 8: an intermediate product reaches rank 58; b = 16: the iterates themselves reach rank 58, so
+    # the Cholesky factor's couplings and every solve run with more than 56 columns
+    n, nmin, eps = 4096, 128, 1e-14
+    A = S.dimer_chain(n, 1.0, t2, 0.0, 1, b=b, s=0.05 / (2 * b + 1))
     r = S.hqdwh(A, nmin, eps)
     assert r.info["kcap"] == 96 and S.load_library().spg_kcap() == 56     # the wide library produced it
     ref = reflib.hqdwh(A.bands, nmin, eps)
@@ -600,7 +603,7 @@ def test_rank_overflow_replans_in_wide_library(reflib, root):
     assert np.linalg.norm(Pg - Pr, 2) <= 1e-10
     assert round(np.trace(Pg)) == int(round(np.trace(Pr)))
     code = ("import paper_1608_01164_b200 as S\n"
-            f"A = S.dimer_chain({n}, 1.0, 0.999, 0.0, 1, b={b}, s=0.05 / (2 * {b} + 1))\n"
+            f"A = S.dimer_chain({n}, 1.0, {t2}, 0.0, 1, b={b}, s=0.05 / (2 * {b} + 1))\n"
             "try:\n"
             f"    S.hqdwh(A, {nmin}, {eps})\n"
             "    print('no error')\n"

@@ -3,8 +3,7 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1608_01164_b200 as S
-for n, b, t2, nmin, eps in [(4096, 4, 0.99, 128, 1e-12), (4096, 8, 0.95, 128, 1e-12), (4096, 8, 0.99, 128, 1e-13),
-                            (8192, 16, 0.95, 256, 1e-12), (8192, 4, 0.999, 256, 1e-14), (4096, 8, 0.999, 128, 1e-14)]:
+for n, b, t2, nmin, eps in [(8192, 4, 0.999, 256, 1e-14), (4096, 4, 0.999, 128, 1e-14), (4096, 8, 0.999, 128, 1e-15), (4096, 16, 0.99, 128, 1e-14), (4096, 8, 0.9995, 128, 1e-14)]:
     A = S.dimer_chain(n, 1.0, t2, 0.0, 1, b=b, s=0.05 / (2 * b + 1)) if b > 1 else S.dimer_chain(n, 1.0, t2, 0.0, 1)
     t0 = time.time()
     try:
