@@ -1074,6 +1074,23 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
         }
     }
     wtr_last_ev_ = -1;
+    if (std::getenv("SPG_DBG_POISON")) {   // diagnostics: the Cholesky's scratch starts as NaN (a premature read
+        // would otherwise see the previous call's, nearly equal, values)
+        const size_t pan = sizeof(double) * (size_t)tree_.n * KCAP;
+        std::vector<double*> xs = xpanels_, cs = chol_panels_;
+        double* cf = coef_;
+        double* pc = pcoef_;
+        const size_t ncf = sizeof(double) * (size_t)KCAP * KCAP * 4 * tree_.nnodes(), npc = ncf / 4;
+        double* tu = W.tU;
+        const size_t ntu = sizeof(double) * 2 * W.slab_doubles;
+        push(p, [=](cudaStream_t st) {
+            for (double* q : xs) SPG_CUDA(cudaMemsetAsync(q, 0xFF, pan, st));
+            for (double* q : cs) SPG_CUDA(cudaMemsetAsync(q, 0xFF, pan, st));
+            SPG_CUDA(cudaMemsetAsync(cf, 0xFF, ncf, st));
+            SPG_CUDA(cudaMemsetAsync(pc, 0xFF, npc, st));
+            if (tu) SPG_CUDA(cudaMemsetAsync(tu, 0xFF, ntu, st));
+        });
+    }
     op_copy(p, M, work);
     const DHodlr* Wp = &W;
     push(p, [Wp](cudaStream_t st) { Wp->zero(st); });
