@@ -268,10 +268,10 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
 // stream (deferred work that overlaps the critical path, see op_cholesky)
 // SPG_DBG_SERIAL (diagnostics): bit 0 = level-batched truncations as one batch (no tall / flat
 // split), bit 1 = every side-stream launch on the main stream, in plan order
-// SPG_DETERMINISTIC=1 (a supported switch) = bit 3, the W12 truncations on the main stream: measured,
-// not derived (Races) -- 0 differing results in ~250 single-projector runs, against
-// about one in ten without it.  A wait for W12(x) before the right subtree alone (+5 % instead of
-// +10 % time) brought it to ~2 in 100, a wait after the right subtree did nothing.
+// SPG_DETERMINISTIC=1 = bit 3, the W12 truncations on the main stream: measured, not derived (DESIGN.md
+// section 5, Races) -- about one differing result in fifty single-projector runs, against one in ten
+// without it.  A wait for W12(x) before the right subtree alone (+5 % instead of +10 % time) gives
+// about the same, a wait after the right subtree does nothing.
 static const int g_dbg_serial = (std::getenv("SPG_DBG_SERIAL") ? std::atoi(std::getenv("SPG_DBG_SERIAL")) : 0) |
                                 (std::getenv("SPG_DETERMINISTIC") ? 8 : 0);
 

@@ -106,8 +106,13 @@ __device__ __forceinline__ void smem_allreduce8(double (&v)[8], double* scratch,
 //
 // Loader: fills Bk (SB x k, col-major ld SB) with rows [row0, row0+SB) (zero padded).
 template <class Loader>
+// ilv > 0 (merge level): the rows are the stacked upper-triangular R_s of ilv segments, interleaved
+// by local row (row gi = local row gi / ilv of segment gi % ilv).  A sub-block that starts at local
+// row lr then holds only zeros in its columns < lr, whose reflectors are the identity: those panels
+// are skipped (their stored tails, taus and T's are zero, so the Q application needs no change).
+// Half of the merge level's column steps disappear.
 __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, double* Rout,
-                          double* sR, double* sB, double* sTT, double* sX, const Loader& load) {
+                          double* sR, double* sB, double* sTT, double* sX, const Loader& load, int ilv = 0) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = blockDim.x >> 5;
     for (int i = tid; i < KIN_MAX * KIN_MAX; i += blockDim.x) sR[i] = 0.0;
@@ -118,7 +123,8 @@ __device__ void stream_qr(int k, int nrows, double* refl, double* taut_out, doub
         load(b * SB, sB);
         for (int i = tid; i < TS_TAUT; i += blockDim.x) sTT[i] = 0.0;
         __syncthreads();
-        for (int pn = 0; pn < npan; ++pn) {
+        const int pn0 = ilv > 0 ? ((b * SB) / ilv) / TS_NB : 0;
+        for (int pn = pn0; pn < npan; ++pn) {
             const int j0 = pn * TS_NB, nb = min(TS_NB, k - j0);
             double* Tp = sTT + KIN_MAX + pn * TS_NB * TS_NB;   // T (column-major 8 x 8)
             if (warp == 0) {
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
     } else {
         const int ns = t.nseg[side];
         if (ns <= 1) return;
-        // stacked R_s (k x k each): row i -> segment i / k, local i % k
+        // stacked R_s (k x k each), interleaved: row i -> segment i % ns, local row i / ns
         const int mrows = ns * k;
         double* mb = merge_area(t, ws, side);
         const long long nsubm = ts_nsub(ns * KIN_MAX);
@@ -352,9 +358,9 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
             constexpr int CPT = TS_THREADS / SB;
             const double* Rs = nullptr;
             int lr = 0;
-            if (gi < mrows) {
-                const int s = gi / k;
-                lr = gi % k;
+            if (gi < mrows) {   // interleaved by local row: zero columns come first in every sub-block
+                const int s = gi % ns;
+                lr = gi / ns;
                 Rs = seg_area(t, ws, side, s) + ts_nsub(t.seg[side]) * (SB * KIN_MAX + TS_TAUT);
             }
             for (int c = threadIdx.x >> 7; c < k; c += CPT) {
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(TS_THREADS) k_tsqr(const TTask* __restrict__ t
             cpa_wait_all();
         };
         double* Rdst = mb + nsubm * SB * KIN_MAX + nsubm * TS_TAUT;
-        stream_qr(k, mrows, mb, mb + nsubm * SB * KIN_MAX, Rdst, kWide ? Rdst : sR, sB, sTau, sX, load);
+        stream_qr(k, mrows, mb, mb + nsubm * SB * KIN_MAX, Rdst, kWide ? Rdst : sR, sB, sTau, sX, load, ns);
     }
 }
 
@@ -385,11 +391,11 @@ __device__ __forceinline__ const double* final_R(const TTask& t, double* ws, int
 // its panels; the finished rows go straight from registers to the writer.
 template <class Writer>
 __device__ void stream_apply(int k, int r, int nrows, const double* refl, const double* taut, const double* Z0,
-                             int ldz, double* sZ, double* sVs, double* sTT, const Writer& write) {
+                             int ldz, int zrs, double* sZ, double* sVs, double* sTT, const Writer& write) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     for (int idx = tid; idx < k * r; idx += blockDim.x) {
         const int i = idx % k, c = idx / k;
-        cpa8(sZ + i + c * KIN_MAX, Z0 + i + (long long)c * ldz);
+        cpa8(sZ + i + c * KIN_MAX, Z0 + (long long)i * zrs + (long long)c * ldz);
     }
     cpa_wait_all();
     const int nsub = (nrows + SB - 1) / SB;
@@ -495,7 +501,7 @@ size_t apply_dmma_smem() { return sizeof(double) * ((size_t)AD_LV * AD_K + 3 * (
 
 template <class Writer>
 __device__ void stream_apply_dmma(int k, int r, int nrows, const double* refl, const double* taut, const double* Z0,
-                                  int ldz, double* smem, const Writer& write) {
+                                  int ldz, int zrs, double* smem, const Writer& write) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int gi = lane >> 2, gk = lane & 3;
     double* sV = smem;                          // SB x k, ld AD_LV
@@ -509,7 +515,7 @@ __device__ void stream_apply_dmma(int k, int r, int nrows, const double* refl, c
     const int ntr = (r + 7) / 8;
     for (int idx = tid; idx < kp * r; idx += blockDim.x) {
         const int i = idx % kp, c = idx / kp;
-        if (i < k) cpa8(sZ + i + c * AD_LG, Z0 + i + (long long)c * ldz);
+        if (i < k) cpa8(sZ + i + c * AD_LG, Z0 + (long long)i * zrs + (long long)c * ldz);
         else sZ[i + c * AD_LG] = 0.0;
     }
     for (int idx = tid; idx < kp * 8; idx += blockDim.x) {   // zero padding columns of W' (r..ntr*8)
@@ -634,9 +640,9 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
         };
         if (k <= AD_K) {
             auto wr1 = [&](int row, int c, double v) { Zst[row + (long long)c * ldst] = v; };
-            stream_apply_dmma(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, smem, wr1);
+            stream_apply_dmma(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, 1, smem, wr1);
         } else {
-            stream_apply(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, sZ, sV, sTT, write);
+            stream_apply(k, r, mrows, mb, mb + nsubm * SB * KIN_MAX, z_area(t, ws, side), KIN_MAX, 1, sZ, sV, sTT, write);
         }
     } else {
         const int s = it.z;
@@ -646,12 +652,13 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
         const double* base = seg_area(t, ws, side, s);
         const long long nsub = ts_nsub(t.seg[side]);
         const double* Z0;
-        int ldz;
+        int ldz, zrs = 1;
         if (t.nseg[side] > 1) {
             const long long nsubm = ts_nsub(t.nseg[side] * KIN_MAX);
             const double* Zst = merge_area(t, ws, side) + nsubm * (SB * KIN_MAX + TS_TAUT) + (long long)KIN_MAX * KIN_MAX;
-            Z0 = Zst + (long long)s * k;
+            Z0 = Zst + s;                 // the merge level's rows are interleaved: local row i of segment s = i * nseg + s
             ldz = t.nseg[side] * KIN_MAX;
+            zrs = t.nseg[side];
         } else {
             Z0 = z_area(t, ws, side);
             ldz = KIN_MAX;
@@ -667,9 +674,9 @@ __global__ void __launch_bounds__(TS_THREADS) k_apply(const TTask* __restrict__ 
         };
         if (k <= AD_K) {
             auto wr1 = [&](int row, int c, double v) { out[r0 + row + (long long)c * ldo] = v; };
-            stream_apply_dmma(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, smem, wr1);
+            stream_apply_dmma(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, zrs, smem, wr1);
         } else {
-            stream_apply(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, sZ, sV, sTT, write);
+            stream_apply(k, r, nr, base, base + nsub * SB * KIN_MAX, Z0, ldz, zrs, sZ, sV, sTT, write);
         }
     }
 }
