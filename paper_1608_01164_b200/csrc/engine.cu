@@ -173,6 +173,51 @@ void dbg_delay(Plan& p, int cls, const std::function<void(Plan&, Launch)>& pushe
     pusher(p, [](cudaStream_t st) { k_dbg_sleep<<<1, 1, 0, st>>>(us * 1000); });
 }
 
+// ---- hash log (race diagnostics)
+__global__ void k_hash_region(const double* ptr, int rows, int cols, int ld, const int* rankp, unsigned long long* out) {
+    __shared__ unsigned long long sh[256];
+    const int k = rankp ? min(cols, *rankp) : cols;
+    unsigned long long acc = 0;
+    for (long long idx = threadIdx.x; idx < (long long)rows * k; idx += blockDim.x) {
+        const int i = (int)(idx % rows), c = (int)(idx / rows);
+        unsigned long long v = (unsigned long long)__double_as_longlong(ptr[i + (long long)c * ld]);
+        v ^= (unsigned long long)(idx + 1) * 0x9E3779B97F4A7C15ULL;
+        v ^= v >> 29; v *= 0xBF58476D1CE4E5B9ULL; v ^= v >> 32;
+        acc += v;   // a sum: independent of the order the threads run in
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = (unsigned long long)k * 0x100000001B3ULL;
+        for (int i = 0; i < 256; ++i) t += sh[i];
+        *out = t;
+    }
+}
+static const bool g_hashlog = std::getenv("SPG_DBG_HASHLOG") != nullptr;
+constexpr size_t kHashSlots = size_t(1) << 18;
+
+void Engine::hash_region(Plan& p, const char* tag, int node, const double* ptr, int rows, int cols, int ld,
+                         const int* rankp) {
+    if (!g_hashlog) return;
+    if (!hashlog_) SPG_CUDA(dev_malloc(&hashlog_, sizeof(unsigned long long) * kHashSlots));
+    if (hashtags_.size() >= kHashSlots) return;
+    unsigned long long* out = hashlog_ + hashtags_.size();
+    hashtags_.push_back(std::string(tag) + " node " + std::to_string(node));
+    push(p, [=](cudaStream_t st) { k_hash_region<<<1, 256, 0, st>>>(ptr, rows, cols, ld, rankp, out); });
+}
+
+void Engine::dump_hashlog(cudaStream_t st) {
+    if (!g_hashlog || hashtags_.empty()) return;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    SPG_CUDA(cudaStreamIsCapturing(st, &cap));
+    if (cap != cudaStreamCaptureStatusNone) { hashtags_.clear(); return; }   // graph capture: no host reads
+    std::vector<unsigned long long> h(hashtags_.size());
+    SPG_CUDA(cudaMemcpyAsync(h.data(), hashlog_, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
+    SPG_CUDA(cudaStreamSynchronize(st));
+    for (size_t i = 0; i < h.size(); ++i) std::fprintf(stderr, "HL %zu %s %016llx\n", i, hashtags_[i].c_str(), h[i]);
+    hashtags_.clear();
+}
+
 struct RankOp { int* out; const int* a; const int* b; };
 __global__ void k_rank_op(const RankOp* ops, int nops) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1119,6 +1164,7 @@ void Engine::op_cholesky(Plan& p, const DHodlr& M, DHodlr& W, DHodlr& work, bool
     }
     if (chol_tv_) W.tready = false;   // tU is not built here (op_solve_prep rebuilds both)
     chol_tv_ = false;
+    if (g_hashlog) push(p, [this](cudaStream_t st) { dump_hashlog(st); });
 }
 
 // deferred Schur cascade of node x into the subtree `root` = r(x): the leaf updates
@@ -1174,6 +1220,10 @@ void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU,
         if (chol_defer_trunc_) wait(p, ev_base2_ + nn + x);
         dbg_delay(p, 2, [this](Plan& pp, Launch l) { push(pp, std::move(l)); });
         trunc(p, bylev[d]);
+        for (int y : nodes[d]) {
+            hash_region(p, "cascU", y, M.upU(y), tree_.size[tree_.left[y]], KCAP, tree_.n, M.rup(y));
+            hash_region(p, "cascV", y, M.upV(y), tree_.size[tree_.right[y]], KCAP, tree_.n, M.rup(y));
+        }
         const int ev = nn * (2 + d) + x;
         record(p, ev);
         for (int y : nodes[d]) last_block_ev_[y] = ev;
@@ -1216,7 +1266,9 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
         std::vector<CholItem> ci{CholItem{M.leaf(x), W.leaf(x), s, s, s, W.leaf_dinv(x), 1}};   // W memset above
         const CholItem* d = arena_->push(ci);
         unsigned* status = sc_.status;
+        hash_region(p, "Mleaf", x, M.leaf(x), s, s, s, nullptr);
         push_timed(p, PC_LEAF, [d, status, s](cudaStream_t st) { launch_leaf_cholesky(d, 1, status, st, s); });
+        hash_region(p, "Wleaf", x, W.leaf(x), s, s, s, nullptr);
         if (s > 576) {   // the large-leaf Cholesky path does not produce the block inverses itself
             const DinvItem* di = arena_->push(std::vector<DinvItem>{DinvItem{W.leaf(x), W.leaf_dinv(x), s, s}});
             push_timed(p, PC_LEAF, [di, status](cudaStream_t st) { launch_leaf_dinv(di, 1, status, st); });
@@ -1245,6 +1297,8 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
             W.tready = tr;
         }
         const int evx = ev_base2_ + x, evw = ev_base2_ + tree_.nnodes() + x;
+        hash_region(p, "X", x, X + bl, s1, KCAP, n, M.rup(x));
+        hash_region(p, "m12V", x, M.upV(x), s2, KCAP, n, M.rup(x));
         record(p, evx);
         {   // W12 = trunc(X, m12.V) on its own stream (lowrank.hpp:67-86)
             side_sel_ = wtr_idx_;
@@ -1255,6 +1309,8 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
             tk.g[0] = TGroup{X + bl, M.upV(x), n, n, M.rup(x), 0, 1.0, nullptr};
             tk.ou = W.upU(x); tk.ov = W.upV(x); tk.ldou = tk.ldov = n; tk.orank = W.rup(x); tk.tag = 600000 + x;
             trunc(p, {tk});
+            hash_region(p, "W12U", x, W.upU(x), s1, KCAP, n, W.rup(x));
+            hash_region(p, "W12V", x, W.upV(x), s2, KCAP, n, W.rup(x));
             record(p, evw);
             side_sel_ = -1;
             wtr_last_ev_ = evw;
@@ -1266,6 +1322,8 @@ void Engine::chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W) {
              {make_int3(KCAP, KCAP, s1)});
         gemm(p, {gitem(M.upV(x), n, 0, G, KCAP, 0, P1 + br, n, s2, nullptr, 0, M.rup(x), 0, M.rup(x), 1.0, 0.0)},
              {make_int3(s2, KCAP, KCAP)});
+        hash_region(p, "G", x, G, KCAP, KCAP, KCAP, M.rup(x));
+        hash_region(p, "P1", x, P1 + br, s2, KCAP, n, M.rup(x));
         record(p, x);
         cascade_chol(p, M, x, r, P1, M.slabV(t), M.rup(x));
         chol_rec(p, r, M, W);

@@ -207,8 +207,17 @@ public:
     void push(Plan& p, Launch l);
     void record(Plan& p, int e);   // event slot e
     void wait(Plan& p, int e);
+    // Race diagnostics (SPG_DBG_HASHLOG=1): an order-independent checksum of a just-written region,
+    // computed by a small kernel queued on the stream of the current mode, into the next log slot.
+    // The log of a run (dump_hashlog) names, in plan order, every intermediate result of the
+    // H-Cholesky; the first slot that differs between two runs is where they part.
+    void hash_region(Plan& p, const char* tag, int node, const double* ptr, int rows, int cols, int ld,
+                     const int* rankp);
+    void dump_hashlog(cudaStream_t st);
 
 private:
+    unsigned long long* hashlog_ = nullptr;
+    std::vector<std::string> hashtags_;
     void chol_rec(Plan& p, int x, DHodlr& M, DHodlr& W);
     void sur_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y);
     void surt_rec(Plan& p, int x, DHodlr& B, const DHodlr& W, DHodlr& Y);
