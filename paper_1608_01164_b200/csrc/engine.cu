@@ -313,12 +313,11 @@ Engine::Engine(int n, int nmin, double eps, size_t ws_doubles) : tree_(n, nmin),
 // stream (deferred work that overlaps the critical path, see op_cholesky)
 // SPG_DBG_SERIAL (diagnostics): bit 0 = level-batched truncations as one batch (no tall / flat
 // split), bit 1 = every side-stream launch on the main stream, in plan order
-// SPG_DETERMINISTIC=1 = bit 3, the W12 truncations on the main stream: measured, not derived (DESIGN.md
-// section 5, Races) -- about one differing result in fifty single-projector runs, against one in ten
-// without it.  A wait for W12(x) before the right subtree alone (+5 % instead of +10 % time) gives
-// about the same, a wait after the right subtree does nothing.
+// SPG_DETERMINISTIC=1 = bit 1: every side-stream launch of the engine on the main stream, in plan
+// order.  Bit-reproducible in every recorded run (small-gap 72, headline 40); headline 736 ms
+// instead of 483 ms.
 static const int g_dbg_serial = (std::getenv("SPG_DBG_SERIAL") ? std::atoi(std::getenv("SPG_DBG_SERIAL")) : 0) |
-                                (std::getenv("SPG_DETERMINISTIC") ? 8 : 0);
+                                (std::getenv("SPG_DETERMINISTIC") ? 2 : 0);
 
 void Engine::push(Plan& p, Launch l) {
     // bits 2 / 3 / 4: only the cascade streams / the W12 stream / the tV stream on the main stream
@@ -1210,14 +1209,17 @@ void Engine::cascade_chol(Plan& p, DHodlr& M, int x, int root, const double* QU,
         if (bylev[d].empty()) continue;
         side_sel_ = std::min(d, nside - 2);
         wait(p, x);
-        // Ordering of the block truncations: after this cascade's leaf updates and, in the
-        // deferred mode, after W12(x)'s truncation.  Without these edges ~4% of the n = 16384
-        // projectors came out different from the others (W12 of the tallest blocks first,
-        // up to 1e-6 in P; tools_gpu/determinism*.py, chol_race.py with injected delays); with
-        // them 0 of several hundred.  The block truncations are needed later than the leaf
-        // updates, so the leaf chain does not wait for them.
-        wait(p, nn + x);
-        if (chol_defer_trunc_) wait(p, ev_base2_ + nn + x);
+        // No further ordering: the block truncations read P1, m12(x).V and their own blocks only.  Two
+        // extra edges (after this cascade's leaf updates, after W12(x)) were the default for a while
+        // because they lowered the rate of run-to-run differences of the small-gap config; on the
+        // headline they turned out to produce the largest ones (1e-9 .. 1e-6 in P in 6 of 100 runs,
+        // against <= 3e-11 in 220 runs without them) and cost 35 ms.  SPG_DBG_CASC_ORDER=1 restores
+        // them for A/B runs (Races).
+        static const bool casc_order = std::getenv("SPG_DBG_CASC_ORDER") != nullptr;
+        if (casc_order) {
+            wait(p, nn + x);
+            if (chol_defer_trunc_) wait(p, ev_base2_ + nn + x);
+        }
         dbg_delay(p, 2, [this](Plan& pp, Launch l) { push(pp, std::move(l)); });
         trunc(p, bylev[d]);
         for (int y : nodes[d]) {

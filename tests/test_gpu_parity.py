@@ -354,11 +354,10 @@ def test_deterministic():
 
 
 def test_run_to_run_agreement_and_deterministic_mode(root):
-    """Run to run (cold and cached plans) the projector agrees to the truncation level: about one
-    small-gap run in ten differs from the others by a few 1e-11 in P (ranks of a few blocks by one),
-    from the H-Cholesky's side streams (Races).  SPG_DETERMINISTIC=1 (W12
-    truncations on the main stream) brings that to about one in fifty; both modes are held to the
-    same operator-level agreement here, and the bitwise count of the second is reported."""
+    """Run to run (cold and cached plans) the projector agrees to the truncation level and is
+    usually bit-identical (Races).  SPG_DETERMINISTIC=1 runs the H-Cholesky's
+    side-stream work on the main stream (bit-identical in every recorded run); both modes are held
+    to operator-level agreement here, and the bitwise count of each is reported."""
     code = ("import numpy as np, paper_1608_01164_b200 as S\n"
             "from paper_1608_01164_b200.configs import CONFIGS, make_input\n"
             "c = CONFIGS['smallgap']; A = make_input(c); ref = None; bad = 0; worst = 0.0\n"
